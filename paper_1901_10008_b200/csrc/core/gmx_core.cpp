@@ -1,0 +1,1126 @@
+// gmx_core.cpp — the coalescing decision core behind include/gmx_core.h.
+//
+// Re-implements the decision path of the reference `gpumux` (pure Python)
+// as a native, allocation-light state machine:
+//   cost model      kernels.py:45-69,202-222   device.py:130-150
+//   coalescer       coalesce.py:56-131
+//   scheduler       scheduler.py:137-471 (all five policy variants)
+// Decisions are bit-exact against the reference (see pyexact.hpp for the two
+// Python-semantics traps); a C2-size step (16 kernels) costs a few
+// microseconds instead of the reference's 1.6 ms, n=512 well under 100 us.
+//
+// Build: g++ -O2 -std=c++17 -ffp-contract=off -fPIC -shared (no -ffast-math).
+
+#include "../../../include/gmx_core.h"
+#include "pyexact.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <new>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+namespace gmx {
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+static const int64_t kNoDeadline = (int64_t)1 << 62;  // kernels.py:25
+static const int kArity[3] = {1, 3, 2};              // elementwise, gemm, gemv
+static const int64_t kDtypeBytes[2] = {2, 4};         // fp16, fp32
+
+// ---------------------------------------------------------------- cost model
+
+static int check_dims(int32_t op, const int64_t* dims, int32_t nd) {
+    if (op < 0 || op > 2) return fail(GMX_EINVAL, "unknown op_kind");
+    if (nd != kArity[op]) return fail(GMX_EINVAL, "wrong number of dims for op_kind");
+    for (int i = 0; i < nd; ++i)
+        if (dims[i] < 1) return fail(GMX_EINVAL, "all dims must be >= 1");
+    return GMX_OK;
+}
+
+static bool mul_ok(int64_t a, int64_t b, int64_t* out) { return !__builtin_mul_overflow(a, b, out); }
+
+// kernels.py:45-54
+static int flops_of(int32_t op, const int64_t* d, int64_t* out) {
+    int64_t t;
+    if (op == GMX_OP_GEMM) {
+        if (!mul_ok(2, d[0], &t) || !mul_ok(t, d[1], &t) || !mul_ok(t, d[2], &t))
+            return fail(GMX_EOVERFLOW, "flop count overflows int64");
+    } else if (op == GMX_OP_GEMV) {
+        if (!mul_ok(2, d[0], &t) || !mul_ok(t, d[1], &t))
+            return fail(GMX_EOVERFLOW, "flop count overflows int64");
+    } else {
+        t = d[0];
+    }
+    *out = t;
+    return GMX_OK;
+}
+
+// kernels.py:57-69
+static int bytes_of(int32_t op, const int64_t* d, int32_t dtype, int64_t* out) {
+    if (dtype < 0 || dtype > 1) return fail(GMX_EINVAL, "unknown dtype");
+    int64_t e, a, b, c;
+    bool ok = true;
+    if (op == GMX_OP_GEMM) {
+        ok = mul_ok(d[0], d[2], &a) && mul_ok(d[2], d[1], &b) && mul_ok(d[0], d[1], &c) &&
+             !__builtin_add_overflow(a, b, &e) && !__builtin_add_overflow(e, c, &e);
+    } else if (op == GMX_OP_GEMV) {
+        ok = mul_ok(d[0], d[1], &a) && !__builtin_add_overflow(a, d[1], &e) &&
+             !__builtin_add_overflow(e, d[0], &e);
+    } else {
+        ok = mul_ok(2, d[0], &e);
+    }
+    if (!ok || !mul_ok(e, kDtypeBytes[dtype], &e))
+        return fail(GMX_EOVERFLOW, "byte count overflows int64");
+    *out = e;
+    return GMX_OK;
+}
+
+// kernels.py:202-213: ceil over a (correctly rounded) float quotient.
+static int64_t ceil_ratio(int64_t a, int64_t b) { return py_ceil(true_div(a, b)); }
+
+static int blocks_of(int32_t op, const int64_t* d, int64_t tm, int64_t tn, int64_t* out) {
+    if (tm < 1 || tn < 1) return fail(GMX_EINVAL, "tile dims must be >= 1");
+    int64_t r;
+    if (op == GMX_OP_GEMM) {
+        if (!mul_ok(ceil_ratio(d[0], std::min(tm, d[0])), ceil_ratio(d[1], std::min(tn, d[1])), &r))
+            return fail(GMX_EOVERFLOW, "block count overflows int64");
+    } else if (op == GMX_OP_GEMV) {
+        r = ceil_ratio(d[0], std::min(tm, d[0]));
+    } else {
+        int64_t area;
+        if (!mul_ok(tm, tn, &area)) return fail(GMX_EOVERFLOW, "tile area overflows");
+        r = ceil_ratio(d[0], std::min(area, d[0]));
+    }
+    *out = r;
+    return GMX_OK;
+}
+
+// device.py:130-137
+static int occupancy(const gmx_profile* p, int64_t blocks, double factor, double* out) {
+    if (blocks < 1) return fail(GMX_EINVAL, "block_count must be >= 1");
+    if (!(factor > 0.0 && factor <= 1.0)) return fail(GMX_EINVAL, "tuning_efficiency_factor must be in (0, 1]");
+    int64_t cap;
+    if (!mul_ok(p->sm_count, p->blocks_per_sm, &cap)) return fail(GMX_EOVERFLOW, "capacity overflow");
+    const double ratio = true_div(blocks, cap);
+    *out = (ratio < 1.0 ? ratio : 1.0) * factor;
+    return GMX_OK;
+}
+
+// device.py:140-150
+static int roofline(const gmx_profile* p, int64_t flops, int64_t nbytes, double eff, int32_t path,
+                    int64_t* out) {
+    if (!(eff > 0.0 && eff <= 1.0)) return fail(GMX_EINVAL, "efficiency must be in (0, 1]");
+    if (flops < 0 || nbytes < 0) return fail(GMX_EINVAL, "flops and bytes must be non-negative");
+    if (path != GMX_PATH_DENSE && path != GMX_PATH_SCALAR) return fail(GMX_EINVAL, "unknown throughput path");
+    const double peak = path == GMX_PATH_DENSE ? p->peak_flops_dense : p->peak_flops_scalar;
+    const int64_t c = flops ? py_ceil((double)flops / (peak * eff) * 1e9) : 0;
+    const int64_t m = nbytes ? py_ceil((double)nbytes / p->mem_bandwidth * 1e9) : 0;
+    *out = c > m ? c : m;
+    return GMX_OK;
+}
+
+static int32_t path_of(int32_t dtype) { return dtype == GMX_DT_FP16 ? GMX_PATH_DENSE : GMX_PATH_SCALAR; }
+
+static const gmx_tuning_config kDefaultConfig = {64, 64, 1.0, 1.0};  // tuning.py:48-49
+
+// kernels.py:216-222
+static int kernel_cost(const gmx_profile* p, int32_t op, int32_t dtype, const int64_t* dims,
+                       const gmx_tuning_config& cfg, gmx_cost* out) {
+    int rc;
+    gmx_cost c;
+    if ((rc = flops_of(op, dims, &c.flops)) || (rc = bytes_of(op, dims, dtype, &c.bytes)) ||
+        (rc = blocks_of(op, dims, cfg.tile_m, cfg.tile_n, &c.block_count)) ||
+        (rc = occupancy(p, c.block_count, cfg.efficiency_factor, &c.efficiency)) ||
+        (rc = roofline(p, c.flops, c.bytes, c.efficiency, path_of(dtype), &c.duration)))
+        return rc;
+    *out = c;
+    return GMX_OK;
+}
+
+// ---------------------------------------------------------------- tuning table
+
+struct ShapeKey {
+    int32_t op, dtype;
+    int64_t d[3];
+    bool operator==(const ShapeKey& o) const {
+        return op == o.op && dtype == o.dtype && d[0] == o.d[0] && d[1] == o.d[1] && d[2] == o.d[2];
+    }
+};
+struct ShapeKeyHash {
+    size_t operator()(const ShapeKey& k) const {
+        uint64_t h = (uint64_t)k.op * 0x9E3779B97F4A7C15ull ^ (uint64_t)k.dtype;
+        for (int i = 0; i < 3; ++i) h = (h ^ (uint64_t)k.d[i]) * 0x100000001B3ull;
+        return (size_t)h;
+    }
+};
+
+static ShapeKey make_key(int32_t op, int32_t dtype, const int64_t* dims, int nd) {
+    ShapeKey k{op, dtype, {0, 0, 0}};
+    for (int i = 0; i < nd; ++i) k.d[i] = dims[i];
+    return k;
+}
+
+}  // namespace gmx
+
+struct gmx_tuning_table {
+    // key -> (tenancy -> config), tenancy levels ordered
+    std::unordered_map<gmx::ShapeKey, std::map<int64_t, gmx_tuning_config>, gmx::ShapeKeyHash> entries;
+
+    // tuning.py:147-160: clamp tenancy to the key's tuned maximum; miss -> default
+    const gmx_tuning_config& lookup(const gmx::ShapeKey& k, int64_t tenancy, bool* found) const {
+        *found = false;
+        auto it = entries.find(k);
+        if (it == entries.end() || it->second.empty()) return gmx::kDefaultConfig;
+        const int64_t top = it->second.rbegin()->first;
+        if (top == 0) return gmx::kDefaultConfig;
+        auto jt = it->second.find(std::min(tenancy, top));
+        if (jt == it->second.end()) return gmx::kDefaultConfig;
+        *found = true;
+        return jt->second;
+    }
+};
+
+namespace gmx {
+
+static const gmx_tuning_config& table_lookup(const gmx_tuning_table* t, const ShapeKey& k,
+                                             int64_t tenancy) {
+    if (!t) return kDefaultConfig;
+    bool found;
+    return t->lookup(k, tenancy, &found);
+}
+
+// coalesce.py:109-123
+static int superkernel_cost(const gmx_profile* p, const gmx_tuning_table* t, int32_t op,
+                            int32_t dtype, const int64_t* padded, int nd, int64_t batch,
+                            int64_t tenancy, gmx_cost* out) {
+    const gmx_tuning_config& cfg = table_lookup(t, make_key(op, dtype, padded, nd), tenancy);
+    int64_t per_blocks, f, b;
+    int rc;
+    if ((rc = blocks_of(op, padded, cfg.tile_m, cfg.tile_n, &per_blocks)) ||
+        (rc = flops_of(op, padded, &f)) || (rc = bytes_of(op, padded, dtype, &b)))
+        return rc;
+    gmx_cost c;
+    if (!mul_ok(batch, per_blocks, &c.block_count) || !mul_ok(batch, f, &c.flops) ||
+        !mul_ok(batch, b, &c.bytes))
+        return fail(GMX_EOVERFLOW, "superkernel cost overflows int64");
+    if ((rc = occupancy(p, c.block_count, cfg.efficiency_factor, &c.efficiency)) ||
+        (rc = roofline(p, c.flops, c.bytes, c.efficiency, path_of(dtype), &c.duration)))
+        return rc;
+    *out = c;
+    return GMX_OK;
+}
+
+// ---------------------------------------------------------------- coalescer
+
+// The coalescer works over a flat array of shape records (one per pending
+// kernel) so that both the stateless ABI and the scheduler can use it.
+struct ShapeRec {
+    int64_t id;
+    int32_t op, dtype, nd;
+    int64_t dims[3];
+    int64_t flops;
+    int32_t src;  // caller's index
+};
+
+struct Cluster {
+    int32_t op, dtype, nd;
+    int64_t padded[3];
+    int32_t begin, end;  // range in the member-order array
+    double waste;
+};
+
+// 1 - sum / (count * padded_flops), the division correctly rounded.
+static double waste_ratio(u128 sum, int64_t count, int64_t padded_flops) {
+    const u128 den = (u128)count * (u128)padded_flops;
+    return 1.0 - true_div(sum, den);
+}
+
+// coalesce.py:69-106. `order` receives member indices (into recs) grouped by
+// cluster in admission order.
+static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vector<int32_t>& order,
+                          std::vector<Cluster>& clusters) {
+    if (!(budget >= 0.0 && budget < 1.0)) return fail(GMX_EINVAL, "pad_budget must be in [0, 1)");
+    const int32_t n = (int32_t)recs.size();
+    std::vector<int32_t> idx(n);
+    for (int32_t i = 0; i < n; ++i) idx[i] = i;
+    std::sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) {
+        const ShapeRec &a = recs[x], &b = recs[y];
+        if (a.op != b.op) return a.op < b.op;
+        if (a.dtype != b.dtype) return a.dtype < b.dtype;
+        for (int i = 0; i < a.nd; ++i)  // dims descending
+            if (a.dims[i] != b.dims[i]) return a.dims[i] > b.dims[i];
+        return a.id < b.id;
+    });
+    std::vector<char> taken(n, 0);
+    order.clear();
+    clusters.clear();
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t s = idx[i];
+        if (taken[s]) continue;
+        taken[s] = 1;
+        const ShapeRec& seed = recs[s];
+        Cluster c{seed.op, seed.dtype, seed.nd, {seed.dims[0], seed.dims[1], seed.dims[2]},
+                  (int32_t)order.size(), 0, 0.0};
+        order.push_back(s);
+        u128 sum = (u128)seed.flops;
+        int64_t count = 1, pf = seed.flops;
+        // kernels of one op/dtype are contiguous in sort order
+        for (int32_t j = i + 1; j < n; ++j) {
+            const int32_t q = idx[j];
+            const ShapeRec& cand = recs[q];
+            if (cand.op != seed.op || cand.dtype != seed.dtype) break;
+            if (taken[q]) continue;
+            int64_t grown[3] = {0, 0, 0};
+            for (int d = 0; d < seed.nd; ++d) grown[d] = std::max(c.padded[d], cand.dims[d]);
+            int64_t gf;
+            int rc = flops_of(seed.op, grown, &gf);
+            if (rc) return rc;
+            if (waste_ratio(sum + (u128)cand.flops, count + 1, gf) <= budget) {
+                order.push_back(q);
+                taken[q] = 1;
+                sum += (u128)cand.flops;
+                ++count;
+                pf = gf;
+                std::memcpy(c.padded, grown, sizeof grown);
+            }
+        }
+        c.end = (int32_t)order.size();
+        c.waste = waste_ratio(sum, count, pf);
+        clusters.push_back(c);
+    }
+    return GMX_OK;
+}
+
+// ---------------------------------------------------------------- scheduler
+
+struct KernelRec {
+    int64_t id;
+    int32_t stream, op, dtype, nd;
+    int64_t dims[3];
+    int64_t arrival, deadline, flops, bytes, predicted;
+    int32_t req, pos;
+    int32_t ready_pos = -1;   // index in Sched::ready, -1 if not ready
+    bool blocked = false, done = false;
+    std::vector<int64_t> waiting;  // pending dependency ids while blocked
+};
+
+struct RequestRec {
+    int64_t id;
+    int32_t stream;
+    int64_t arrival;
+    std::vector<int32_t> kernels;  // kernel slots in request order (empty if refused)
+    std::vector<int64_t> kernel_ids;
+    int64_t remaining;
+    bool evicted = false, finished = false;
+};
+
+struct DispatchRec {
+    gmx_dispatch_rec rec;
+    std::vector<int32_t> kernels;   // slots
+    std::vector<int32_t> streams;   // sorted by name, unique
+};
+
+}  // namespace gmx
+
+struct gmx_sched {
+    gmx_profile prof;
+    int32_t policy;
+    gmx_policy_params params;
+    gmx_tuning_table table;
+    bool has_table = false;
+    double fp_base, fp_slope;
+    gmx::SplitMix64 rng;
+
+    std::vector<std::string> stream_names;
+    std::unordered_map<std::string, int32_t> stream_ids;
+    std::vector<char> evicted_stream;
+
+    std::vector<gmx::KernelRec> kernels;
+    std::unordered_map<int64_t, int32_t> kernel_slot;
+    std::vector<gmx::RequestRec> requests;
+    std::unordered_map<int64_t, int32_t> request_slot;
+    std::vector<int32_t> ready;                 // kernel slots
+    std::map<int64_t, gmx::DispatchRec> in_flight;  // ordered == insertion order
+    int64_t free_sms;
+    int64_t dispatch_seq = 0;
+    bool has_last_ctx = false;
+    std::string last_ctx;
+    int32_t rr_last = -1;
+    std::set<std::vector<int64_t>> withheld_sigs;
+
+    // view storage
+    std::vector<gmx_dispatch_rec> v_disp;
+    std::vector<int64_t> v_disp_kids, v_held_kids, v_ids_a, v_ids_b, v_ids_c;
+    std::vector<int32_t> v_held_off;
+    // scratch
+    std::vector<gmx::ShapeRec> s_recs;
+    std::vector<int32_t> s_order;
+    std::vector<gmx::Cluster> s_clusters;
+
+    const gmx_tuning_table* tbl() const { return has_table ? &table : nullptr; }
+    bool stream_less(int32_t a, int32_t b) const { return stream_names[a] < stream_names[b]; }
+};
+
+namespace gmx {
+
+using S = gmx_sched;
+
+static const gmx_tuning_config& solo_config(const S* s, const KernelRec& k) {
+    return table_lookup(s->tbl(), make_key(k.op, k.dtype, k.dims, k.nd), 1);
+}
+
+static void ready_add(S* s, int32_t slot) {
+    KernelRec& k = s->kernels[slot];
+    if (k.ready_pos >= 0) return;
+    k.ready_pos = (int32_t)s->ready.size();
+    s->ready.push_back(slot);
+}
+
+static void ready_remove(S* s, int32_t slot) {
+    KernelRec& k = s->kernels[slot];
+    if (k.ready_pos < 0) return;
+    const int32_t last = s->ready.back();
+    s->ready[k.ready_pos] = last;
+    s->kernels[last].ready_pos = k.ready_pos;
+    s->ready.pop_back();
+    k.ready_pos = -1;
+}
+
+// scheduler.py:195-203
+static int64_t predicted_remaining(const S* s, const KernelRec& k) {
+    const RequestRec& r = s->requests[k.req];
+    int64_t total = 0;
+    for (size_t i = (size_t)k.pos; i < r.kernels.size(); ++i) {
+        const KernelRec& succ = s->kernels[r.kernels[i]];
+        if (!succ.done) total += succ.predicted;
+    }
+    return total;
+}
+
+static int64_t kernel_slack(const S* s, const KernelRec& k, int64_t now) {
+    return k.deadline - now - predicted_remaining(s, k);
+}
+
+static int64_t slo_of(const S* s, const KernelRec& k) { return k.deadline - s->requests[k.req].arrival; }
+
+// scheduler.py:331-333
+static void live_ready(const S* s, std::vector<int32_t>& out) {
+    out.clear();
+    for (int32_t slot : s->ready)
+        if (!s->evicted_stream[s->kernels[slot].stream]) out.push_back(slot);
+}
+
+// scheduler.py:282-286 (sorted by name, evicted removed)
+static void active_streams(const S* s, std::vector<int32_t>& out) {
+    std::vector<char> seen(s->stream_names.size(), 0);
+    for (int32_t slot : s->ready) seen[s->kernels[slot].stream] = 1;
+    for (const auto& kv : s->in_flight)
+        for (int32_t st : kv.second.streams) seen[st] = 1;
+    out.clear();
+    for (size_t i = 0; i < seen.size(); ++i)
+        if (seen[i] && !s->evicted_stream[i]) out.push_back((int32_t)i);
+    std::sort(out.begin(), out.end(), [s](int32_t a, int32_t b) { return s->stream_less(a, b); });
+}
+
+// scheduler.py:288-292
+static double noise_factor(S* s) {
+    const double w = s->params.duration_noise;
+    if (w <= 0) return 1.0;
+    return 1.0 + s->rng.uniform(-w, w);
+}
+
+// scheduler.py:294-316
+static void make_dispatch(S* s, const std::vector<int32_t>& members, int64_t now, int64_t duration,
+                          int64_t predicted, int64_t alloc, int32_t context, const std::string& ctx_name,
+                          bool ctx_switch, bool is_super, int64_t useful, int64_t padded, bool infeasible) {
+    DispatchRec d;
+    d.rec.dispatch_id = ++s->dispatch_seq;
+    d.rec.start = now + (ctx_switch ? s->prof.context_switch_cost : 0);
+    d.rec.end = d.rec.start + duration;
+    d.rec.useful_flops = useful;
+    d.rec.padded_flops = padded;
+    d.rec.predicted_duration = predicted;
+    d.rec.duration = duration;
+    d.rec.sm_allocation = (int32_t)alloc;
+    d.rec.context = context;
+    d.rec.ctx_switch = ctx_switch;
+    d.rec.infeasible = infeasible;
+    d.rec.is_super = is_super;
+    d.rec.kernel_offset = (int32_t)s->v_disp_kids.size();
+    d.rec.n_kernels = (int32_t)members.size();
+    d.rec._pad = 0;
+    d.kernels = members;
+    for (int32_t slot : members) {
+        s->v_disp_kids.push_back(s->kernels[slot].id);
+        d.streams.push_back(s->kernels[slot].stream);
+        ready_remove(s, slot);
+    }
+    std::sort(d.streams.begin(), d.streams.end(), [s](int32_t a, int32_t b) { return s->stream_less(a, b); });
+    d.streams.erase(std::unique(d.streams.begin(), d.streams.end()), d.streams.end());
+    s->v_disp.push_back(d.rec);
+    s->free_sms -= alloc;
+    s->has_last_ctx = true;
+    s->last_ctx = ctx_name;
+    s->in_flight.emplace(d.rec.dispatch_id, std::move(d));
+}
+
+static int64_t useful_of(const S* s, const std::vector<int32_t>& members) {
+    int64_t u = 0;
+    for (int32_t slot : members) u += s->kernels[slot].flops;
+    return u;
+}
+
+static int solo_duration(const S* s, const KernelRec& k, int64_t* out) {
+    gmx_cost c;
+    int rc = kernel_cost(&s->prof, k.op, k.dtype, k.dims, solo_config(s, k), &c);
+    if (rc) return rc;
+    *out = c.duration;
+    return GMX_OK;
+}
+
+// scheduler.py:335-347
+static int step_serial(S* s, int64_t now, bool by_deadline) {
+    std::vector<int32_t> live;
+    live_ready(s, live);
+    if (!s->in_flight.empty() || live.empty()) return GMX_OK;
+    int32_t best = live[0];
+    for (int32_t slot : live) {
+        const KernelRec &a = s->kernels[slot], &b = s->kernels[best];
+        const int64_t ka = by_deadline ? a.deadline : a.arrival, kb = by_deadline ? b.deadline : b.arrival;
+        if (ka < kb || (ka == kb && a.id < b.id)) best = slot;
+    }
+    const KernelRec& k = s->kernels[best];
+    int64_t pred;
+    int rc = solo_duration(s, k, &pred);
+    if (rc) return rc;
+    const int64_t dur = py_ceil((double)pred * noise_factor(s));
+    const bool inf = kernel_slack(s, k, now) < 0;
+    make_dispatch(s, {best}, now, dur, pred, s->prof.sm_count, k.stream, s->stream_names[k.stream],
+                  false, false, k.flops, k.flops, inf);
+    return GMX_OK;
+}
+
+static int32_t earliest_arrival(const S* s, const std::vector<int32_t>& live, int32_t stream) {
+    int32_t best = -1;
+    for (int32_t slot : live) {
+        const KernelRec& a = s->kernels[slot];
+        if (a.stream != stream) continue;
+        if (best < 0) { best = slot; continue; }
+        const KernelRec& b = s->kernels[best];
+        if (a.arrival < b.arrival || (a.arrival == b.arrival && a.id < b.id)) best = slot;
+    }
+    return best;
+}
+
+// scheduler.py:349-370
+static int step_time_mux(S* s, int64_t now) {
+    if (!s->in_flight.empty()) return GMX_OK;
+    std::vector<int32_t> live;
+    live_ready(s, live);
+    std::vector<int32_t> streams;
+    for (int32_t slot : live) streams.push_back(s->kernels[slot].stream);
+    if (streams.empty()) return GMX_OK;
+    std::sort(streams.begin(), streams.end(), [s](int32_t a, int32_t b) { return s->stream_less(a, b); });
+    streams.erase(std::unique(streams.begin(), streams.end()), streams.end());
+    int32_t pick;
+    if (s->rr_last < 0 || !s->stream_less(s->rr_last, streams.back())) {
+        pick = streams[0];
+    } else {
+        pick = streams[0];
+        for (int32_t st : streams)
+            if (s->stream_less(s->rr_last, st)) { pick = st; break; }
+    }
+    s->rr_last = pick;
+    const int32_t slot = earliest_arrival(s, live, pick);
+    const KernelRec& k = s->kernels[slot];
+    int64_t pred;
+    int rc = solo_duration(s, k, &pred);
+    if (rc) return rc;
+    const int64_t dur = py_ceil((double)pred * noise_factor(s));
+    const std::string& name = s->stream_names[pick];
+    const bool sw = s->has_last_ctx && s->last_ctx != name;
+    const bool inf = kernel_slack(s, k, now) < 0;
+    make_dispatch(s, {slot}, now, dur, pred, s->prof.sm_count, pick, name, sw, false, k.flops,
+                  k.flops, inf);
+    return GMX_OK;
+}
+
+// scheduler.py:372-391
+static int shared_duration(const S* s, const KernelRec& k, int64_t tenants, int64_t* out) {
+    const gmx_tuning_config& cfg = solo_config(s, k);
+    if (tenants <= 1) return solo_duration(s, k, out);
+    const double share = 1.0 / (double)tenants;
+    int64_t blocks;
+    int rc = blocks_of(k.op, k.dims, cfg.tile_m, cfg.tile_n, &blocks);
+    if (rc) return rc;
+    const double capacity = share * (double)(s->prof.sm_count * s->prof.blocks_per_sm);
+    const double q = (double)blocks / capacity;
+    const double occ = q < 1.0 ? q : 1.0;
+    const double degradation = s->fp_base + s->fp_slope * share;
+    const double base_peak = k.dtype == GMX_DT_FP16 ? s->prof.peak_flops_dense : s->prof.peak_flops_scalar;
+    const double peak = base_peak * share * occ * degradation;
+    const int64_t c = py_ceil((double)k.flops / peak * 1e9);
+    const int64_t m = py_ceil((double)k.bytes / (s->prof.mem_bandwidth * share) * 1e9);
+    *out = c > m ? c : m;
+    return GMX_OK;
+}
+
+// scheduler.py:393-412
+static int step_space_mux(S* s, int64_t now) {
+    std::vector<int32_t> active;
+    active_streams(s, active);
+    const int64_t tenants = (int64_t)active.size();
+    if (tenants == 0) return GMX_OK;
+    const int64_t alloc = std::max<int64_t>(1, s->prof.sm_count / tenants);
+    std::vector<char> busy(s->stream_names.size(), 0);
+    for (const auto& kv : s->in_flight)
+        for (int32_t st : kv.second.streams) busy[st] = 1;
+    const double width = tenants >= 2 ? s->params.jitter_width * (double)(1 + tenants % 2) : 0.0;
+    std::vector<int32_t> live;
+    for (int32_t st : active) {
+        if (busy[st]) continue;
+        live_ready(s, live);
+        const int32_t slot = earliest_arrival(s, live, st);
+        if (slot < 0 || s->free_sms < alloc) continue;
+        const KernelRec& k = s->kernels[slot];
+        int64_t base;
+        int rc = shared_duration(s, k, tenants, &base);
+        if (rc) return rc;
+        const double factor = 1.0 + (width != 0.0 ? s->rng.uniform(0.0, width) : 0.0);
+        const int64_t dur = py_ceil((double)base * factor * noise_factor(s));
+        const bool inf = kernel_slack(s, k, now) < 0;
+        make_dispatch(s, {slot}, now, dur, base, alloc, st, s->stream_names[st], false, false,
+                      k.flops, k.flops, inf);
+    }
+    return GMX_OK;
+}
+
+struct Scored {
+    int32_t infeasible_rank;   // 0 if any member late
+    int64_t earliest_deadline;
+    int64_t min_id;
+    int32_t cluster;
+    bool late;
+};
+
+// scheduler.py:414-471
+static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
+    std::vector<int32_t> live;
+    live_ready(s, live);
+    if (live.empty()) return GMX_OK;
+    std::vector<int32_t> act;
+    active_streams(s, act);
+    const int64_t tenancy = std::max<int64_t>(1, (int64_t)act.size());
+
+    auto& recs = s->s_recs;
+    recs.clear();
+    for (int32_t slot : live) {
+        const KernelRec& k = s->kernels[slot];
+        ShapeRec r{k.id, k.op, k.dtype, k.nd, {k.dims[0], k.dims[1], k.dims[2]}, k.flops, slot};
+        recs.push_back(r);
+    }
+    int rc = cluster_shapes(recs, s->params.pad_budget, s->s_order, s->s_clusters);
+    if (rc) return rc;
+    const auto& order = s->s_order;
+    const auto& clusters = s->s_clusters;
+
+    std::vector<int64_t> slack(recs.size());
+    std::vector<Scored> scored;
+    scored.reserve(clusters.size());
+    for (int32_t c = 0; c < (int32_t)clusters.size(); ++c) {
+        Scored sc{1, INT64_MAX, INT64_MAX, c, false};
+        for (int32_t i = clusters[c].begin; i < clusters[c].end; ++i) {
+            const KernelRec& k = s->kernels[recs[order[i]].src];
+            slack[order[i]] = kernel_slack(s, k, now);
+            if (slack[order[i]] < 0) sc.late = true;
+            sc.earliest_deadline = std::min(sc.earliest_deadline, k.deadline);
+            sc.min_id = std::min(sc.min_id, k.id);
+        }
+        sc.infeasible_rank = sc.late ? 0 : 1;
+        scored.push_back(sc);
+    }
+    std::sort(scored.begin(), scored.end(), [](const Scored& a, const Scored& b) {
+        if (a.infeasible_rank != b.infeasible_rank) return a.infeasible_rank < b.infeasible_rank;
+        if (a.earliest_deadline != b.earliest_deadline) return a.earliest_deadline < b.earliest_deadline;
+        return a.min_id < b.min_id;
+    });
+
+    const double frac = s->params.max_delay_fraction;
+    std::vector<int32_t> members;
+    std::vector<int64_t> sig;
+    for (const Scored& sc : scored) {
+        const Cluster& cl = clusters[sc.cluster];
+        gmx_cost cost;
+        rc = superkernel_cost(&s->prof, s->tbl(), cl.op, cl.dtype, cl.padded, cl.nd,
+                              cl.end - cl.begin, tenancy, &cost);
+        if (rc) return rc;
+        members.clear();
+        for (int32_t i = cl.begin; i < cl.end; ++i) members.push_back(recs[order[i]].src);
+        bool can_delay = !sc.late && cost.efficiency < 1.0;
+        if (can_delay) {
+            for (int32_t i = cl.begin; i < cl.end && can_delay; ++i) {
+                const KernelRec& k = s->kernels[recs[order[i]].src];
+                can_delay = int_ge_float(slack[order[i]], frac * (double)slo_of(s, k));
+            }
+        }
+        if (can_delay) {
+            sig.clear();
+            for (int32_t slot : members) sig.push_back(s->kernels[slot].id);
+            std::sort(sig.begin(), sig.end());
+            if (s->withheld_sigs.insert(sig).second) {
+                // withhold once per member set; wakeup clamps to the slack boundary
+                for (int32_t slot : members) s->v_held_kids.push_back(s->kernels[slot].id);
+                s->v_held_off.push_back((int32_t)s->v_held_kids.size());
+                int64_t bound = now + s->params.stagger_horizon;
+                for (int32_t slot : members) {
+                    const KernelRec& k = s->kernels[slot];
+                    if (k.deadline >= kNoDeadline) continue;
+                    const int64_t edge = py_trunc((double)(k.deadline - predicted_remaining(s, k)) -
+                                                  frac * (double)slo_of(s, k));
+                    bound = std::min(bound, edge);
+                }
+                wakeups.push_back(std::max(bound, now + 1));
+                continue;
+            }
+        }
+        const int64_t alloc = std::min<int64_t>(s->prof.sm_count, ceil_ratio(cost.block_count, s->prof.blocks_per_sm));
+        if (s->free_sms < alloc) continue;
+        const int64_t dur = py_ceil((double)cost.duration * noise_factor(s));
+        make_dispatch(s, members, now, dur, cost.duration, alloc, GMX_CONTEXT_JIT, "jit", false, true,
+                      useful_of(s, members), cost.flops, sc.late);
+    }
+    return GMX_OK;
+}
+
+// scheduler.py:210-235
+static void unlock_dependents(S* s, int64_t done_id, const RequestRec& r, std::vector<int64_t>& unlocked) {
+    for (int32_t slot : r.kernels) {
+        KernelRec& k = s->kernels[slot];
+        if (!k.blocked) continue;
+        auto it = std::find(k.waiting.begin(), k.waiting.end(), done_id);
+        if (it != k.waiting.end()) k.waiting.erase(it);
+        if (k.waiting.empty()) {
+            k.blocked = false;
+            ready_add(s, slot);
+            unlocked.push_back(k.id);
+        }
+    }
+}
+
+}  // namespace gmx
+
+// ======================================================================= ABI
+
+using namespace gmx;
+
+extern "C" {
+
+const char* gmx_last_error(void) { return g_err.c_str(); }
+int gmx_core_version(void) { return 1; }
+
+int gmx_flop_count(int32_t op, const int64_t* dims, int32_t nd, int64_t* out) {
+    if (!dims || !out) return fail(GMX_EINVAL, "null argument");
+    int rc = check_dims(op, dims, nd);
+    return rc ? rc : flops_of(op, dims, out);
+}
+
+int gmx_bytes_moved(int32_t op, const int64_t* dims, int32_t nd, int32_t dtype, int64_t* out) {
+    if (!dims || !out) return fail(GMX_EINVAL, "null argument");
+    int rc = check_dims(op, dims, nd);
+    return rc ? rc : bytes_of(op, dims, dtype, out);
+}
+
+int gmx_block_count(int32_t op, const int64_t* dims, int32_t nd, int64_t tm, int64_t tn, int64_t* out) {
+    if (!dims || !out) return fail(GMX_EINVAL, "null argument");
+    if (op < 0 || op > 2 || nd != kArity[op]) return fail(GMX_EINVAL, "bad op/dims");
+    return blocks_of(op, dims, tm, tn, out);
+}
+
+int gmx_occupancy_efficiency(const gmx_profile* p, int64_t blocks, double factor, double* out) {
+    if (!p || !out) return fail(GMX_EINVAL, "null argument");
+    return occupancy(p, blocks, factor, out);
+}
+
+int gmx_roofline_duration(const gmx_profile* p, int64_t flops, int64_t nbytes, double eff,
+                          int32_t path, int64_t* out) {
+    if (!p || !out) return fail(GMX_EINVAL, "null argument");
+    return roofline(p, flops, nbytes, eff, path, out);
+}
+
+int gmx_kernel_cost(const gmx_profile* p, const gmx_kernel_desc* k, const gmx_tuning_config* cfg,
+                    gmx_cost* out) {
+    if (!p || !k || !out) return fail(GMX_EINVAL, "null argument");
+    int rc = check_dims(k->op, k->dims, k->ndims);
+    if (rc) return rc;
+    return kernel_cost(p, k->op, k->dtype, k->dims, cfg ? *cfg : kDefaultConfig, out);
+}
+
+int gmx_tuning_table_create(gmx_tuning_table** out) {
+    if (!out) return fail(GMX_EINVAL, "null argument");
+    *out = new (std::nothrow) gmx_tuning_table();
+    return *out ? GMX_OK : fail(GMX_ENOMEM, "out of memory");
+}
+
+void gmx_tuning_table_destroy(gmx_tuning_table* t) { delete t; }
+
+int gmx_tuning_table_put(gmx_tuning_table* t, int32_t op, int32_t dtype, const int64_t* dims,
+                         int32_t nd, int64_t tenancy, const gmx_tuning_config* cfg) {
+    if (!t || !dims || !cfg) return fail(GMX_EINVAL, "null argument");
+    int rc = check_dims(op, dims, nd);
+    if (rc) return rc;
+    t->entries[make_key(op, dtype, dims, nd)][tenancy] = *cfg;
+    return GMX_OK;
+}
+
+int gmx_tuning_table_lookup(const gmx_tuning_table* t, int32_t op, int32_t dtype, const int64_t* dims,
+                            int32_t nd, int64_t tenancy, gmx_tuning_config* out, int32_t* found) {
+    if (!dims || !out) return fail(GMX_EINVAL, "null argument");
+    bool f = false;
+    *out = t ? t->lookup(make_key(op, dtype, dims, nd), tenancy, &f) : kDefaultConfig;
+    if (found) *found = f;
+    return GMX_OK;
+}
+
+int gmx_padding_waste(int32_t op, const int64_t* member_flops, int32_t n, const int64_t* padded,
+                      int32_t nd, double* out) {
+    if (!member_flops || !padded || !out) return fail(GMX_EINVAL, "null argument");
+    if (n < 1) return fail(GMX_EINVAL, "empty cluster");
+    int rc = check_dims(op, padded, nd);
+    if (rc) return rc;
+    int64_t pf;
+    if ((rc = flops_of(op, padded, &pf))) return rc;
+    u128 sum = 0;
+    for (int32_t i = 0; i < n; ++i) sum += (u128)member_flops[i];
+    *out = waste_ratio(sum, n, pf);
+    return GMX_OK;
+}
+
+int gmx_cluster_shapes(const gmx_kernel_desc* pending, int32_t n, double budget, int32_t* out_members,
+                       int32_t* out_offsets, int64_t* out_padded, double* out_waste, int32_t* out_nc) {
+    if (n < 0 || (n > 0 && (!pending || !out_members || !out_offsets || !out_padded || !out_waste)) ||
+        !out_nc)
+        return fail(GMX_EINVAL, "null argument");
+    std::vector<ShapeRec> recs((size_t)n);
+    for (int32_t i = 0; i < n; ++i) {
+        const gmx_kernel_desc& k = pending[i];
+        int rc = check_dims(k.op, k.dims, k.ndims);
+        if (rc) return rc;
+        ShapeRec& r = recs[i];
+        r.id = k.kernel_id;
+        r.op = k.op;
+        r.dtype = k.dtype;
+        r.nd = k.ndims;
+        for (int d = 0; d < 3; ++d) r.dims[d] = d < k.ndims ? k.dims[d] : 0;
+        if ((rc = flops_of(k.op, k.dims, &r.flops))) return rc;
+        r.src = i;
+    }
+    std::vector<int32_t> order;
+    std::vector<Cluster> clusters;
+    int rc = cluster_shapes(recs, budget, order, clusters);
+    if (rc) return rc;
+    for (size_t i = 0; i < order.size(); ++i) out_members[i] = recs[order[i]].src;
+    for (size_t c = 0; c < clusters.size(); ++c) {
+        out_offsets[c] = clusters[c].begin;
+        for (int d = 0; d < 3; ++d) out_padded[3 * c + d] = clusters[c].padded[d];
+        out_waste[c] = clusters[c].waste;
+    }
+    if (n > 0) out_offsets[clusters.size()] = (int32_t)order.size();
+    *out_nc = (int32_t)clusters.size();
+    return GMX_OK;
+}
+
+int gmx_form_superkernel(const gmx_profile* p, const gmx_tuning_table* t, int32_t op, int32_t dtype,
+                         const int64_t* padded, int32_t nd, int64_t batch, int64_t tenancy, gmx_cost* out) {
+    if (!p || !padded || !out) return fail(GMX_EINVAL, "null argument");
+    int rc = check_dims(op, padded, nd);
+    if (rc) return rc;
+    if (batch < 1) return fail(GMX_EINVAL, "empty cluster");
+    return superkernel_cost(p, t, op, dtype, padded, nd, batch, tenancy, out);
+}
+
+int gmx_sched_create(const gmx_profile* p, int32_t policy, const gmx_policy_params* params,
+                     const gmx_tuning_table* table, double fp_base, double fp_slope, uint64_t jitter,
+                     gmx_sched** out) {
+    if (!p || !params || !out) return fail(GMX_EINVAL, "null argument");
+    if (policy < GMX_POLICY_FIFO || policy > GMX_POLICY_SPACE_MUX) return fail(GMX_EINVAL, "unknown policy");
+    if (p->sm_count <= 0 || p->blocks_per_sm <= 0) return fail(GMX_EINVAL, "bad profile");
+    if (!(params->pad_budget >= 0.0 && params->pad_budget < 1.0))
+        return fail(GMX_EINVAL, "pad_budget must be in [0, 1)");
+    if (params->stagger_horizon < 1) return fail(GMX_EINVAL, "stagger_horizon must be >= 1 ns");
+    gmx_sched* s = new (std::nothrow) gmx_sched();
+    if (!s) return fail(GMX_ENOMEM, "out of memory");
+    s->prof = *p;
+    s->policy = policy;
+    s->params = *params;
+    if (table) {
+        s->table = *table;
+        s->has_table = true;
+    }
+    s->fp_base = fp_base;
+    s->fp_slope = fp_slope;
+    s->rng.state = jitter;
+    s->free_sms = p->sm_count;
+    *out = s;
+    return GMX_OK;
+}
+
+void gmx_sched_destroy(gmx_sched* s) { delete s; }
+
+int gmx_sched_intern_stream(gmx_sched* s, const char* name, int32_t* out) {
+    if (!s || !name || !out) return fail(GMX_EINVAL, "null argument");
+    auto it = s->stream_ids.find(name);
+    if (it != s->stream_ids.end()) {
+        *out = it->second;
+        return GMX_OK;
+    }
+    const int32_t id = (int32_t)s->stream_names.size();
+    s->stream_names.emplace_back(name);
+    s->stream_ids.emplace(name, id);
+    s->evicted_stream.push_back(0);
+    *out = id;
+    return GMX_OK;
+}
+
+int gmx_sched_add_request(gmx_sched* s, int64_t request_id, int32_t stream, int64_t arrival,
+                          const gmx_kernel_desc* ks, int32_t n, const int64_t* dep_ids,
+                          const int32_t* dep_off, int64_t* out_pred, int32_t* accepted) {
+    if (!s || (n > 0 && (!ks || !dep_off)) || !accepted) return fail(GMX_EINVAL, "null argument");
+    if (stream < 0 || stream >= (int32_t)s->stream_names.size()) return fail(GMX_EINVAL, "unknown stream");
+    for (int32_t i = 0; i < n; ++i) {
+        int rc = check_dims(ks[i].op, ks[i].dims, ks[i].ndims);
+        if (rc) return rc;
+        if (ks[i].stream < 0 || ks[i].stream >= (int32_t)s->stream_names.size())
+            return fail(GMX_EINVAL, "unknown kernel stream");
+    }
+    RequestRec r;
+    r.id = request_id;
+    r.stream = stream;
+    r.arrival = arrival;
+    std::unordered_set<int64_t> distinct;
+    for (int32_t i = 0; i < n; ++i) {
+        distinct.insert(ks[i].kernel_id);
+        r.kernel_ids.push_back(ks[i].kernel_id);
+    }
+    r.remaining = (int64_t)distinct.size();
+    const int32_t rslot = (int32_t)s->requests.size();
+    if (s->evicted_stream[stream]) {
+        r.evicted = true;
+        s->requests.push_back(std::move(r));
+        s->request_slot[request_id] = rslot;
+        *accepted = 0;
+        return GMX_OK;
+    }
+    // compute predictions first so a failure leaves the state untouched
+    std::vector<KernelRec> recs((size_t)n);
+    for (int32_t i = 0; i < n; ++i) {
+        const gmx_kernel_desc& d = ks[i];
+        KernelRec& k = recs[i];
+        k.id = d.kernel_id;
+        k.stream = d.stream;
+        k.op = d.op;
+        k.dtype = d.dtype;
+        k.nd = d.ndims;
+        for (int j = 0; j < 3; ++j) k.dims[j] = j < d.ndims ? d.dims[j] : 0;
+        k.arrival = d.arrival;
+        k.deadline = d.deadline;
+        int rc;
+        if ((rc = flops_of(k.op, k.dims, &k.flops)) || (rc = bytes_of(k.op, k.dims, k.dtype, &k.bytes)))
+            return rc;
+        gmx_cost c;
+        if ((rc = kernel_cost(&s->prof, k.op, k.dtype, k.dims, solo_config(s, k), &c))) return rc;
+        k.predicted = c.duration;
+        k.req = rslot;
+        k.pos = i;
+        for (int32_t j = dep_off[i]; j < dep_off[i + 1]; ++j) {
+            if (std::find(k.waiting.begin(), k.waiting.end(), dep_ids[j]) == k.waiting.end())
+                k.waiting.push_back(dep_ids[j]);
+        }
+    }
+    s->requests.push_back(std::move(r));
+    s->request_slot[request_id] = rslot;
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t slot = (int32_t)s->kernels.size();
+        KernelRec& k = recs[i];
+        // a re-used kernel id shadows the old record (dict assignment semantics)
+        auto old = s->kernel_slot.find(k.id);
+        if (old != s->kernel_slot.end()) {
+            ready_remove(s, old->second);
+            s->kernels[old->second].blocked = false;
+        }
+        s->kernel_slot[k.id] = slot;
+        const bool has_deps = !k.waiting.empty();
+        s->kernels.push_back(std::move(k));
+        s->requests[rslot].kernels.push_back(slot);
+        if (out_pred) out_pred[i] = s->kernels[slot].predicted;
+        if (has_deps)
+            s->kernels[slot].blocked = true;
+        else
+            ready_add(s, slot);
+    }
+    *accepted = 1;
+    return GMX_OK;
+}
+
+int gmx_sched_step(gmx_sched* s, int64_t now, gmx_step_view* out) {
+    if (!s || !out) return fail(GMX_EINVAL, "null argument");
+    s->v_disp.clear();
+    s->v_disp_kids.clear();
+    s->v_held_kids.clear();
+    s->v_held_off.assign(1, 0);
+    std::vector<int64_t> wakeups;
+    int rc = GMX_OK;
+    switch (s->policy) {
+        case GMX_POLICY_FIFO: rc = step_serial(s, now, false); break;
+        case GMX_POLICY_EDF: rc = step_serial(s, now, true); break;
+        case GMX_POLICY_TIME_MUX: rc = step_time_mux(s, now); break;
+        case GMX_POLICY_SPACE_MUX: rc = step_space_mux(s, now); break;
+        default: rc = step_ooo(s, now, wakeups); break;
+    }
+    if (rc) return rc;
+    out->n_dispatches = (int32_t)s->v_disp.size();
+    out->dispatches = s->v_disp.data();
+    out->dispatch_kernel_ids = s->v_disp_kids.data();
+    out->n_withheld = (int32_t)s->v_held_off.size() - 1;
+    out->withheld_offsets = s->v_held_off.data();
+    out->withheld_kernel_ids = s->v_held_kids.data();
+    out->has_wakeup = !wakeups.empty();
+    out->wakeup = wakeups.empty() ? 0 : *std::min_element(wakeups.begin(), wakeups.end());
+    return GMX_OK;
+}
+
+int gmx_sched_complete(gmx_sched* s, int64_t did, int64_t now, gmx_complete_view* out) {
+    if (!s || !out) return fail(GMX_EINVAL, "null argument");
+    auto it = s->in_flight.find(did);
+    if (it == s->in_flight.end()) return fail(GMX_ENOTFOUND, "unknown dispatch id");
+    DispatchRec d = std::move(it->second);
+    s->in_flight.erase(it);
+    s->free_sms += d.rec.sm_allocation;
+    s->v_ids_a.clear();  // kernel ids
+    s->v_ids_b.clear();  // finished requests
+    s->v_ids_c.clear();  // unlocked kernels
+    for (int32_t slot : d.kernels) {
+        KernelRec& k = s->kernels[slot];
+        s->v_ids_a.push_back(k.id);
+        const bool first = !k.done;
+        k.done = true;
+        RequestRec& r = s->requests[k.req];
+        if (first && r.remaining > 0) --r.remaining;
+        if (r.remaining == 0 && !r.finished) {
+            r.finished = true;
+            s->v_ids_b.push_back(r.id);
+        }
+        unlock_dependents(s, k.id, r, s->v_ids_c);
+    }
+    out->dispatch = d.rec;
+    out->dispatch.kernel_offset = 0;
+    out->kernel_ids = s->v_ids_a.data();
+    out->n_finished = (int32_t)s->v_ids_b.size();
+    out->finished_request_ids = s->v_ids_b.data();
+    out->n_unlocked = (int32_t)s->v_ids_c.size();
+    out->unlocked_kernel_ids = s->v_ids_c.data();
+    return GMX_OK;
+}
+
+int gmx_sched_evict_stream(gmx_sched* s, int32_t stream, int64_t now, gmx_evict_view* out) {
+    (void)now;
+    if (!s || !out) return fail(GMX_EINVAL, "null argument");
+    if (stream < 0 || stream >= (int32_t)s->stream_names.size()) return fail(GMX_EINVAL, "unknown stream");
+    s->evicted_stream[stream] = 1;
+    s->v_ids_a.clear();  // cancelled dispatches
+    s->v_ids_b.clear();  // evicted requests
+    s->v_ids_c.clear();  // dropped kernels
+    for (auto it = s->in_flight.begin(); it != s->in_flight.end();) {
+        if (it->second.streams.size() == 1 && it->second.streams[0] == stream) {
+            s->v_ids_a.push_back(it->first);
+            s->free_sms += it->second.rec.sm_allocation;
+            it = s->in_flight.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    for (RequestRec& r : s->requests) {
+        if (r.stream != stream || r.finished) continue;
+        if (!r.evicted) {
+            r.evicted = true;
+            s->v_ids_b.push_back(r.id);
+        }
+        for (int32_t slot : r.kernels) {
+            KernelRec& k = s->kernels[slot];
+            if (k.ready_pos >= 0 || k.blocked) s->v_ids_c.push_back(k.id);
+            ready_remove(s, slot);
+            k.blocked = false;
+            k.waiting.clear();
+        }
+    }
+    std::sort(s->v_ids_b.begin(), s->v_ids_b.end());
+    out->n_cancelled = (int32_t)s->v_ids_a.size();
+    out->cancelled_dispatch_ids = s->v_ids_a.data();
+    out->n_evicted = (int32_t)s->v_ids_b.size();
+    out->evicted_request_ids = s->v_ids_b.data();
+    out->n_dropped = (int32_t)s->v_ids_c.size();
+    out->dropped_kernel_ids = s->v_ids_c.data();
+    return GMX_OK;
+}
+
+static const KernelRec* find_kernel(const gmx_sched* s, int64_t id) {
+    auto it = s->kernel_slot.find(id);
+    return it == s->kernel_slot.end() ? nullptr : &s->kernels[it->second];
+}
+
+int gmx_sched_predicted_remaining(const gmx_sched* s, int64_t id, int64_t* out) {
+    if (!s || !out) return fail(GMX_EINVAL, "null argument");
+    const KernelRec* k = find_kernel(s, id);
+    if (!k) return fail(GMX_ENOTFOUND, "unknown kernel id");
+    *out = predicted_remaining(s, *k);
+    return GMX_OK;
+}
+
+int gmx_sched_kernel_slack(const gmx_sched* s, int64_t id, int64_t now, int64_t* out) {
+    if (!s || !out) return fail(GMX_EINVAL, "null argument");
+    const KernelRec* k = find_kernel(s, id);
+    if (!k) return fail(GMX_ENOTFOUND, "unknown kernel id");
+    *out = kernel_slack(s, *k, now);
+    return GMX_OK;
+}
+
+int gmx_sched_free_sms(const gmx_sched* s, int64_t* out) {
+    if (!s || !out) return fail(GMX_EINVAL, "null argument");
+    *out = s->free_sms;
+    return GMX_OK;
+}
+
+int gmx_sched_set_free_sms(gmx_sched* s, int64_t v) {
+    if (!s) return fail(GMX_EINVAL, "null argument");
+    s->free_sms = v;
+    return GMX_OK;
+}
+
+int gmx_sched_num_ready(const gmx_sched* s, int64_t* out) {
+    if (!s || !out) return fail(GMX_EINVAL, "null argument");
+    *out = (int64_t)s->ready.size();
+    return GMX_OK;
+}
+
+int gmx_sched_jitter_state(const gmx_sched* s, uint64_t* out) {
+    if (!s || !out) return fail(GMX_EINVAL, "null argument");
+    *out = s->rng.state;
+    return GMX_OK;
+}
+
+int gmx_sched_set_jitter_state(gmx_sched* s, uint64_t st) {
+    if (!s) return fail(GMX_EINVAL, "null argument");
+    s->rng.state = st;
+    return GMX_OK;
+}
+
+}  // extern "C"
