@@ -1,0 +1,105 @@
+/*
+ * gmx_exec.h — C ABI of the coalesced sm_100a executor (libgmx_exec.so).
+ *
+ * The reference never executes a kernel: a dispatch's "execution" is the
+ * number roofline_duration() returns (gpumux/device.py:140-150), turned into
+ * a COMPLETE event at d.end (gpumux/engine.py:359-364). This library is the
+ * real thing: ONE persistent launch per scheduler step whose work list spans
+ * every member of every superkernel dispatched in that step.
+ *
+ *   gmx_exec_register  <- a kernel's operands (KernelSpec has none in the
+ *                         reference: kernels.py:95-124 is shape-only)
+ *   gmx_exec_launch    <- the execution of a step's dispatches
+ *                         (engine.py:359-364, scheduler.py:294-316)
+ *
+ * Members run at their TRUE dims: coalescing padding is a billing concept of
+ * the decision model (coalesce.py:7-8), not materialised on the device.
+ *
+ * Operand conventions (row-major, leading dims in ELEMENTS):
+ *   gemm (m,n,k):  C[m x n] = act(A[m x k] . B[k x n] + bias[m])
+ *                  A given as A[m][lda] (K contiguous), B given TRANSPOSED as
+ *                  Bt[n][ldb] (K contiguous: the NHWC im2col layout), C[m][ldc].
+ *                  bf16 in, fp32 accumulate (tcgen05/TMEM), bf16 or fp32 out.
+ *                  lda, ldb multiples of 8; pointers 16-byte aligned (TMA).
+ *   gemv (m,n):    y[m] = act(W[m x n] . x[n] + bias[m]); W[m][lda]; fp32 or bf16.
+ *   elementwise n: y[i] = act(x[i] + bias?) ; x, y contiguous; fp32 or bf16.
+ * All device pointers are caller-owned (torch tensors); the executor owns its
+ * descriptor table, plans, and split-K workspace. Launches are asynchronous on
+ * the caller's stream; one executor handle must not be launched from two
+ * streams concurrently (shared split-K workspace). Not thread-safe.
+ */
+#ifndef GMX_EXEC_H
+#define GMX_EXEC_H
+
+#include <stdint.h>
+
+#include "gmx_core.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GMX_ST_BF16 0      /* storage dtypes */
+#define GMX_ST_F32 1
+
+#define GMX_ACT_NONE 0     /* fused epilogue activation */
+#define GMX_ACT_RELU 1
+#define GMX_ACT_GELU 2     /* erf form: 0.5 x (1 + erf(x / sqrt 2)) */
+
+typedef struct gmx_exec gmx_exec;
+
+typedef struct gmx_problem_desc {
+    int32_t op;            /* GMX_OP_GEMM / GMX_OP_GEMV / GMX_OP_ELEMENTWISE */
+    int32_t in_dtype;      /* GMX_ST_*: gemm must be BF16 */
+    int32_t out_dtype;     /* GMX_ST_* */
+    int32_t activation;    /* GMX_ACT_* */
+    int64_t m, n, k;       /* gemm (m,n,k); gemv (m,n,-); elementwise (n,-,-) in m */
+    const void* a;         /* gemm A / gemv W / elementwise x */
+    int64_t lda;
+    const void* b;         /* gemm Bt / gemv x / unused */
+    int64_t ldb;
+    void* c;               /* output */
+    int64_t ldc;
+    const float* bias;     /* optional, length m (gemm/gemv); NULL for none */
+} gmx_problem_desc;
+
+typedef struct gmx_plan_stats {
+    int32_t grid;               /* CTAs launched (<= SM count, persistent) */
+    int32_t n_items;            /* work items in the list */
+    int32_t n_gemm_tiles;       /* 128 x BN output tiles (before split-K) */
+    int32_t n_split_items;      /* items that are split-K partials */
+    int32_t n_gemv_items;
+    int32_t n_eltwise_items;
+    int32_t cached;             /* 1 if the plan came from the plan cache */
+    int32_t _pad;
+    int64_t operand_bytes;      /* algorithmic bytes: each operand + result once */
+    int64_t tile_load_bytes;    /* bytes the tile loads request (re-reads included) */
+    int64_t flops;              /* useful flops of the launch */
+    double max_cta_cost;        /* planner's makespan estimate (bytes-equivalent) */
+    double mean_cta_cost;
+} gmx_plan_stats;
+
+/* message of the last failed executor call on this thread */
+const char* gmx_exec_last_error(void);
+int gmx_exec_create(int32_t device, gmx_exec** out);
+void gmx_exec_destroy(gmx_exec* ex);
+/* number of SMs / persistent CTAs of the device */
+int gmx_exec_num_sms(const gmx_exec* ex, int32_t* out);
+/* Register one member's operands; returns a slot (encodes its TMA descriptors). */
+int gmx_exec_register(gmx_exec* ex, const gmx_problem_desc* desc, int32_t* out_slot);
+int gmx_exec_unregister(gmx_exec* ex, int32_t slot);
+/* One coalesced persistent launch over `n` registered slots (order irrelevant).
+ * Plans (tile list, LPT assignment across SMs, split-K choice) are cached per
+ * slot set. `stream` is a cudaStream_t (NULL = legacy default stream). */
+int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream);
+/* Stats of the plan used by the last launch. */
+int gmx_exec_last_plan(const gmx_exec* ex, gmx_plan_stats* out);
+/* Drop cached plans (e.g. after unregistering many slots). */
+int gmx_exec_clear_plans(gmx_exec* ex);
+/* Planner knobs: max split-K factor (1 disables split-K), plan cache on/off. */
+int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GMX_EXEC_H */

@@ -1,0 +1,923 @@
+// gmx_exec.cu — coalesced persistent executor for sm_100a (B200) behind include/gmx_exec.h.
+//
+// One launch per scheduler step. The launch's work list spans every member of every
+// superkernel the OoO scheduler dispatched in that step (gpumux/scheduler.py:414-454 decides
+// WHAT runs together; this file is HOW it runs on the device):
+//
+//   GEMM items   128 x BN output tiles (BN in {32..128}), K streamed in 64-element blocks:
+//                TMA (SWIZZLE_128B) -> 6-stage smem ring -> tcgen05.mma (M=128, fp32 accumulate
+//                in TMEM, double-buffered accumulators) -> tcgen05.ld epilogue with fused bias +
+//                activation -> bf16/fp32 stores. Long-K tiles are split along K; partials meet in
+//                an fp32 workspace and the last-arriving CTA reduces them in split order
+//                (deterministic). The larger of m/n goes on the UMMA-M side ("role swap").
+//   GEMV items   row blocks of y = W x, streamed with 16-byte non-allocating loads.
+//   Eltwise      vectorised y = act(x) ranges.
+//
+// Warp roles (6 warps, 1 CTA per SM, grid <= #SMs, persistent):
+//   warp 0  TMA producer (one lane)       warp 1  TMEM owner + UMMA issuer (one lane)
+//   warps 2-5  epilogue: TMEM -> registers -> global, and the CUDA-core GEMV / eltwise items.
+// Each role walks the same per-CTA item list; only the roles an item needs act on it.
+//
+// Host side: operand registration encodes the TMA descriptors once (tensor maps live in a
+// device-resident problem table); a per-slot-set plan (tile list, split-K choice, LPT
+// assignment of items to CTAs) is built once and cached, so a recurring step costs one
+// kernel launch.
+
+#include "../../../include/gmx_exec.h"
+#include "sm100_ptx.cuh"
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <queue>
+#include <string>
+#include <vector>
+
+namespace gmx {
+
+// ------------------------------------------------------------------ device-side types
+
+enum : int32_t { kItemGemm = 0, kItemGemv = 1, kItemEltwise = 2 };
+
+constexpr int kThreads = 192;
+constexpr int kStages = 6;
+constexpr int kTileRows = 128;             // UMMA M
+constexpr int kBlockK = 64;                // 64 bf16 = 128 B = one swizzle atom row
+constexpr int kMaxBN = 128;
+constexpr int kStageA = kTileRows * kBlockK * 2;   // 16 KB
+constexpr int kStageB = kMaxBN * kBlockK * 2;      // 16 KB
+constexpr int kStageBytes = kStageA + kStageB;
+constexpr int kTmemCols = 256;             // 2 accumulators x 128 fp32 columns
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kWsBlock = 4096;             // split-K workspace allocation unit (floats)
+
+struct alignas(64) DevProblem {
+    CUtensorMap tm_rows;     // operand on the UMMA-M side (128-row boxes)
+    CUtensorMap tm_cols;     // operand on the UMMA-N side (BN-row boxes)
+    void* out;
+    const void* in0;         // gemv W / eltwise x
+    const void* in1;         // gemv x
+    const float* bias;
+    int64_t ld_out;
+    int64_t ld_in0;
+    int32_t kind;            // kItem*
+    int32_t swap;            // gemm: rows side is n (Bt), cols side is m (A)
+    int32_t rows;            // gemm: extent on the M side; gemv: m; eltwise: count
+    int32_t cols;            // gemm: extent on the N side; gemv: n
+    int32_t K;
+    int32_t bn;
+    int32_t act;
+    int32_t in_dt;
+    int32_t out_dt;
+    int32_t kblocks;
+    int32_t _pad[6];
+};
+static_assert(sizeof(DevProblem) % 64 == 0, "DevProblem must keep 64-byte tensor map alignment");
+
+struct WorkItem {
+    int32_t problem;
+    uint8_t type;
+    uint8_t nsplit;
+    uint8_t split;
+    uint8_t _pad;
+    int32_t row0;            // gemm: M-side origin; gemv: first row; eltwise: first element
+    int32_t col0;            // gemm: N-side origin; gemv: end row;  eltwise: end element
+    int32_t kb0, kb1;        // gemm: k-block range of this (split) item
+    int32_t tile_slot;       // split-K: arrival counter index
+    int32_t ws_blk;          // split-K: workspace offset in kWsBlock units
+};
+static_assert(sizeof(WorkItem) == 32, "WorkItem layout");
+
+struct KernelArgs {
+    const DevProblem* probs;
+    const WorkItem* items;
+    const int32_t* cta_off;
+    float* ws;
+    int32_t* counters;
+};
+
+__device__ __forceinline__ float apply_act(float x, int32_t act) {
+    if (act == GMX_ACT_RELU) return fmaxf(x, 0.0f);
+    if (act == GMX_ACT_GELU) return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+    return x;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void store_one(void* out, int64_t idx, int32_t dt, float v) {
+    if (dt == GMX_ST_BF16)
+        reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
+    else
+        reinterpret_cast<float*>(out)[idx] = v;
+}
+
+// Write 32 accumulator columns of the thread's tile row to the output.
+__device__ __forceinline__ void store_tile_chunk(const DevProblem& P, const WorkItem& it, int trow, int c,
+                                                 float (&v)[32]) {
+    const int gr = it.row0 + trow;                  // M-side index
+    if (gr >= P.rows) return;
+    const int gc0 = it.col0 + c * 32;               // N-side index of v[0]
+    const int nvalid = min(32, P.cols - gc0);
+    if (nvalid <= 0) return;
+    if (!P.swap) {
+        // gr = m (output row), columns = n: contiguous in memory
+        const float b = P.bias ? __ldg(P.bias + gr) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j] + b, P.act);
+        const int64_t base = (int64_t)gr * P.ld_out + gc0;
+        if (P.out_dt == GMX_ST_BF16) {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(P.out) + base;
+            if (nvalid == 32 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+                uint4* o4 = reinterpret_cast<uint4*>(o);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    o4[q] = make_uint4(pack_bf16x2(v[8 * q + 0], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                                       pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+                return;
+            }
+        } else {
+            float* o = reinterpret_cast<float*>(P.out) + base;
+            if (nvalid == 32 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+                float4* o4 = reinterpret_cast<float4*>(o);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) o4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                return;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < nvalid) store_one(P.out, base + j, P.out_dt, v[j]);
+    } else {
+        // gr = n (output column), columns = m (output rows): lanes write consecutive n
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (j < nvalid) {
+                const int m = gc0 + j;
+                const float b = P.bias ? __ldg(P.bias + m) : 0.0f;
+                store_one(P.out, (int64_t)m * P.ld_out + gr, P.out_dt, apply_act(v[j] + b, P.act));
+            }
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ float load_f(const T* p);
+template <>
+__device__ __forceinline__ float load_f<float>(const float* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ float load_f<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+__device__ __forceinline__ float dot_v4(uint4 w, uint4 x, float) {
+    return __uint_as_float(w.x) * __uint_as_float(x.x) + __uint_as_float(w.y) * __uint_as_float(x.y) +
+           __uint_as_float(w.z) * __uint_as_float(x.z) + __uint_as_float(w.w) * __uint_as_float(x.w);
+}
+__device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
+__device__ __forceinline__ float dot_v4(uint4 w, uint4 x, __nv_bfloat16) {
+    return bf_lo(w.x) * bf_lo(x.x) + bf_hi(w.x) * bf_hi(x.x) + bf_lo(w.y) * bf_lo(x.y) + bf_hi(w.y) * bf_hi(x.y) +
+           bf_lo(w.z) * bf_lo(x.z) + bf_hi(w.z) * bf_hi(x.z) + bf_lo(w.w) * bf_lo(x.w) + bf_hi(w.w) * bf_hi(x.w);
+}
+
+// y[r] for r in [r0, r1): each epilogue warp owns every 4th row; 16-byte streaming loads of W
+// with 4 outstanding per lane, x re-read through L1.
+template <typename T>
+__device__ void gemv_rows(const DevProblem& P, int r0, int r1, int ew) {
+    const T* W = reinterpret_cast<const T*>(P.in0);
+    const T* x = reinterpret_cast<const T*>(P.in1);
+    const int n = P.cols;
+    constexpr int kVec = 16 / sizeof(T);
+    const int lane = lane_id();
+    const bool vec_ok = (n % kVec == 0) && (P.ld_in0 % kVec == 0) &&
+                        ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(x)) & 15) == 0;
+    for (int r = r0 + ew; r < r1; r += 4) {
+        const T* w = W + (int64_t)r * P.ld_in0;
+        float acc = 0.0f;
+        if (vec_ok) {
+            const int nv = n / kVec;
+            int j = lane;
+            for (; j + 96 < nv; j += 128) {
+                const uint4 w0 = ld_stream_v4(w + (int64_t)j * kVec);
+                const uint4 w1 = ld_stream_v4(w + (int64_t)(j + 32) * kVec);
+                const uint4 w2 = ld_stream_v4(w + (int64_t)(j + 64) * kVec);
+                const uint4 w3 = ld_stream_v4(w + (int64_t)(j + 96) * kVec);
+                const uint4* xv = reinterpret_cast<const uint4*>(x);
+                acc += dot_v4(w0, __ldg(xv + j), T()) + dot_v4(w1, __ldg(xv + j + 32), T()) +
+                       dot_v4(w2, __ldg(xv + j + 64), T()) + dot_v4(w3, __ldg(xv + j + 96), T());
+            }
+            for (; j < nv; j += 32)
+                acc += dot_v4(ld_stream_v4(w + (int64_t)j * kVec), __ldg(reinterpret_cast<const uint4*>(x) + j), T());
+        } else {
+            for (int j = lane; j < n; j += 32) acc += load_f<T>(w + j) * load_f<T>(x + j);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            const float b = P.bias ? __ldg(P.bias + r) : 0.0f;
+            store_one(P.out, r, P.out_dt, apply_act(acc + b, P.act));
+        }
+    }
+}
+
+template <typename T>
+__device__ void eltwise_range(const DevProblem& P, int e0, int e1, int tid, int nthreads) {
+    const T* x = reinterpret_cast<const T*>(P.in0);
+    T* y = reinterpret_cast<T*>(P.out);
+    constexpr int kVec = 16 / sizeof(T);
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0 &&
+                        (e0 % kVec) == 0;
+    int i = e0;
+    if (vec_ok) {
+        const int nvec = (e1 - e0) / kVec;
+        for (int v = tid; v < nvec; v += nthreads) {
+            const int64_t idx = (int64_t)e0 + (int64_t)v * kVec;
+            uint4 u = ld_stream_v4(x + idx);
+            if constexpr (sizeof(T) == 4) {
+                u.x = __float_as_uint(apply_act(__uint_as_float(u.x), P.act));
+                u.y = __float_as_uint(apply_act(__uint_as_float(u.y), P.act));
+                u.z = __float_as_uint(apply_act(__uint_as_float(u.z), P.act));
+                u.w = __float_as_uint(apply_act(__uint_as_float(u.w), P.act));
+            } else {
+                u.x = pack_bf16x2(apply_act(bf_lo(u.x), P.act), apply_act(bf_hi(u.x), P.act));
+                u.y = pack_bf16x2(apply_act(bf_lo(u.y), P.act), apply_act(bf_hi(u.y), P.act));
+                u.z = pack_bf16x2(apply_act(bf_lo(u.z), P.act), apply_act(bf_hi(u.z), P.act));
+                u.w = pack_bf16x2(apply_act(bf_lo(u.w), P.act), apply_act(bf_hi(u.w), P.act));
+            }
+            *reinterpret_cast<uint4*>(y + idx) = u;
+        }
+        i = e0 + nvec * kVec;
+    }
+    for (int j = i + tid; j < e1; j += nthreads) {
+        const float v = apply_act(load_f<T>(x + j), P.act);
+        store_one(y, j, sizeof(T) == 4 ? GMX_ST_F32 : GMX_ST_BF16, v);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const KernelArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int32_t* split_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = lane_id();
+    const int beg = args.cta_off[blockIdx.x];
+    const int end = args.cta_off[blockIdx.x + 1];
+
+    bool has_gemm = false;
+    for (int i = beg; i < end; ++i) has_gemm |= args.items[i].type == kItemGemm;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);   // one arrival per epilogue warp
+        }
+        mbar_fence_init();
+    }
+    if (warp == 1 && has_gemm) tmem_alloc(tmem_slot, kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = has_gemm ? *tmem_slot : 0u;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0 && has_gemm) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int i = beg; i < end; ++i) {
+                const WorkItem it = args.items[i];
+                if (it.type != kItemGemm) continue;
+                const DevProblem* P = args.probs + it.problem;
+                const uint32_t bytes = kStageA + (uint32_t)P->bn * (kBlockK * 2);
+                for (int kb = it.kb0; kb < it.kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* tile = smem + stage * kStageBytes;
+                    mbar_expect_tx(&full[stage], bytes);
+                    tma_load_2d(tile, &P->tm_rows, &full[stage], kb * kBlockK, it.row0);
+                    tma_load_2d(tile + kStageA, &P->tm_cols, &full[stage], kb * kBlockK, it.col0);
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- UMMA issuer ----------------
+        if (lane == 0 && has_gemm) {
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            for (int i = beg; i < end; ++i) {
+                const WorkItem it = args.items[i];
+                if (it.type != kItemGemm) continue;
+                const uint32_t idesc = idesc_bf16_m128((uint32_t)args.probs[it.problem].bn);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)acc * kMaxBN;
+                for (int kb = it.kb0; kb < it.kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint8_t* tile = smem + stage * kStageBytes;
+                    const uint64_t a_desc = smem_desc_sw128(tile);
+                    const uint64_t b_desc = smem_desc_sw128(tile + kStageA);
+#pragma unroll
+                    for (int k = 0; k < kBlockK / 16; ++k)   // 16-element UMMA K steps = +32 B
+                        umma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb > it.kb0 || k > 0) ? 1u : 0u);
+                    umma_commit(&empty[stage]);
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+                umma_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else {
+        // ---------------- epilogue / CUDA-core items ----------------
+        const int ew = warp - 2;                 // 0..3
+        const int lgrp = warp & 3;               // TMEM lane quarter this warp may access
+        const int trow = lgrp * 32 + lane;       // tile row owned by this thread
+        const int etid = ew * 32 + lane;         // 0..127
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int i = beg; i < end; ++i) {
+            const WorkItem it = args.items[i];
+            const DevProblem& P = args.probs[it.problem];
+            if (it.type == kItemGemm) {
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + ((uint32_t)(lgrp * 32) << 16) + (uint32_t)acc * kMaxBN;
+                const int nchunks = P.bn / 32;
+                const bool split = it.nsplit > 1;
+                float* part = split ? args.ws + (int64_t)it.ws_blk * kWsBlock + (int64_t)it.split * (kTileRows * P.bn)
+                                    : nullptr;
+                for (int c = 0; c < nchunks; ++c) {
+                    float v[32];
+                    tmem_ld32(taddr + (uint32_t)(c * 32), v);
+                    if (!split) {
+                        store_tile_chunk(P, it, trow, c, v);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) part[(c * 32 + j) * kTileRows + trow] = v[j];
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+                if (split) {
+                    // last-arriving split reduces all partials in split order (deterministic)
+                    __threadfence();
+                    named_bar_sync(1, 128);
+                    if (etid == 0) {
+                        const int prev = atomicAdd(args.counters + it.tile_slot, 1);
+                        *split_flag = (prev == it.nsplit - 1);
+                    }
+                    named_bar_sync(1, 128);
+                    if (*split_flag) {
+                        __threadfence();
+                        const float* base = args.ws + (int64_t)it.ws_blk * kWsBlock;
+                        for (int c = 0; c < nchunks; ++c) {
+                            float v[32];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                float s = 0.0f;
+                                for (int sp = 0; sp < it.nsplit; ++sp)
+                                    s += __ldcg(base + (int64_t)sp * (kTileRows * P.bn) + (c * 32 + j) * kTileRows + trow);
+                                v[j] = s;
+                            }
+                            store_tile_chunk(P, it, trow, c, v);
+                        }
+                        if (etid == 0) args.counters[it.tile_slot] = 0;   // re-arm for the next launch
+                    }
+                }
+            } else if (it.type == kItemGemv) {
+                if (P.in_dt == GMX_ST_F32)
+                    gemv_rows<float>(P, it.row0, it.col0, ew);
+                else
+                    gemv_rows<__nv_bfloat16>(P, it.row0, it.col0, ew);
+            } else {
+                if (P.in_dt == GMX_ST_F32)
+                    eltwise_range<float>(P, it.row0, it.col0, etid, 128);
+                else
+                    eltwise_range<__nv_bfloat16>(P, it.row0, it.col0, etid, 128);
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1 && has_gemm) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& m) {
+    g_err = m;
+    return code;
+}
+
+#define GMX_CUDA(call)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) return fail(GMX_ECUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// bf16 [rows x K] row-major operand, leading dim `ld` elements, boxes of 64 (K) x box_rows.
+static int make_tmap(CUtensorMap* map, const void* ptr, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return fail(GMX_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+    cuuint32_t box[2] = {(cuuint32_t)kBlockK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(GMX_EINVAL, "cuTensorMapEncodeTiled failed (alignment/stride?) code " + std::to_string((int)r));
+    return GMX_OK;
+}
+
+static int choose_bn(int64_t cols) {
+    const int64_t t = (cols + kMaxBN - 1) / kMaxBN;
+    const int64_t per = (cols + t - 1) / t;
+    return (int)std::min<int64_t>(kMaxBN, ((per + 31) / 32) * 32);
+}
+
+struct HostProblem {
+    DevProblem dev;
+    gmx_problem_desc desc;
+    bool live = false;
+    int64_t op_bytes = 0;   // algorithmic bytes (each operand + result once)
+    int64_t flops = 0;
+};
+
+struct Plan {
+    std::vector<WorkItem> items;
+    std::vector<int32_t> cta_off;
+    WorkItem* d_items = nullptr;
+    int32_t* d_off = nullptr;
+    bool uploaded = false;
+    int64_t ws_floats = 0;
+    int32_t n_counters = 0;
+    gmx_plan_stats stats{};
+    ~Plan() {
+        if (d_items) cudaFree(d_items);
+        if (d_off) cudaFree(d_off);
+    }
+};
+
+}  // namespace gmx
+
+struct gmx_exec {
+    int device = 0;
+    int num_sms = 148;
+    std::vector<gmx::HostProblem> probs;
+    gmx::DevProblem* d_probs = nullptr;
+    size_t d_cap = 0;
+    bool table_dirty = false;
+    std::map<std::vector<int32_t>, std::unique_ptr<gmx::Plan>> plans;
+    gmx::Plan* last = nullptr;
+    std::unique_ptr<gmx::Plan> uncached;
+    float* ws = nullptr;
+    int64_t ws_cap = 0;
+    int32_t* counters = nullptr;
+    int32_t counters_cap = 0;
+    int64_t max_split = 32;
+    bool cache_plans = true;
+    bool attr_set = false;
+};
+
+namespace gmx {
+
+static int ensure_table(gmx_exec* ex, cudaStream_t stream) {
+    if (!ex->table_dirty) return GMX_OK;
+    if (ex->probs.size() > ex->d_cap) {
+        size_t cap = std::max<size_t>(64, ex->d_cap);
+        while (cap < ex->probs.size()) cap *= 2;
+        if (ex->d_probs) GMX_CUDA(cudaFree(ex->d_probs));
+        GMX_CUDA(cudaMalloc(&ex->d_probs, cap * sizeof(DevProblem)));
+        ex->d_cap = cap;
+    }
+    std::vector<DevProblem> host(ex->probs.size());
+    for (size_t i = 0; i < host.size(); ++i) host[i] = ex->probs[i].dev;
+    GMX_CUDA(cudaMemcpy(ex->d_probs, host.data(), host.size() * sizeof(DevProblem), cudaMemcpyHostToDevice));
+    ex->table_dirty = false;
+    (void)stream;
+    return GMX_OK;
+}
+
+// Planner cost unit: bytes a work item moves between L2 and the SM (plus a fixed per-item
+// overhead), which is what bounds these HBM/L2-bound steps.
+static double gemm_tile_cost(const DevProblem& P, int kb) {
+    return (double)kb * (kTileRows + P.bn) * kBlockK * 2.0 + (double)kTileRows * P.bn * 2.0 + 16384.0;
+}
+
+static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& plan) {
+    struct Cand {
+        WorkItem it;
+        double cost;
+    };
+    std::vector<Cand> cands;
+    double total = 0.0;
+    gmx_plan_stats st{};
+    // pass 1: base items (no split) to size the per-SM target
+    struct TileRef { int32_t slot; int32_t r0, c0; double cost; };
+    std::vector<TileRef> tiles;
+    for (int32_t s : slots) {
+        const HostProblem& hp = ex->probs[s];
+        const DevProblem& P = hp.dev;
+        st.operand_bytes += hp.op_bytes;
+        st.flops += hp.flops;
+        if (P.kind == kItemGemm) {
+            for (int r0 = 0; r0 < P.rows; r0 += kTileRows)
+                for (int c0 = 0; c0 < P.cols; c0 += P.bn) {
+                    const double c = gemm_tile_cost(P, P.kblocks);
+                    tiles.push_back({s, r0, c0, c});
+                    total += c;
+                    st.tile_load_bytes += (int64_t)P.kblocks * (kTileRows + P.bn) * kBlockK * 2;
+                }
+        } else {
+            total += (double)hp.op_bytes;
+        }
+    }
+    const double target = std::max(total / ex->num_sms, 65536.0);
+    // GEMM tiles, split along K when one tile exceeds the per-SM share
+    int32_t n_counters = 0;
+    int64_t ws_blocks = 0;
+    for (const TileRef& t : tiles) {
+        const DevProblem& P = ex->probs[t.slot].dev;
+        int nsplit = 1;
+        if (t.cost > target && P.kblocks >= 2)
+            nsplit = (int)std::min<int64_t>({(int64_t)std::ceil(t.cost / target), (int64_t)P.kblocks, ex->max_split, 255});
+        ++st.n_gemm_tiles;
+        int32_t slot = -1, blk = 0;
+        if (nsplit > 1) {
+            slot = n_counters++;
+            blk = (int32_t)ws_blocks;
+            ws_blocks += ((int64_t)nsplit * kTileRows * P.bn + kWsBlock - 1) / kWsBlock;
+        }
+        for (int sp = 0; sp < nsplit; ++sp) {
+            WorkItem it{};
+            it.problem = t.slot;
+            it.type = kItemGemm;
+            it.nsplit = (uint8_t)nsplit;
+            it.split = (uint8_t)sp;
+            it.row0 = t.r0;
+            it.col0 = t.c0;
+            it.kb0 = (int32_t)((int64_t)P.kblocks * sp / nsplit);
+            it.kb1 = (int32_t)((int64_t)P.kblocks * (sp + 1) / nsplit);
+            it.tile_slot = slot;
+            it.ws_blk = blk;
+            const double c = gemm_tile_cost(P, it.kb1 - it.kb0) + (nsplit > 1 ? 2.0 * kTileRows * P.bn * 4 : 0.0);
+            cands.push_back({it, c});
+            if (nsplit > 1) ++st.n_split_items;
+        }
+    }
+    // CUDA-core items: chunk so no item exceeds about half the per-SM share
+    for (int32_t s : slots) {
+        const HostProblem& hp = ex->probs[s];
+        const DevProblem& P = hp.dev;
+        if (P.kind == kItemGemv) {
+            const double row_bytes = (double)P.cols * (P.in_dt == GMX_ST_F32 ? 4 : 2);
+            int rows_per = (int)std::max(4.0, std::floor(std::max(target * 0.5, 32768.0) / row_bytes));
+            rows_per = std::max(4, (rows_per / 4) * 4);
+            for (int r0 = 0; r0 < P.rows; r0 += rows_per) {
+                WorkItem it{};
+                it.problem = s;
+                it.type = kItemGemv;
+                it.row0 = r0;
+                it.col0 = std::min(P.rows, r0 + rows_per);
+                cands.push_back({it, row_bytes * (it.col0 - it.row0) + 4096.0});
+                ++st.n_gemv_items;
+            }
+        } else if (P.kind == kItemEltwise) {
+            const int esz = P.in_dt == GMX_ST_F32 ? 4 : 2;
+            int64_t per = (int64_t)std::max(32768.0, target * 0.5) / (2 * esz);
+            per = std::max<int64_t>(1024, (per / 1024) * 1024);
+            for (int64_t e0 = 0; e0 < P.rows; e0 += per) {
+                WorkItem it{};
+                it.problem = s;
+                it.type = kItemEltwise;
+                it.row0 = (int32_t)e0;
+                it.col0 = (int32_t)std::min<int64_t>(P.rows, e0 + per);
+                cands.push_back({it, 2.0 * esz * (it.col0 - it.row0) + 4096.0});
+                ++st.n_eltwise_items;
+            }
+        }
+    }
+    // LPT: longest item first onto the least-loaded CTA
+    std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.cost > b.cost; });
+    const int grid = (int)std::max<size_t>(1, std::min<size_t>((size_t)ex->num_sms, cands.size()));
+    std::vector<std::vector<int32_t>> per_cta(grid);
+    std::vector<double> load(grid, 0.0);
+    using QE = std::pair<double, int>;
+    std::priority_queue<QE, std::vector<QE>, std::greater<QE>> heap;
+    for (int c = 0; c < grid; ++c) heap.push({0.0, c});
+    for (size_t i = 0; i < cands.size(); ++i) {
+        QE top = heap.top();
+        heap.pop();
+        per_cta[top.second].push_back((int32_t)i);
+        load[top.second] += cands[i].cost;
+        heap.push({load[top.second], top.second});
+    }
+    plan.items.clear();
+    plan.cta_off.assign(1, 0);
+    for (int c = 0; c < grid; ++c) {
+        for (int32_t idx : per_cta[c]) plan.items.push_back(cands[idx].it);
+        plan.cta_off.push_back((int32_t)plan.items.size());
+    }
+    if (plan.items.empty()) {   // keep the device arrays non-empty
+        plan.cta_off.assign(2, 0);
+    }
+    st.grid = grid;
+    st.n_items = (int32_t)plan.items.size();
+    st.max_cta_cost = *std::max_element(load.begin(), load.end());
+    st.mean_cta_cost = std::accumulate(load.begin(), load.end(), 0.0) / grid;
+    plan.stats = st;
+    plan.ws_floats = ws_blocks * kWsBlock;
+    plan.n_counters = n_counters;
+    return GMX_OK;
+}
+
+static int upload_plan(gmx_exec* ex, Plan& plan, cudaStream_t stream) {
+    if (plan.uploaded) return GMX_OK;
+    const size_t ni = std::max<size_t>(1, plan.items.size());
+    GMX_CUDA(cudaMalloc(&plan.d_items, ni * sizeof(WorkItem)));
+    GMX_CUDA(cudaMalloc(&plan.d_off, plan.cta_off.size() * sizeof(int32_t)));
+    if (!plan.items.empty())
+        GMX_CUDA(cudaMemcpyAsync(plan.d_items, plan.items.data(), plan.items.size() * sizeof(WorkItem),
+                                 cudaMemcpyHostToDevice, stream));
+    GMX_CUDA(cudaMemcpyAsync(plan.d_off, plan.cta_off.data(), plan.cta_off.size() * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, stream));
+    plan.uploaded = true;
+    (void)ex;
+    return GMX_OK;
+}
+
+static int ensure_workspace(gmx_exec* ex, const Plan& plan) {
+    if (plan.ws_floats > ex->ws_cap) {
+        if (ex->ws) GMX_CUDA(cudaFree(ex->ws));
+        GMX_CUDA(cudaMalloc(&ex->ws, plan.ws_floats * sizeof(float)));
+        ex->ws_cap = plan.ws_floats;
+    }
+    if (plan.n_counters > ex->counters_cap) {
+        if (ex->counters) GMX_CUDA(cudaFree(ex->counters));
+        GMX_CUDA(cudaMalloc(&ex->counters, plan.n_counters * sizeof(int32_t)));
+        GMX_CUDA(cudaMemset(ex->counters, 0, plan.n_counters * sizeof(int32_t)));
+        ex->counters_cap = plan.n_counters;
+    }
+    return GMX_OK;
+}
+
+}  // namespace gmx
+
+using namespace gmx;
+
+extern "C" {
+
+int gmx_exec_create(int32_t device, gmx_exec** out) {
+    if (!out) return fail(GMX_EINVAL, "null argument");
+    int ndev = 0;
+    GMX_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(GMX_EINVAL, "no such CUDA device");
+    cudaDeviceProp prop;
+    GMX_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(GMX_ECUDA, std::string("executor targets sm_100a; device is ") + prop.name);
+    GMX_CUDA(cudaSetDevice(device));
+    auto* ex = new gmx_exec();
+    ex->device = device;
+    ex->num_sms = prop.multiProcessorCount;
+    *out = ex;
+    return GMX_OK;
+}
+
+void gmx_exec_destroy(gmx_exec* ex) {
+    if (!ex) return;
+    cudaSetDevice(ex->device);
+    ex->plans.clear();
+    ex->uncached.reset();
+    if (ex->d_probs) cudaFree(ex->d_probs);
+    if (ex->ws) cudaFree(ex->ws);
+    if (ex->counters) cudaFree(ex->counters);
+    delete ex;
+}
+
+int gmx_exec_num_sms(const gmx_exec* ex, int32_t* out) {
+    if (!ex || !out) return fail(GMX_EINVAL, "null argument");
+    *out = ex->num_sms;
+    return GMX_OK;
+}
+
+int gmx_exec_register(gmx_exec* ex, const gmx_problem_desc* d, int32_t* out_slot) {
+    if (!ex || !d || !out_slot) return fail(GMX_EINVAL, "null argument");
+    HostProblem hp;
+    hp.desc = *d;
+    DevProblem& P = hp.dev;
+    std::memset(&P, 0, sizeof P);
+    P.out = d->c;
+    P.bias = d->bias;
+    P.act = d->activation;
+    P.in_dt = d->in_dtype;
+    P.out_dt = d->out_dtype;
+    P.ld_out = d->ldc;
+    if (d->activation < GMX_ACT_NONE || d->activation > GMX_ACT_GELU) return fail(GMX_EINVAL, "unknown activation");
+    if ((d->in_dtype != GMX_ST_BF16 && d->in_dtype != GMX_ST_F32) ||
+        (d->out_dtype != GMX_ST_BF16 && d->out_dtype != GMX_ST_F32))
+        return fail(GMX_EINVAL, "unknown storage dtype");
+    if (!d->a || !d->c) return fail(GMX_EINVAL, "operand pointer is NULL");
+    const int64_t isz = d->in_dtype == GMX_ST_F32 ? 4 : 2, osz = d->out_dtype == GMX_ST_F32 ? 4 : 2;
+    if (d->op == GMX_OP_GEMM) {
+        if (d->in_dtype != GMX_ST_BF16) return fail(GMX_EINVAL, "gemm operands must be bf16");
+        if (d->m < 1 || d->n < 1 || d->k < 1) return fail(GMX_EINVAL, "gemm dims must be >= 1");
+        if (d->m >= (1 << 30) || d->n >= (1 << 30) || d->k >= (1 << 30)) return fail(GMX_EINVAL, "gemm dims too large");
+        if (!d->b) return fail(GMX_EINVAL, "gemm B operand is NULL");
+        if (d->lda < d->k || d->ldb < d->k || d->ldc < d->n) return fail(GMX_EINVAL, "leading dimension too small");
+        if (d->lda % 8 || d->ldb % 8) return fail(GMX_EINVAL, "lda/ldb must be multiples of 8 elements (TMA 16-byte strides)");
+        if ((reinterpret_cast<uintptr_t>(d->a) | reinterpret_cast<uintptr_t>(d->b)) & 15)
+            return fail(GMX_EINVAL, "A/B must be 16-byte aligned");
+        // orientation: the side that needs fewer (128 + BN) x K tile loads goes on UMMA-M
+        auto traffic = [](int64_t R, int64_t Cc) {
+            const int bn = choose_bn(Cc);
+            return ((R + kTileRows - 1) / kTileRows) * ((Cc + bn - 1) / bn) * (int64_t)(kTileRows + bn);
+        };
+        const bool swap = traffic(d->n, d->m) < traffic(d->m, d->n);
+        P.kind = kItemGemm;
+        P.swap = swap;
+        P.rows = (int32_t)(swap ? d->n : d->m);
+        P.cols = (int32_t)(swap ? d->m : d->n);
+        P.K = (int32_t)d->k;
+        P.bn = choose_bn(P.cols);
+        P.kblocks = (int32_t)((d->k + kBlockK - 1) / kBlockK);
+        const void* rows_ptr = swap ? d->b : d->a;
+        const void* cols_ptr = swap ? d->a : d->b;
+        const int64_t rows_ld = swap ? d->ldb : d->lda, cols_ld = swap ? d->lda : d->ldb;
+        int rc;
+        if ((rc = make_tmap(&P.tm_rows, rows_ptr, P.rows, d->k, rows_ld, kTileRows)) ||
+            (rc = make_tmap(&P.tm_cols, cols_ptr, P.cols, d->k, cols_ld, P.bn)))
+            return rc;
+        hp.op_bytes = 2 * (d->m * d->k + d->k * d->n) + osz * d->m * d->n;
+        hp.flops = 2 * d->m * d->n * d->k;
+    } else if (d->op == GMX_OP_GEMV) {
+        if (d->m < 1 || d->n < 1 || d->m >= (1 << 30) || d->n >= (1 << 30)) return fail(GMX_EINVAL, "bad gemv dims");
+        if (!d->b) return fail(GMX_EINVAL, "gemv x operand is NULL");
+        if (d->lda < d->n) return fail(GMX_EINVAL, "leading dimension too small");
+        P.kind = kItemGemv;
+        P.rows = (int32_t)d->m;
+        P.cols = (int32_t)d->n;
+        P.in0 = d->a;
+        P.in1 = d->b;
+        P.ld_in0 = d->lda;
+        hp.op_bytes = isz * (d->m * d->n + d->n) + osz * d->m;
+        hp.flops = 2 * d->m * d->n;
+    } else if (d->op == GMX_OP_ELEMENTWISE) {
+        if (d->m < 1 || d->m >= ((int64_t)1 << 31)) return fail(GMX_EINVAL, "bad elementwise length");
+        if (d->in_dtype != d->out_dtype) return fail(GMX_EINVAL, "elementwise keeps its dtype");
+        P.kind = kItemEltwise;
+        P.rows = (int32_t)d->m;
+        P.in0 = d->a;
+        hp.op_bytes = isz * d->m + osz * d->m;
+        hp.flops = d->m;
+    } else {
+        return fail(GMX_EINVAL, "unknown op");
+    }
+    hp.live = true;
+    int32_t slot = -1;
+    for (size_t i = 0; i < ex->probs.size(); ++i)
+        if (!ex->probs[i].live) { slot = (int32_t)i; break; }
+    if (slot < 0) {
+        slot = (int32_t)ex->probs.size();
+        ex->probs.push_back(hp);
+    } else {
+        ex->probs[slot] = hp;
+    }
+    ex->table_dirty = true;
+    *out_slot = slot;
+    return GMX_OK;
+}
+
+int gmx_exec_unregister(gmx_exec* ex, int32_t slot) {
+    if (!ex || slot < 0 || slot >= (int32_t)ex->probs.size() || !ex->probs[slot].live)
+        return fail(GMX_EINVAL, "bad slot");
+    ex->probs[slot].live = false;
+    // plans referencing the slot become invalid
+    for (auto it = ex->plans.begin(); it != ex->plans.end();) {
+        if (std::find(it->first.begin(), it->first.end(), slot) != it->first.end()) {
+            if (ex->last == it->second.get()) ex->last = nullptr;
+            it = ex->plans.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    return GMX_OK;
+}
+
+int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream_ptr) {
+    if (!ex || (n > 0 && !slots)) return fail(GMX_EINVAL, "null argument");
+    if (n == 0) return GMX_OK;
+    cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
+    std::vector<int32_t> key(slots, slots + n);
+    std::sort(key.begin(), key.end());
+    for (int32_t s : key)
+        if (s < 0 || s >= (int32_t)ex->probs.size() || !ex->probs[s].live) return fail(GMX_EINVAL, "bad slot");
+    int rc;
+    if ((rc = ensure_table(ex, stream))) return rc;
+    Plan* plan = nullptr;
+    bool cached = false;
+    if (ex->cache_plans) {
+        auto it = ex->plans.find(key);
+        if (it != ex->plans.end()) {
+            plan = it->second.get();
+            cached = true;
+        } else {
+            if (ex->plans.size() >= 512) ex->plans.clear(), ex->last = nullptr;
+            auto p = std::make_unique<Plan>();
+            if ((rc = build_plan(ex, key, *p))) return rc;
+            plan = p.get();
+            ex->plans.emplace(key, std::move(p));
+        }
+    } else {
+        ex->uncached = std::make_unique<Plan>();
+        if ((rc = build_plan(ex, key, *ex->uncached))) return rc;
+        plan = ex->uncached.get();
+    }
+    if ((rc = upload_plan(ex, *plan, stream)) || (rc = ensure_workspace(ex, *plan))) return rc;
+    if (!ex->attr_set) {
+        GMX_CUDA(cudaFuncSetAttribute(coalesced_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+        ex->attr_set = true;
+    }
+    KernelArgs args{ex->d_probs, plan->d_items, plan->d_off, ex->ws, ex->counters};
+    coalesced_step_kernel<<<plan->stats.grid, kThreads, kSmemBytes, stream>>>(args);
+    GMX_CUDA(cudaGetLastError());
+    plan->stats.cached = cached;
+    ex->last = plan;
+    return GMX_OK;
+}
+
+int gmx_exec_last_plan(const gmx_exec* ex, gmx_plan_stats* out) {
+    if (!ex || !out) return fail(GMX_EINVAL, "null argument");
+    if (!ex->last) return fail(GMX_ESTATE, "no launch yet");
+    *out = ex->last->stats;
+    return GMX_OK;
+}
+
+int gmx_exec_clear_plans(gmx_exec* ex) {
+    if (!ex) return fail(GMX_EINVAL, "null argument");
+    ex->plans.clear();
+    ex->last = nullptr;
+    return GMX_OK;
+}
+
+int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
+    if (!ex || !name) return fail(GMX_EINVAL, "null argument");
+    const std::string n(name);
+    if (n == "max_split") {
+        if (value < 1 || value > 255) return fail(GMX_EINVAL, "max_split must be in [1, 255]");
+        ex->max_split = value;
+    } else if (n == "cache_plans") {
+        ex->cache_plans = value != 0;
+    } else {
+        return fail(GMX_EINVAL, "unknown option " + n);
+    }
+    ex->plans.clear();
+    ex->last = nullptr;
+    return GMX_OK;
+}
+
+const char* gmx_exec_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,265 @@
+"""Coalesced B200 executor: one persistent sm_100a launch per scheduler step.
+
+The reference turns each dispatch into a simulated completion at
+`d.end` (gpumux/engine.py:359-364). Here a step's dispatches really run:
+
+    ex = Executor()                                # device = current CUDA device
+    ops = ex.operands_for(kernel)                  # or bring your own tensors
+    ex.bind(kernel.kernel_id, ex.register_gemm(a, bt, c, bias=..., activation="relu"))
+    ...
+    dispatches, withheld, wakeup = scheduler.step(now)
+    ex.launch_dispatches(dispatches)               # ONE kernel for all members of all dispatches
+
+Members run at their true dims (padding is only billed by the decision model).
+The work is done by libgmx_exec.so (include/gmx_exec.h); this module only
+validates torch tensors and marshals pointers. There is no CPU or eager
+fallback: without an sm_100 GPU or the library, construction raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _build, _lib
+
+ST = {torch.bfloat16: 0, torch.float32: 1}
+ACT = {"none": 0, "relu": 1, "gelu": 2}
+
+
+class ProblemDesc(C.Structure):
+    _fields_ = [("op", C.c_int32), ("in_dtype", C.c_int32), ("out_dtype", C.c_int32),
+                ("activation", C.c_int32), ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64),
+                ("a", C.c_void_p), ("lda", C.c_int64), ("b", C.c_void_p), ("ldb", C.c_int64),
+                ("c", C.c_void_p), ("ldc", C.c_int64), ("bias", C.c_void_p)]
+
+
+class PlanStats(C.Structure):
+    _fields_ = [("grid", C.c_int32), ("n_items", C.c_int32), ("n_gemm_tiles", C.c_int32),
+                ("n_split_items", C.c_int32), ("n_gemv_items", C.c_int32),
+                ("n_eltwise_items", C.c_int32), ("cached", C.c_int32), ("_pad", C.c_int32),
+                ("operand_bytes", C.c_int64), ("tile_load_bytes", C.c_int64),
+                ("flops", C.c_int64), ("max_cta_cost", C.c_double), ("mean_cta_cost", C.c_double)]
+
+
+EXEC_SIGNATURES = {
+    "gmx_exec_last_error": (C.c_char_p, []),
+    "gmx_exec_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
+    "gmx_exec_destroy": (None, [C.c_void_p]),
+    "gmx_exec_num_sms": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    "gmx_exec_register": (C.c_int, [C.c_void_p, C.POINTER(ProblemDesc), C.POINTER(C.c_int32)]),
+    "gmx_exec_unregister": (C.c_int, [C.c_void_p, C.c_int32]),
+    "gmx_exec_launch": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_void_p]),
+    "gmx_exec_last_plan": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
+    "gmx_exec_clear_plans": (C.c_int, [C.c_void_p]),
+    "gmx_exec_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
+}
+
+_exec_lib = None
+
+
+def exec_lib():
+    global _exec_lib
+    if _exec_lib is None:
+        lib = C.CDLL(_build.build_exec())
+        for name, (res, args) in EXEC_SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _exec_lib = lib
+    return _exec_lib
+
+
+def _check(rc):
+    if rc != 0:
+        msg = (exec_lib().gmx_exec_last_error() or b"").decode(errors="replace")
+        if rc == _lib.EINVAL:
+            raise ValueError(msg)
+        raise _lib.GmxError(f"executor error {rc}: {msg}")
+
+
+def padded_ld(k: int, dtype=torch.bfloat16) -> int:
+    """Leading dimension (elements) with 16-byte row strides, as TMA requires."""
+    per = 16 // torch.tensor([], dtype=dtype).element_size()
+    return (k + per - 1) // per * per
+
+
+class Executor:
+    """Registered member operands + the coalesced launch (libgmx_exec.so)."""
+
+    def __init__(self, device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("the coalesced executor needs a CUDA device (sm_100a)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        self._lib = exec_lib()
+        h = C.c_void_p()
+        _check(self._lib.gmx_exec_create(self.device.index, C.byref(h)))
+        self._h = h
+        self._keep = {}            # slot -> tensors kept alive while registered
+        self._kernel_slot = {}     # kernel_id -> slot
+        n = C.c_int32()
+        _check(self._lib.gmx_exec_num_sms(h, C.byref(n)))
+        self.num_sms = n.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._lib.gmx_exec_destroy(h)
+            self._h = None
+
+    # ---- registration ---------------------------------------------------------------
+
+    def _check_tensor(self, t, name, dtypes):
+        if t.device != self.device:
+            raise ValueError(f"{name} must live on {self.device}, got {t.device}")
+        if t.dtype not in dtypes:
+            raise ValueError(f"{name} dtype {t.dtype} not in {dtypes}")
+
+    def _register(self, desc, keep):
+        slot = C.c_int32()
+        _check(self._lib.gmx_exec_register(self._h, C.byref(desc), C.byref(slot)))
+        self._keep[slot.value] = keep
+        return slot.value
+
+    def register_gemm(self, a, bt, c, bias=None, activation="none", k=None):
+        """C[m,n] = act(A[m,k] . Bt[n,k]^T + bias[m]); A/Bt bf16 with row stride % 8 == 0."""
+        self._check_tensor(a, "A", (torch.bfloat16,))
+        self._check_tensor(bt, "Bt", (torch.bfloat16,))
+        self._check_tensor(c, "C", (torch.bfloat16, torch.float32))
+        m, n = c.shape
+        k = a.shape[1] if k is None else k
+        if a.shape[0] != m or bt.shape[0] != n or a.shape[1] < k or bt.shape[1] < k:
+            raise ValueError("gemm operand shapes disagree")
+        if a.stride(1) != 1 or bt.stride(1) != 1 or c.stride(1) != 1:
+            raise ValueError("gemm operands must be row-major (unit inner stride)")
+        d = ProblemDesc(op=_lib.OP_CODE["gemm"], in_dtype=0, out_dtype=ST[c.dtype],
+                        activation=ACT[activation], m=m, n=n, k=k, a=a.data_ptr(), lda=a.stride(0),
+                        b=bt.data_ptr(), ldb=bt.stride(0), c=c.data_ptr(), ldc=c.stride(0),
+                        bias=self._bias_ptr(bias, m))
+        return self._register(d, (a, bt, c, bias))
+
+    def register_gemv(self, w, x, y, bias=None, activation="none"):
+        """y[m] = act(W[m,n] . x[n] + bias[m]); fp32 or bf16."""
+        self._check_tensor(w, "W", (torch.bfloat16, torch.float32))
+        self._check_tensor(x, "x", (w.dtype,))
+        self._check_tensor(y, "y", (torch.bfloat16, torch.float32))
+        m, n = w.shape
+        if x.numel() != n or y.numel() != m or w.stride(1) != 1 or not x.is_contiguous() \
+                or not y.is_contiguous():
+            raise ValueError("gemv operand shapes/strides disagree")
+        d = ProblemDesc(op=_lib.OP_CODE["gemv"], in_dtype=ST[w.dtype], out_dtype=ST[y.dtype],
+                        activation=ACT[activation], m=m, n=n, k=1, a=w.data_ptr(), lda=w.stride(0),
+                        b=x.data_ptr(), ldb=0, c=y.data_ptr(), ldc=1, bias=self._bias_ptr(bias, m))
+        return self._register(d, (w, x, y, bias))
+
+    def register_elementwise(self, x, y, activation="none"):
+        """y[i] = act(x[i]) over contiguous tensors of one dtype."""
+        self._check_tensor(x, "x", (torch.bfloat16, torch.float32))
+        self._check_tensor(y, "y", (x.dtype,))
+        if x.numel() != y.numel() or not x.is_contiguous() or not y.is_contiguous():
+            raise ValueError("elementwise operands must be contiguous and equal-sized")
+        d = ProblemDesc(op=_lib.OP_CODE["elementwise"], in_dtype=ST[x.dtype], out_dtype=ST[y.dtype],
+                        activation=ACT[activation], m=x.numel(), n=1, k=1, a=x.data_ptr(), lda=0,
+                        b=None, ldb=0, c=y.data_ptr(), ldc=0, bias=None)
+        return self._register(d, (x, y))
+
+    def _bias_ptr(self, bias, m):
+        if bias is None:
+            return None
+        self._check_tensor(bias, "bias", (torch.float32,))
+        if bias.numel() != m or not bias.is_contiguous():
+            raise ValueError("bias must be a contiguous fp32 vector of length m")
+        return bias.data_ptr()
+
+    def unregister(self, slot: int):
+        _check(self._lib.gmx_exec_unregister(self._h, int(slot)))
+        self._keep.pop(slot, None)
+        for kid in [k for k, s in self._kernel_slot.items() if s == slot]:
+            del self._kernel_slot[kid]
+
+    def bind(self, kernel_id: int, slot: int):
+        """Associate a scheduler kernel id with registered operands."""
+        self._kernel_slot[kernel_id] = slot
+
+    def slot_of(self, kernel_id: int) -> int:
+        return self._kernel_slot[kernel_id]
+
+    # ---- execution ----------------------------------------------------------------------
+
+    def launch(self, slots, stream=None):
+        """One coalesced launch over the given registered slots (async on `stream`)."""
+        slots = list(slots)
+        arr = (C.c_int32 * max(1, len(slots)))(*slots)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(self._lib.gmx_exec_launch(self._h, arr, len(slots), C.c_void_p(s.cuda_stream)))
+
+    def launch_dispatches(self, dispatches, stream=None):
+        """Execute every member of every dispatch of one scheduler step in ONE launch."""
+        self.launch([self._kernel_slot[kid] for d in dispatches for kid in d.kernel_ids], stream)
+
+    def last_plan(self) -> dict:
+        st = PlanStats()
+        _check(self._lib.gmx_exec_last_plan(self._h, C.byref(st)))
+        return {name: getattr(st, name) for name, _ in PlanStats._fields_ if name != "_pad"}
+
+    def set_option(self, name: str, value: int):
+        _check(self._lib.gmx_exec_set_option(self._h, name.encode(), int(value)))
+
+    def clear_plans(self):
+        _check(self._lib.gmx_exec_clear_plans(self._h))
+
+
+class OperandSet:
+    """Synthetic per-kernel operands in the executor's HBM layout (bench / tests).
+
+    gemm:  A[m, lda] bf16 ~ N(0,1)/sqrt(k), Bt[n, ldb] bf16 ~ N(0,1), C[m, n]
+    gemv:  W[m, n] ~ U(-1,1), x[n] ~ U(-1,1), y[m]   (fp32 or bf16)
+    elementwise: x[n] ~ N(0,1), y[n]
+    lda/ldb are padded to 16-byte rows; the pad columns hold garbage (NaN) on
+    purpose so a kernel that reads past k is caught by the parity tests.
+    """
+
+    def __init__(self, op_kind, dims, dtype="fp16", device="cuda", seed=0, out_dtype=None,
+                 bias=False, activation="none"):
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        self.op_kind, self.dims, self.activation = op_kind, tuple(dims), activation
+        st = torch.bfloat16 if dtype == "fp16" else torch.float32
+        self.storage = st
+        if op_kind == "gemm":
+            m, n, k = dims
+            ld = padded_ld(k)
+            a = torch.full((m, ld), float("nan"), dtype=torch.bfloat16)
+            a[:, :k] = (torch.randn(m, k, generator=g) / k ** 0.5).to(torch.bfloat16)
+            bt = torch.full((n, ld), float("nan"), dtype=torch.bfloat16)
+            bt[:, :k] = torch.randn(n, k, generator=g).to(torch.bfloat16)
+            self.a, self.b = a.to(device), bt.to(device)
+            self.c = torch.empty(m, n, dtype=out_dtype or torch.bfloat16, device=device)
+            self.bias = (torch.randn(m, generator=g) * 0.1).to(device) if bias else None
+        elif op_kind == "gemv":
+            m, n = dims
+            self.a = (torch.rand(m, n, generator=g) * 2 - 1).to(st).to(device)
+            self.b = (torch.rand(n, generator=g) * 2 - 1).to(st).to(device)
+            self.c = torch.empty(m, dtype=out_dtype or st, device=device)
+            self.bias = (torch.randn(m, generator=g) * 0.1).to(device) if bias else None
+        else:
+            (n,) = dims
+            self.a = torch.randn(n, generator=g).to(st).to(device)
+            self.b = None
+            self.c = torch.empty(n, dtype=st, device=device)
+            self.bias = None
+
+    def register(self, ex: Executor) -> int:
+        if self.op_kind == "gemm":
+            return ex.register_gemm(self.a, self.b, self.c, self.bias, self.activation,
+                                    k=self.dims[2])
+        if self.op_kind == "gemv":
+            return ex.register_gemv(self.a, self.b, self.c, self.bias, self.activation)
+        return ex.register_elementwise(self.a, self.c, self.activation)
+
+    def host_inputs(self):
+        """CPU copies of the operands (for the oracle)."""
+        out = {"a": self.a.cpu(), "b": None if self.b is None else self.b.cpu(),
+               "bias": None if self.bias is None else self.bias.cpu()}
+        return out

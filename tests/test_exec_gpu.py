@@ -1,0 +1,178 @@
+"""GPU parity of the coalesced sm_100a executor against the numerics oracle.
+
+Every test launches through the product path (libgmx_exec.so via the C ABI)
+and compares with oracle/numerics.py on the same rounded operands.
+Tolerances (stated in oracle/numerics.py):
+  bf16 out: max|C-ref| <= 4e-3*max|ref| + 1e-6 ;  fp32 out: <= 1e-4*max|ref| + 1e-6
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import numerics as on  # noqa: E402
+
+C2_SHAPES = [(64, 3136, 147), (64, 3136, 64), (64, 3136, 576), (256, 3136, 64), (128, 784, 256),
+             (128, 784, 1152), (512, 784, 128), (256, 196, 512), (256, 196, 2304),
+             (1024, 196, 256), (512, 49, 1024), (512, 49, 4608), (2048, 49, 512)]
+
+
+@pytest.fixture(scope="module")
+def ex():
+    from paper_1901_10008_b200.executor import Executor
+    return Executor()
+
+
+def _np(t):
+    return t.detach().float().cpu().numpy()
+
+
+def _ref(ops):
+    if ops.op_kind == "gemm":
+        return on.gemm(_np(ops.a), _np(ops.b), ops.dims[2],
+                       None if ops.bias is None else _np(ops.bias), ops.activation)
+    if ops.op_kind == "gemv":
+        return on.gemv(_np(ops.a), _np(ops.b), None if ops.bias is None else _np(ops.bias),
+                       ops.activation)
+    return on.elementwise(_np(ops.a), ops.activation)
+
+
+def _check(ops):
+    got = _np(ops.c)
+    ref = _ref(ops)
+    bf = ops.c.dtype == torch.bfloat16
+    assert on.within(got, ref, bf), (ops.op_kind, ops.dims, on.rel_err(got, ref))
+
+
+def _run(ex, opsets):
+    slots = [o.register(ex) for o in opsets]
+    ex.launch(slots)
+    torch.cuda.synchronize()
+    try:
+        for o in opsets:
+            _check(o)
+    finally:
+        for s in slots:
+            ex.unregister(s)
+
+
+def test_single_gemm_basic(ex):
+    from paper_1901_10008_b200.executor import OperandSet
+    _run(ex, [OperandSet("gemm", (128, 128, 64), seed=1)])
+
+
+@pytest.mark.parametrize("dims", C2_SHAPES)
+def test_c2_shapes_each(ex, dims):
+    from paper_1901_10008_b200.executor import OperandSet
+    _run(ex, [OperandSet("gemm", dims, seed=hash(dims) % 1000)])
+
+
+@pytest.mark.parametrize("dims", [(1, 1, 1), (7, 5, 3), (130, 33, 65), (33, 130, 200), (300, 300, 8),
+                                  (129, 1000, 1000), (2048, 2048, 64), (16, 4096, 128),
+                                  (4096, 16, 128), (96, 96, 4608)])
+def test_ragged_gemm_shapes(ex, dims):
+    from paper_1901_10008_b200.executor import OperandSet
+    _run(ex, [OperandSet("gemm", dims, seed=sum(dims))])
+
+
+@pytest.mark.parametrize("act", ["relu", "gelu"])
+@pytest.mark.parametrize("out", [torch.bfloat16, torch.float32])
+def test_fused_bias_activation(ex, act, out):
+    from paper_1901_10008_b200.executor import OperandSet
+    _run(ex, [OperandSet("gemm", (256, 196, 512), seed=3, bias=True, activation=act, out_dtype=out),
+              OperandSet("gemm", (64, 3136, 147), seed=4, bias=True, activation=act, out_dtype=out),
+              OperandSet("gemm", (512, 49, 4608), seed=5, bias=True, activation=act, out_dtype=out)])
+
+
+def test_c2_coalesced_single_launch(ex):
+    from paper_1901_10008_b200.executor import OperandSet
+    ops = [OperandSet("gemm", C2_SHAPES[i % 13], seed=100 + i) for i in range(16)]
+    slots = [o.register(ex) for o in ops]
+    ex.launch(slots)
+    torch.cuda.synchronize()
+    plan = ex.last_plan()
+    assert plan["grid"] <= ex.num_sms and plan["n_items"] >= plan["n_gemm_tiles"]
+    for o in ops:
+        _check(o)
+    # repeated launches (cached plan, split-K counters re-armed) are bitwise identical
+    first = [o.c.clone() for o in ops]
+    for _ in range(3):
+        ex.launch(slots)
+    torch.cuda.synchronize()
+    assert ex.last_plan()["cached"] == 1
+    for o, f in zip(ops, first):
+        assert torch.equal(o.c, f)
+    for s in slots:
+        ex.unregister(s)
+
+
+def test_c1_gemv_fp32(ex):
+    from paper_1901_10008_b200.executor import OperandSet
+    _run(ex, [OperandSet("gemv", (1000, 2048), dtype="fp32", seed=10 + i) for i in range(4)])
+
+
+@pytest.mark.parametrize("dims,dtype", [((1024, 1024), "fp32"), ((1000, 2048), "fp16"),
+                                        ((33, 17), "fp32"), ((5, 3), "fp16")])
+def test_gemv_variants(ex, dims, dtype):
+    from paper_1901_10008_b200.executor import OperandSet
+    _run(ex, [OperandSet("gemv", dims, dtype=dtype, seed=7, bias=True, activation="relu")])
+
+
+@pytest.mark.parametrize("n,dtype,act", [(50176, "fp16", "gelu"), (802816, "fp32", "relu"),
+                                         (5, "fp32", "none"), (12345, "fp16", "relu")])
+def test_elementwise(ex, n, dtype, act):
+    from paper_1901_10008_b200.executor import OperandSet
+    _run(ex, [OperandSet("elementwise", (n,), dtype=dtype, seed=n, activation=act)])
+
+
+def test_mixed_kinds_one_launch(ex):
+    from paper_1901_10008_b200.executor import OperandSet
+    ops = [OperandSet("gemm", (256, 196, 512), seed=1), OperandSet("gemv", (1000, 2048), dtype="fp32", seed=2),
+           OperandSet("elementwise", (50176,), seed=3, activation="gelu"),
+           OperandSet("gemm", (64, 784, 256), seed=4), OperandSet("gemv", (1000, 2048), seed=5),
+           OperandSet("gemm", (512, 49, 4608), seed=6)]
+    _run(ex, ops)
+
+
+def test_split_k_disabled_matches(ex):
+    from paper_1901_10008_b200.executor import OperandSet
+    ex.set_option("max_split", 1)
+    try:
+        _run(ex, [OperandSet("gemm", (512, 49, 4608), seed=11)])
+    finally:
+        ex.set_option("max_split", 32)
+
+
+def test_scheduler_step_drives_one_launch(ex):
+    """OoO decisions (native core) -> one coalesced launch for all dispatched members."""
+    import paper_1901_10008_b200 as gm
+    from paper_1901_10008_b200.executor import OperandSet
+    prof = gm.load_profile("b200")
+    sched = gm.Scheduler(prof, gm.SchedulerPolicy("ooo"))
+    ops = {}
+    for i in range(16):
+        dims = C2_SHAPES[i % 13]
+        k = gm.KernelSpec(i, f"t{i:02d}", "gemm", dims, "fp16", arrival=0, deadline=10_000_000)
+        sched.add_request(gm.InferenceRequest(i, k.stream_id, (k,), 0, gm.LatencyConstraint(10_000_000)))
+        o = OperandSet("gemm", dims, seed=200 + i)
+        ex.bind(i, o.register(ex))
+        ops[i] = o
+    now, done = 0, set()
+    for _ in range(64):
+        dispatches, _held, wake = sched.step(now)
+        if dispatches:
+            ex.launch_dispatches(dispatches)
+            torch.cuda.synchronize()
+            for d in dispatches:
+                sched.complete(d.dispatch_id, d.end)
+                done.update(d.kernel_ids)
+            now = max(d.end for d in dispatches)
+        elif wake is not None:
+            now = wake
+        if len(done) == 16:
+            break
+    assert done == set(range(16))
+    for o in ops.values():
+        _check(o)
