@@ -96,8 +96,14 @@ int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream)
 int gmx_exec_last_plan(const gmx_exec* ex, gmx_plan_stats* out);
 /* Drop cached plans (e.g. after unregistering many slots). */
 int gmx_exec_clear_plans(gmx_exec* ex);
-/* Planner knobs: max split-K factor (1 disables split-K), plan cache on/off. */
+/* Knobs: "max_split" (1 disables split-K), "cache_plans" (0/1), "trace" (0/1: the kernel
+ * stamps %globaltimer per work item: producer start, last UMMA issued, epilogue start, end,
+ * then epilogue sub-phases: staging start, staged, barrier, store issued). */
 int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value);
+/* Copy the last traced launch: stamps[8*n_items], items[8*n_items] (raw 32-byte work items),
+ * cta_off[grid+1]. Call with capacity 0 to query sizes. Synchronizes the device. */
+int gmx_exec_read_trace(const gmx_exec* ex, uint64_t* stamps, int32_t* items, int32_t* cta_off,
+                        int32_t capacity, int32_t* n_items, int32_t* grid);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,66 @@
+/*
+ * gmx_runtime.h — native driver loop: scheduler decisions -> coalesced launches.
+ *
+ * Restates the reference's event loop (gpumux/engine.py:320-367) natively so a
+ * serving step costs no Python: all events at one timestamp are drained
+ * (COMPLETE before ARRIVAL before WAKEUP, ascending id), then the scheduler
+ * steps once; the members of every dispatch returned by that step are executed
+ * by ONE gmx_exec_launch; each dispatch's completion event is queued at d.end
+ * and the wakeup (if any) as a WAKEUP event.
+ *
+ * Mode GMX_RT_LOCKSTEP: virtual time, completions at the decision model's
+ * d.end (the reference's clock) — decisions are bit-identical to the
+ * reference engine for the same arrivals, while the launches really run on
+ * the GPU, back to back on the caller's stream.
+ *
+ * Straggler eviction (engine.py:345-351) is not run by this loop: in lockstep
+ * mode observed == predicted, so no stream can exceed the threshold.
+ */
+#ifndef GMX_RUNTIME_H
+#define GMX_RUNTIME_H
+
+#include <stdint.h>
+
+#include "gmx_core.h"
+#include "gmx_exec.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GMX_RT_LOCKSTEP 0
+
+typedef struct gmx_runtime gmx_runtime;
+
+typedef struct gmx_runtime_stats {
+    int64_t now;                 /* virtual time after the run */
+    int64_t steps;               /* scheduler steps taken */
+    int64_t launches;            /* coalesced kernel launches issued */
+    int64_t dispatches;          /* superkernels dispatched */
+    int64_t kernels;             /* member kernels executed */
+    int64_t withheld;            /* clusters withheld */
+    int64_t completed_requests;
+    int64_t useful_flops;        /* padding excluded (engine.py:425) */
+    int64_t slo_misses;          /* completions after the request deadline */
+} gmx_runtime_stats;
+
+/* Borrows `sched` and `ex` (caller keeps them alive). */
+int gmx_runtime_create(gmx_sched* sched, gmx_exec* ex, int32_t mode, gmx_runtime** out);
+void gmx_runtime_destroy(gmx_runtime* rt);
+/* Queue one request's ARRIVAL (engine.py:316-318) and bind each kernel id to
+ * the executor slot holding its operands. CSR deps as in gmx_sched_add_request. */
+int gmx_runtime_submit(gmx_runtime* rt, int64_t request_id, int32_t stream, int64_t arrival,
+                       int64_t deadline, const gmx_kernel_desc* kernels, int32_t n,
+                       const int64_t* dep_ids, const int32_t* dep_offsets, const int32_t* slots);
+/* Run the event loop until the heap is empty or the next event is later than
+ * `until`; launches go to `cuda_stream`. Accumulates into the runtime's stats. */
+int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* cuda_stream, gmx_runtime_stats* out);
+/* Completion records since the last call: request id and virtual completion time. */
+int gmx_runtime_drain_completions(gmx_runtime* rt, int64_t* request_ids, int64_t* times,
+                                  int32_t capacity, int32_t* n_out);
+const char* gmx_runtime_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GMX_RUNTIME_H */

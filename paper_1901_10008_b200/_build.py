@@ -56,7 +56,7 @@ def build_core(force=False):
     tmp = CORE_SO + ".tmp"
     _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-ffp-contract=off",
           "-fno-fast-math", "-Wall", "-Wextra", "-Wno-unused-parameter",
-          "-I", INCLUDE, *srcs, "-o", tmp])
+          "-Wl,-soname,libgmx_core.so", "-I", INCLUDE, *srcs, "-o", tmp])
     os.replace(tmp, CORE_SO)
     return CORE_SO
 
@@ -70,7 +70,9 @@ def nvcc_path():
 
 def build_exec(force=False, verbose_ptxas=False):
     srcs = _sources("exec", (".cu",)) + _sources("exec", (".cpp",))
-    deps = srcs + _sources("exec", (".cuh", ".hpp", ".h")) + [os.path.join(INCLUDE, "gmx_exec.h")]
+    core = build_core()
+    deps = srcs + _sources("exec", (".cuh", ".hpp", ".h")) + [
+        os.path.join(INCLUDE, h) for h in ("gmx_exec.h", "gmx_runtime.h", "gmx_core.h")] + [core]
     if not force and not _stale(EXEC_SO, deps):
         return EXEC_SO
     os.makedirs(LIB_DIR, exist_ok=True)
@@ -78,7 +80,8 @@ def build_exec(force=False, verbose_ptxas=False):
     cmd = [nvcc_path(), *NVCC_ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared",
            "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
            "--expt-relaxed-constexpr", "-cudart", "static",
-           "-I", INCLUDE, *srcs, "-o", tmp, "-lcuda" if False else "-ldl"]
+           "-I", INCLUDE, *srcs, "-o", tmp, "-L", LIB_DIR, "-lgmx_core",
+           "-Xlinker", "-rpath,$ORIGIN", "-ldl"]
     if verbose_ptxas:
         cmd.insert(1, "-Xptxas=-v")
     log = _run(cmd)

@@ -57,12 +57,14 @@ constexpr int kStageA = kTileRows * kBlockK * 2;   // 16 KB
 constexpr int kStageB = kMaxBN * kBlockK * 2;      // 16 KB
 constexpr int kStageBytes = kStageA + kStageB;
 constexpr int kTmemCols = 256;             // 2 accumulators x 128 fp32 columns
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kStageOut = 32 * 1024;       // epilogue staging tile for TMA stores
+constexpr int kSmemBytes = kStages * kStageBytes + kStageOut + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int kWsBlock = 4096;             // split-K workspace allocation unit (floats)
 
 struct alignas(64) DevProblem {
     CUtensorMap tm_rows;     // operand on the UMMA-M side (128-row boxes)
     CUtensorMap tm_cols;     // operand on the UMMA-N side (BN-row boxes)
+    CUtensorMap tm_out;      // output C[m][n]: 128-byte-wide boxes, SWIZZLE_128B (if tma_out)
     void* out;
     const void* in0;         // gemv W / eltwise x
     const void* in1;         // gemv x
@@ -79,7 +81,8 @@ struct alignas(64) DevProblem {
     int32_t in_dt;
     int32_t out_dt;
     int32_t kblocks;
-    int32_t _pad[6];
+    int32_t tma_out;         // 1: epilogue stages the tile in smem and TMA-stores it
+    int32_t _pad[5];
 };
 static_assert(sizeof(DevProblem) % 64 == 0, "DevProblem must keep 64-byte tensor map alignment");
 
@@ -101,8 +104,10 @@ struct KernelArgs {
     const DevProblem* probs;
     const WorkItem* items;
     const int32_t* cta_off;
+    const int32_t* cta_flags;
     float* ws;
     int32_t* counters;
+    uint64_t* trace;         // optional: 4 globaltimer stamps per item (debug/profiling)
 };
 
 __device__ __forceinline__ float apply_act(float x, int32_t act) {
@@ -123,22 +128,74 @@ __device__ __forceinline__ void store_one(void* out, int64_t idx, int32_t dt, fl
         reinterpret_cast<float*>(out)[idx] = v;
 }
 
-// Write 32 accumulator columns of the thread's tile row to the output.
-__device__ __forceinline__ void store_tile_chunk(const DevProblem& P, const WorkItem& it, int trow, int c,
-                                                 float (&v)[32]) {
-    const int gr = it.row0 + trow;                  // M-side index
-    if (gr >= P.rows) return;
-    const int gc0 = it.col0 + c * 32;               // N-side index of v[0]
-    const int nvalid = min(32, P.cols - gc0);
-    if (nvalid <= 0) return;
-    if (!P.swap) {
-        // gr = m (output row), columns = n: contiguous in memory
-        const float b = P.bias ? __ldg(P.bias + gr) : 0.0f;
+// Epilogue parameters copied out of the (global) problem descriptor once per item so the
+// compiler keeps them in registers: stores to the output may alias global memory, so reading
+// DevProblem fields inside the store loops would re-load them after every store.
+struct EpiParams {
+    void* out;
+    const float* bias;
+    const CUtensorMap* tm_out;
+    int64_t ld_out;
+    int32_t swap, rows, cols, bn, act, out_dt, tma_out;
+};
+
+__device__ __forceinline__ EpiParams load_epi(const DevProblem* P) {
+    EpiParams e;
+    e.tm_out = &P->tm_out;
+    e.tma_out = P->tma_out;
+    e.out = P->out;
+    e.bias = P->bias;
+    e.ld_out = P->ld_out;
+    e.swap = P->swap;
+    e.rows = P->rows;
+    e.cols = P->cols;
+    e.bn = P->bn;
+    e.act = P->act;
+    e.out_dt = P->out_dt;
+    return e;
+}
+
+__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+
+// bias + activation over one 32-column accumulator chunk, with every branch hoisted out of
+// the (fully unrolled) element loops: the epilogue runs one warp per SMSP, so per-element
+// control flow would be paid at full latency.
+//   non-swap: the chunk is one output row m (bias[m] scalar)
+//   swap:     the chunk is 32 output rows m0..m0+31 (bias per element)
+__device__ __forceinline__ void transform_chunk(float (&v)[32], const EpiParams& E, int m, bool swap) {
+    if (E.bias) {
+        if (!swap) {
+            const float b = m < E.rows ? __ldg(E.bias + m) : 0.0f;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j] + b, P.act);
-        const int64_t base = (int64_t)gr * P.ld_out + gc0;
-        if (P.out_dt == GMX_ST_BF16) {
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(P.out) + base;
+            for (int j = 0; j < 32; ++j) v[j] += b;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += (m + j < E.cols) ? __ldg(E.bias + m + j) : 0.0f;
+        }
+    }
+    if (E.act == GMX_ACT_RELU) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+    } else if (E.act == GMX_ACT_GELU) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+    }
+}
+
+// Write 32 accumulator columns of the thread's tile row to the output.
+__device__ __forceinline__ void store_tile_chunk(const EpiParams& E, int row0, int col0, int trow, int c,
+                                                 float (&v)[32]) {
+    const int gr = row0 + trow;                     // M-side index
+    if (gr >= E.rows) return;
+    const int gc0 = col0 + c * 32;                  // N-side index of v[0]
+    const int nvalid = min(32, E.cols - gc0);
+    if (nvalid <= 0) return;
+    transform_chunk(v, E, E.swap ? gc0 : gr, E.swap);
+    if (!E.swap) {
+        // gr = m (output row), columns = n: contiguous in memory
+        const int64_t base = (int64_t)gr * E.ld_out + gc0;
+        if (E.out_dt == GMX_ST_BF16) {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(E.out) + base;
             if (nvalid == 32 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
                 uint4* o4 = reinterpret_cast<uint4*>(o);
 #pragma unroll
@@ -148,7 +205,7 @@ __device__ __forceinline__ void store_tile_chunk(const DevProblem& P, const Work
                 return;
             }
         } else {
-            float* o = reinterpret_cast<float*>(P.out) + base;
+            float* o = reinterpret_cast<float*>(E.out) + base;
             if (nvalid == 32 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
                 float4* o4 = reinterpret_cast<float4*>(o);
 #pragma unroll
@@ -158,16 +215,144 @@ __device__ __forceinline__ void store_tile_chunk(const DevProblem& P, const Work
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j)
-            if (j < nvalid) store_one(P.out, base + j, P.out_dt, v[j]);
+            if (j < nvalid) store_one(E.out, base + j, E.out_dt, v[j]);
     } else {
         // gr = n (output column), columns = m (output rows): lanes write consecutive n
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            if (j < nvalid) {
-                const int m = gc0 + j;
-                const float b = P.bias ? __ldg(P.bias + m) : 0.0f;
-                store_one(P.out, (int64_t)m * P.ld_out + gr, P.out_dt, apply_act(v[j] + b, P.act));
+        for (int j = 0; j < 32; ++j)
+            if (j < nvalid) store_one(E.out, (int64_t)(gc0 + j) * E.ld_out + gr, E.out_dt, v[j]);
+    }
+}
+
+// Split-K workspace layout of one output tile: [split][column][row (128)] fp32, so a warp's
+// access for one column is one coalesced 128-byte line (lanes = consecutive tile rows).
+__device__ __forceinline__ float* ws_chunk(float* tile_base, int bn, int sp, int c, int trow) {
+    return tile_base + (int64_t)sp * kTileRows * bn + (int64_t)(c * 32) * kTileRows + trow;
+}
+
+__device__ __forceinline__ void ws_store_chunk(float* dst, const float (&v)[32]) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) __stcg(dst + j * kTileRows, v[j]);
+}
+
+// Sum the chunk over all splits in split order (deterministic) with two splits' loads in
+// flight per round (64 independent coalesced loads per thread).
+__device__ __forceinline__ void ws_reduce_chunk(const float* tile_base, int bn, int nsplit, int c, int trow,
+                                                float (&v)[32]) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+    for (int sp = 0; sp < nsplit; sp += 2) {
+        const float* pa = ws_chunk(const_cast<float*>(tile_base), bn, sp, c, trow);
+        float a[32], b[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) a[j] = __ldcg(pa + j * kTileRows);
+        if (sp + 1 < nsplit) {
+            const float* pb = pa + (int64_t)kTileRows * bn;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) b[j] = __ldcg(pb + j * kTileRows);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = (v[j] + a[j]) + b[j];
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += a[j];
+        }
+    }
+}
+
+// Staged epilogue: accumulator chunks (32 columns each) -> bias/activation -> bf16/fp32 ->
+// SWIZZLE_128B smem staging laid out exactly as the output TMA box -> cp.async.bulk.tensor
+// store. Chunks come from TMEM (kFromTmem: the accumulator is released to the MMA warp right
+// after its last tcgen05.ld) or from the split-K workspace (reduced in split order).
+//   non-swap: tile rows = m (128), chunk = 32 n-columns; box {128 B of n, 128 m-rows}
+//   swap:     tile rows = n (128), chunk = 32 m-rows;    box {128 B of n, 32 m-rows}
+template <bool kFromTmem>
+__device__ __forceinline__ void epilogue_staged(const EpiParams& E, int row0, int col0, uint8_t* stg, int trow,
+                                                int etid, uint32_t taddr, const float* ws_base, int nsplit,
+                                                uint64_t* tempty_bar, uint64_t* tr = nullptr) {
+    const int esz = E.out_dt == GMX_ST_BF16 ? 2 : 4;
+    const int inner = 128 / esz;                      // elements per 128-byte box row
+    const int nchunks = E.bn / 32;
+    const int chunk_bytes = 128 * 32 * esz;
+    const int per_pass = kStageOut / chunk_bytes;     // 4 (bf16) or 2 (fp32)
+    const int64_t tile_floats = (int64_t)kTileRows * E.bn;
+    const uint32_t stg_u32 = smem_u32(stg);
+    const int lane = lane_id();
+    for (int c0 = 0; c0 < nchunks; c0 += per_pass) {
+        const int cend = min(nchunks, c0 + per_pass);
+        float vbuf[32];
+        // staging must be free: the previous TMA store has finished reading it
+        if (etid == 0) bulk_wait_read0();
+        named_bar_sync(3, 128);
+        if (tr && etid == 0 && c0 == 0) tr[4] = global_timer_ns();
+        for (int c = c0; c < cend; ++c) {
+            float (&v)[32] = vbuf;
+            if constexpr (kFromTmem) {
+                tmem_ld32(taddr + (uint32_t)(c * 32), v);
+                if (c == nchunks - 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty_bar);
+                }
+            } else {
+                ws_reduce_chunk(ws_base, E.bn, nsplit, c, trow, v);
             }
+            const int slot = c - c0;
+            transform_chunk(v, E, E.swap ? col0 + c * 32 : row0 + trow, E.swap);
+            if (!E.swap) {
+                const uint32_t row_base = (uint32_t)trow * 128u;
+                const uint32_t sw = (uint32_t)(trow & 7);
+                if (esz == 2) {
+                    const uint32_t sub = stg_u32 + (uint32_t)(slot >> 1) * 16384u + row_base;
+                    const uint32_t h = (uint32_t)(slot & 1) * 4u;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        st_shared_v4(sub + (((h + q) ^ sw) << 4), pack_bf16x2(v[8 * q], v[8 * q + 1]),
+                                     pack_bf16x2(v[8 * q + 2], v[8 * q + 3]), pack_bf16x2(v[8 * q + 4], v[8 * q + 5]),
+                                     pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+                } else {
+                    const uint32_t sub = stg_u32 + (uint32_t)slot * 16384u + row_base;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        st_shared_v4(sub + (((uint32_t)q ^ sw) << 4), __float_as_uint(v[4 * q]),
+                                     __float_as_uint(v[4 * q + 1]), __float_as_uint(v[4 * q + 2]),
+                                     __float_as_uint(v[4 * q + 3]));
+                }
+            } else {
+                const uint32_t sb = (uint32_t)(trow / inner);
+                const uint32_t byte = (uint32_t)(trow % inner) * (uint32_t)esz;
+                const uint32_t base = stg_u32 + (uint32_t)slot * (uint32_t)chunk_bytes + sb * 4096u + (byte & 15u);
+                const uint32_t unit = byte >> 4;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t addr = base + (uint32_t)j * 128u + ((unit ^ (uint32_t)(j & 7)) << 4);
+                    if (esz == 2)
+                        st_shared_u16(addr, __bfloat16_as_ushort(__float2bfloat16_rn(v[j])));
+                    else
+                        st_shared_f32(addr, v[j]);
+                }
+            }
+        }
+        if (tr && etid == 0 && c0 == 0) tr[5] = global_timer_ns();
+        fence_async_smem();
+        named_bar_sync(3, 128);
+        if (tr && etid == 0 && c0 == 0) tr[6] = global_timer_ns();
+        if (etid == 0) {
+            for (int c = c0; c < cend; ++c) {
+                const int slot = c - c0;
+                if (!E.swap) {
+                    if (esz == 2) {
+                        if ((slot & 1) == 0)
+                            tma_store_2d(E.tm_out, stg + (slot >> 1) * 16384, col0 + c * 32, row0);
+                    } else {
+                        tma_store_2d(E.tm_out, stg + slot * 16384, col0 + c * 32, row0);
+                    }
+                } else {
+                    for (int sb = 0; sb < 128 / inner; ++sb)
+                        tma_store_2d(E.tm_out, stg + slot * chunk_bytes + sb * 4096, row0 + sb * inner, col0 + c * 32);
+                }
+            }
+            bulk_commit();
+            if (tr && c0 == 0) tr[7] = global_timer_ns();
         }
     }
 }
@@ -193,16 +378,20 @@ __device__ __forceinline__ float dot_v4(uint4 w, uint4 x, __nv_bfloat16) {
 // y[r] for r in [r0, r1): each epilogue warp owns every 4th row; 16-byte streaming loads of W
 // with 4 outstanding per lane, x re-read through L1.
 template <typename T>
-__device__ void gemv_rows(const DevProblem& P, int r0, int r1, int ew) {
-    const T* W = reinterpret_cast<const T*>(P.in0);
-    const T* x = reinterpret_cast<const T*>(P.in1);
-    const int n = P.cols;
+__device__ void gemv_rows(const DevProblem* Pg, int r0, int r1, int ew) {
+    const T* __restrict__ W = reinterpret_cast<const T*>(Pg->in0);
+    const T* __restrict__ x = reinterpret_cast<const T*>(Pg->in1);
+    const int n = Pg->cols;
+    const int64_t ld = Pg->ld_in0;
+    void* out = Pg->out;
+    const float* bias = Pg->bias;
+    const int32_t act = Pg->act, out_dt = Pg->out_dt;
     constexpr int kVec = 16 / sizeof(T);
     const int lane = lane_id();
-    const bool vec_ok = (n % kVec == 0) && (P.ld_in0 % kVec == 0) &&
+    const bool vec_ok = (n % kVec == 0) && (ld % kVec == 0) &&
                         ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(x)) & 15) == 0;
     for (int r = r0 + ew; r < r1; r += 4) {
-        const T* w = W + (int64_t)r * P.ld_in0;
+        const T* w = W + (int64_t)r * ld;
         float acc = 0.0f;
         if (vec_ok) {
             const int nv = n / kVec;
@@ -224,16 +413,17 @@ __device__ void gemv_rows(const DevProblem& P, int r0, int r1, int ew) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) {
-            const float b = P.bias ? __ldg(P.bias + r) : 0.0f;
-            store_one(P.out, r, P.out_dt, apply_act(acc + b, P.act));
+            const float b = bias ? __ldg(bias + r) : 0.0f;
+            store_one(out, r, out_dt, apply_act(acc + b, act));
         }
     }
 }
 
 template <typename T>
-__device__ void eltwise_range(const DevProblem& P, int e0, int e1, int tid, int nthreads) {
-    const T* x = reinterpret_cast<const T*>(P.in0);
-    T* y = reinterpret_cast<T*>(P.out);
+__device__ void eltwise_range(const DevProblem* Pg, int e0, int e1, int tid, int nthreads) {
+    const T* __restrict__ x = reinterpret_cast<const T*>(Pg->in0);
+    T* __restrict__ y = reinterpret_cast<T*>(Pg->out);
+    const int32_t act = Pg->act;
     constexpr int kVec = 16 / sizeof(T);
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0 &&
                         (e0 % kVec) == 0;
@@ -244,22 +434,22 @@ __device__ void eltwise_range(const DevProblem& P, int e0, int e1, int tid, int 
             const int64_t idx = (int64_t)e0 + (int64_t)v * kVec;
             uint4 u = ld_stream_v4(x + idx);
             if constexpr (sizeof(T) == 4) {
-                u.x = __float_as_uint(apply_act(__uint_as_float(u.x), P.act));
-                u.y = __float_as_uint(apply_act(__uint_as_float(u.y), P.act));
-                u.z = __float_as_uint(apply_act(__uint_as_float(u.z), P.act));
-                u.w = __float_as_uint(apply_act(__uint_as_float(u.w), P.act));
+                u.x = __float_as_uint(apply_act(__uint_as_float(u.x), act));
+                u.y = __float_as_uint(apply_act(__uint_as_float(u.y), act));
+                u.z = __float_as_uint(apply_act(__uint_as_float(u.z), act));
+                u.w = __float_as_uint(apply_act(__uint_as_float(u.w), act));
             } else {
-                u.x = pack_bf16x2(apply_act(bf_lo(u.x), P.act), apply_act(bf_hi(u.x), P.act));
-                u.y = pack_bf16x2(apply_act(bf_lo(u.y), P.act), apply_act(bf_hi(u.y), P.act));
-                u.z = pack_bf16x2(apply_act(bf_lo(u.z), P.act), apply_act(bf_hi(u.z), P.act));
-                u.w = pack_bf16x2(apply_act(bf_lo(u.w), P.act), apply_act(bf_hi(u.w), P.act));
+                u.x = pack_bf16x2(apply_act(bf_lo(u.x), act), apply_act(bf_hi(u.x), act));
+                u.y = pack_bf16x2(apply_act(bf_lo(u.y), act), apply_act(bf_hi(u.y), act));
+                u.z = pack_bf16x2(apply_act(bf_lo(u.z), act), apply_act(bf_hi(u.z), act));
+                u.w = pack_bf16x2(apply_act(bf_lo(u.w), act), apply_act(bf_hi(u.w), act));
             }
             *reinterpret_cast<uint4*>(y + idx) = u;
         }
         i = e0 + nvec * kVec;
     }
     for (int j = i + tid; j < e1; j += nthreads) {
-        const float v = apply_act(load_f<T>(x + j), P.act);
+        const float v = apply_act(load_f<T>(x + j), act);
         store_one(y, j, sizeof(T) == 4 ? GMX_ST_F32 : GMX_ST_BF16, v);
     }
 }
@@ -267,7 +457,8 @@ __device__ void eltwise_range(const DevProblem& P, int e0, int e1, int tid, int 
 __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const KernelArgs args) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint8_t* stg = smem + kStages * kStageBytes;                       // epilogue staging (1024-aligned)
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes + kStageOut);
     uint64_t* empty = full + kStages;
     uint64_t* tfull = empty + kStages;
     uint64_t* tempty = tfull + 2;
@@ -279,8 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
     const int beg = args.cta_off[blockIdx.x];
     const int end = args.cta_off[blockIdx.x + 1];
 
-    bool has_gemm = false;
-    for (int i = beg; i < end; ++i) has_gemm |= args.items[i].type == kItemGemm;
+    const bool has_gemm = (args.cta_flags[blockIdx.x] & 1) != 0;   // host-computed: CTA owns GEMM tiles
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -309,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
                 if (it.type != kItemGemm) continue;
                 const DevProblem* P = args.probs + it.problem;
                 const uint32_t bytes = kStageA + (uint32_t)P->bn * (kBlockK * 2);
+                if (args.trace) args.trace[8 * i + 0] = global_timer_ns();
                 for (int kb = it.kb0; kb < it.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* tile = smem + stage * kStageBytes;
@@ -344,6 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
                 umma_commit(&tfull[acc]);
+                if (args.trace) args.trace[8 * i + 1] = global_timer_ns();
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
@@ -358,68 +550,85 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
         uint32_t acc_phase = 0;
         for (int i = beg; i < end; ++i) {
             const WorkItem it = args.items[i];
-            const DevProblem& P = args.probs[it.problem];
+            const DevProblem* Pg = args.probs + it.problem;
+            if (args.trace && etid == 0 && it.type != kItemGemm) args.trace[8 * i + 0] = global_timer_ns();
             if (it.type == kItemGemm) {
+                const EpiParams E = load_epi(Pg);
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
+                if (args.trace && etid == 0) args.trace[8 * i + 2] = global_timer_ns();
                 const uint32_t taddr = tmem_base + ((uint32_t)(lgrp * 32) << 16) + (uint32_t)acc * kMaxBN;
-                const int nchunks = P.bn / 32;
+                const int nchunks = E.bn / 32;
                 const bool split = it.nsplit > 1;
-                float* part = split ? args.ws + (int64_t)it.ws_blk * kWsBlock + (int64_t)it.split * (kTileRows * P.bn)
-                                    : nullptr;
-                for (int c = 0; c < nchunks; ++c) {
-                    float v[32];
-                    tmem_ld32(taddr + (uint32_t)(c * 32), v);
-                    if (!split) {
-                        store_tile_chunk(P, it, trow, c, v);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) part[(c * 32 + j) * kTileRows + trow] = v[j];
+                const int64_t tile_floats = (int64_t)kTileRows * E.bn;
+                if (!split && E.tma_out) {
+                    epilogue_staged<true>(E, it.row0, it.col0, stg, trow, etid, taddr, nullptr, 1, &tempty[acc],
+                                          args.trace ? args.trace + 8 * i : nullptr);
+                } else {
+                    float* tile_ws = split ? args.ws + (int64_t)it.ws_blk * kWsBlock : nullptr;
+                    for (int c = 0; c < nchunks; ++c) {
+                        float v[32];
+                        tmem_ld32(taddr + (uint32_t)(c * 32), v);
+                        if (!split)
+                            store_tile_chunk(E, it.row0, it.col0, trow, c, v);
+                        else
+                            ws_store_chunk(ws_chunk(tile_ws, E.bn, it.split, c, trow), v);
                     }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
                 if (split) {
-                    // last-arriving split reduces all partials in split order (deterministic)
-                    __threadfence();
+                    // Serial split-K fixup: the CTA that completes a tile's arrival count reduces
+                    // all partials in split order (deterministic). One thread publishes with a
+                    // release fence + relaxed atomic after a CTA barrier; the winner acquires.
+                    uint64_t* tr = args.trace ? args.trace + 8 * i : nullptr;
+                    if (tr && etid == 0) tr[4] = global_timer_ns();
                     named_bar_sync(1, 128);
+                    if (tr && etid == 0) tr[5] = global_timer_ns();
                     if (etid == 0) {
+                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
                         const int prev = atomicAdd(args.counters + it.tile_slot, 1);
-                        *split_flag = (prev == it.nsplit - 1);
+                        const int last = prev == it.nsplit - 1;
+                        if (last) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                        *split_flag = last;
                     }
                     named_bar_sync(1, 128);
+                    if (tr && etid == 0) tr[6] = global_timer_ns();
                     if (*split_flag) {
-                        __threadfence();
                         const float* base = args.ws + (int64_t)it.ws_blk * kWsBlock;
-                        for (int c = 0; c < nchunks; ++c) {
-                            float v[32];
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                float s = 0.0f;
-                                for (int sp = 0; sp < it.nsplit; ++sp)
-                                    s += __ldcg(base + (int64_t)sp * (kTileRows * P.bn) + (c * 32 + j) * kTileRows + trow);
-                                v[j] = s;
+                        if (E.tma_out) {
+                            epilogue_staged<false>(E, it.row0, it.col0, stg, trow, etid, 0, base, it.nsplit, nullptr);
+                        } else {
+                            for (int c = 0; c < nchunks; ++c) {
+                                float v[32];
+                                ws_reduce_chunk(base, E.bn, it.nsplit, c, trow, v);
+                                store_tile_chunk(E, it.row0, it.col0, trow, c, v);
                             }
-                            store_tile_chunk(P, it, trow, c, v);
                         }
                         if (etid == 0) args.counters[it.tile_slot] = 0;   // re-arm for the next launch
+                        if (tr && etid == 0) tr[7] = global_timer_ns();
                     }
                 }
             } else if (it.type == kItemGemv) {
-                if (P.in_dt == GMX_ST_F32)
-                    gemv_rows<float>(P, it.row0, it.col0, ew);
+                if (Pg->in_dt == GMX_ST_F32)
+                    gemv_rows<float>(Pg, it.row0, it.col0, ew);
                 else
-                    gemv_rows<__nv_bfloat16>(P, it.row0, it.col0, ew);
+                    gemv_rows<__nv_bfloat16>(Pg, it.row0, it.col0, ew);
             } else {
-                if (P.in_dt == GMX_ST_F32)
-                    eltwise_range<float>(P, it.row0, it.col0, etid, 128);
+                if (Pg->in_dt == GMX_ST_F32)
+                    eltwise_range<float>(Pg, it.row0, it.col0, etid, 128);
                 else
-                    eltwise_range<__nv_bfloat16>(P, it.row0, it.col0, etid, 128);
+                    eltwise_range<__nv_bfloat16>(Pg, it.row0, it.col0, etid, 128);
+            }
+            if (args.trace) {
+                named_bar_sync(2, 128);
+                if (etid == 0) args.trace[8 * i + 3] = global_timer_ns();
             }
         }
+        if (etid == 0) bulk_wait0();   // all TMA stores of this CTA complete
     }
 
     tc_fence_before();
@@ -472,11 +681,9 @@ static int make_tmap(CUtensorMap* map, const void* ptr, int64_t rows, int64_t K,
     return GMX_OK;
 }
 
-static int choose_bn(int64_t cols) {
-    const int64_t t = (cols + kMaxBN - 1) / kMaxBN;
-    const int64_t per = (cols + t - 1) / t;
-    return (int)std::min<int64_t>(kMaxBN, ((per + 31) / 32) * 32);
-}
+// UMMA N of a problem: 64 for narrow outputs, else 128 (multiples of 64 keep every output
+// TMA box inside its own tile).
+static int choose_bn(int64_t cols) { return cols <= 64 ? 64 : kMaxBN; }
 
 struct HostProblem {
     DevProblem dev;
@@ -520,6 +727,10 @@ struct gmx_exec {
     int64_t max_split = 32;
     bool cache_plans = true;
     bool attr_set = false;
+    bool tracing = false;
+    uint64_t* trace = nullptr;
+    int64_t trace_cap = 0;
+    int64_t trace_items = 0;
 };
 
 namespace gmx {
@@ -657,13 +868,20 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
     }
     plan.items.clear();
     plan.cta_off.assign(1, 0);
+    std::vector<int32_t> flags(grid, 0);
     for (int c = 0; c < grid; ++c) {
-        for (int32_t idx : per_cta[c]) plan.items.push_back(cands[idx].it);
+        for (int32_t idx : per_cta[c]) {
+            plan.items.push_back(cands[idx].it);
+            if (cands[idx].it.type == kItemGemm) flags[c] |= 1;
+        }
         plan.cta_off.push_back((int32_t)plan.items.size());
     }
     if (plan.items.empty()) {   // keep the device arrays non-empty
         plan.cta_off.assign(2, 0);
+        flags.assign(1, 0);
     }
+    // device layout: cta_off[grid + 1] followed by cta_flags[grid]
+    plan.cta_off.insert(plan.cta_off.end(), flags.begin(), flags.end());
     st.grid = grid;
     st.n_items = (int32_t)plan.items.size();
     st.max_cta_cost = *std::max_element(load.begin(), load.end());
@@ -790,6 +1008,22 @@ int gmx_exec_register(gmx_exec* ex, const gmx_problem_desc* d, int32_t* out_slot
         if ((rc = make_tmap(&P.tm_rows, rows_ptr, P.rows, d->k, rows_ld, kTileRows)) ||
             (rc = make_tmap(&P.tm_cols, cols_ptr, P.cols, d->k, cols_ld, P.bn)))
             return rc;
+        // output tensor map (TMA-store epilogue) when C allows 16-byte-aligned rows
+        P.tma_out = 0;
+        if ((reinterpret_cast<uintptr_t>(d->c) & 15) == 0 && (d->ldc * osz) % 16 == 0) {
+            auto fn = encode_fn();
+            const int inner = (int)(128 / osz);
+            cuuint64_t dims[2] = {(cuuint64_t)d->n, (cuuint64_t)d->m};
+            cuuint64_t strides[1] = {(cuuint64_t)(d->ldc * osz)};
+            cuuint32_t box[2] = {(cuuint32_t)inner, (cuuint32_t)(swap ? 32 : kTileRows)};
+            cuuint32_t estr[2] = {1, 1};
+            if (fn && fn(&P.tm_out, d->out_dtype == GMX_ST_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                                 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                         2, d->c, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+                P.tma_out = 1;
+        }
         hp.op_bytes = 2 * (d->m * d->k + d->k * d->n) + osz * d->m * d->n;
         hp.flops = 2 * d->m * d->n * d->k;
     } else if (d->op == GMX_OP_GEMV) {
@@ -880,7 +1114,17 @@ int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream_
         GMX_CUDA(cudaFuncSetAttribute(coalesced_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
         ex->attr_set = true;
     }
-    KernelArgs args{ex->d_probs, plan->d_items, plan->d_off, ex->ws, ex->counters};
+    if (ex->tracing && (int64_t)plan->items.size() > ex->trace_cap) {
+        if (ex->trace) GMX_CUDA(cudaFree(ex->trace));
+        ex->trace_cap = std::max<int64_t>(1024, (int64_t)plan->items.size());
+        GMX_CUDA(cudaMalloc(&ex->trace, ex->trace_cap * 8 * sizeof(uint64_t)));
+    }
+    if (ex->tracing) {
+        GMX_CUDA(cudaMemsetAsync(ex->trace, 0, plan->items.size() * 8 * sizeof(uint64_t), stream));
+        ex->trace_items = (int64_t)plan->items.size();
+    }
+    KernelArgs args{ex->d_probs, plan->d_items, plan->d_off, plan->d_off + plan->stats.grid + 1, ex->ws,
+                    ex->counters, ex->tracing ? ex->trace : nullptr};
     coalesced_step_kernel<<<plan->stats.grid, kThreads, kSmemBytes, stream>>>(args);
     GMX_CUDA(cudaGetLastError());
     plan->stats.cached = cached;
@@ -910,6 +1154,9 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
         ex->max_split = value;
     } else if (n == "cache_plans") {
         ex->cache_plans = value != 0;
+    } else if (n == "trace") {
+        ex->tracing = value != 0;
+        return GMX_OK;
     } else {
         return fail(GMX_EINVAL, "unknown option " + n);
     }
@@ -919,5 +1166,20 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
 }
 
 const char* gmx_exec_last_error(void) { return g_err.c_str(); }
+
+int gmx_exec_read_trace(const gmx_exec* ex, uint64_t* stamps, int32_t* items, int32_t* cta_off,
+                        int32_t capacity, int32_t* n_items, int32_t* grid) {
+    if (!ex || !n_items || !grid) return fail(GMX_EINVAL, "null argument");
+    if (!ex->tracing || !ex->last) return fail(GMX_ESTATE, "tracing off or no launch");
+    const int32_t n = (int32_t)ex->trace_items;
+    *n_items = n;
+    *grid = ex->last->stats.grid;
+    if (capacity < n) return GMX_OK;
+    GMX_CUDA(cudaDeviceSynchronize());
+    GMX_CUDA(cudaMemcpy(stamps, ex->trace, (size_t)n * 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    for (int32_t i = 0; i < n; ++i) std::memcpy(items + 8 * i, &ex->last->items[i], sizeof(WorkItem));
+    for (int32_t c = 0; c <= ex->last->stats.grid; ++c) cta_off[c] = ex->last->cta_off[c];
+    return GMX_OK;
+}
 
 }  // extern "C"

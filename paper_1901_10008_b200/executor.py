@@ -54,6 +54,9 @@ EXEC_SIGNATURES = {
     "gmx_exec_last_plan": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
     "gmx_exec_clear_plans": (C.c_int, [C.c_void_p]),
     "gmx_exec_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
+    "gmx_exec_read_trace": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int32)]),
 }
 
 _exec_lib = None
@@ -207,6 +210,35 @@ class Executor:
     def set_option(self, name: str, value: int):
         _check(self._lib.gmx_exec_set_option(self._h, name.encode(), int(value)))
 
+    def read_trace(self):
+        """Per-item %globaltimer stamps of the last launch (set_option("trace", 1) first).
+
+        Returns (items, cta_off) with items = list of dicts: problem, type, row0, col0, kb0,
+        kb1, split, nsplit, cta, t_prod, t_mma_done, t_epi, t_end (ns, absolute)."""
+        n, grid = C.c_int32(), C.c_int32()
+        _check(self._lib.gmx_exec_read_trace(self._h, None, None, None, 0, C.byref(n), C.byref(grid)))
+        stamps = (C.c_uint64 * (8 * max(1, n.value)))()
+        raw = (C.c_int32 * (8 * max(1, n.value)))()
+        off = (C.c_int32 * (grid.value + 1))()
+        _check(self._lib.gmx_exec_read_trace(self._h, stamps, raw, off, n.value, C.byref(n),
+                                             C.byref(grid)))
+        cta_of = {}
+        for c in range(grid.value):
+            for i in range(off[c], off[c + 1]):
+                cta_of[i] = c
+        items = []
+        for i in range(n.value):
+            w = raw[8 * i: 8 * i + 8]
+            packed = w[1] & 0xFFFFFFFF
+            items.append({"problem": w[0], "type": packed & 0xFF, "nsplit": (packed >> 8) & 0xFF,
+                          "split": (packed >> 16) & 0xFF, "row0": w[2], "col0": w[3], "kb0": w[4],
+                          "kb1": w[5], "cta": cta_of.get(i, -1),
+                          "t_prod": stamps[8 * i], "t_mma_done": stamps[8 * i + 1],
+                          "t_epi": stamps[8 * i + 2], "t_end": stamps[8 * i + 3],
+                          "t_e_start": stamps[8 * i + 4], "t_e_staged": stamps[8 * i + 5],
+                          "t_e_bar": stamps[8 * i + 6], "t_e_issued": stamps[8 * i + 7]})
+        return items, list(off)
+
     def clear_plans(self):
         _check(self._lib.gmx_exec_clear_plans(self._h))
 
@@ -235,7 +267,9 @@ class OperandSet:
             bt = torch.full((n, ld), float("nan"), dtype=torch.bfloat16)
             bt[:, :k] = torch.randn(n, k, generator=g).to(torch.bfloat16)
             self.a, self.b = a.to(device), bt.to(device)
-            self.c = torch.empty(m, n, dtype=out_dtype or torch.bfloat16, device=device)
+            odt = out_dtype or torch.bfloat16
+            # C rows padded to 16 bytes so the epilogue can TMA-store whole tiles
+            self.c = torch.empty(m, padded_ld(n, odt), dtype=odt, device=device)[:, :n]
             self.bias = (torch.randn(m, generator=g) * 0.1).to(device) if bias else None
         elif op_kind == "gemv":
             m, n = dims
