@@ -1,0 +1,151 @@
+// flatmap.hpp — allocation-light containers for the decision core's hot path.
+//
+//   IdMap       int64 key -> int32 value, open addressing (linear probing, backward-shift
+//               deletion), power-of-two capacity; no per-insert allocation.
+//   SigSet      exact set of sorted int64 id lists (withheld cluster signatures,
+//               scheduler.py:435-443): 64-bit hash + arena-stored members verified on hit.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+namespace gmx {
+
+inline uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+class IdMap {
+   public:
+    IdMap() { rehash(64); }
+
+    int32_t find(int64_t key) const {
+        size_t i = mix64((uint64_t)key) & mask_;
+        while (used_[i]) {
+            if (keys_[i] == key) return vals_[i];
+            i = (i + 1) & mask_;
+        }
+        return -1;
+    }
+
+    void put(int64_t key, int32_t val) {
+        if ((size_ + 1) * 4 > (mask_ + 1) * 3) rehash((mask_ + 1) * 2);
+        size_t i = mix64((uint64_t)key) & mask_;
+        while (used_[i]) {
+            if (keys_[i] == key) {
+                vals_[i] = val;
+                return;
+            }
+            i = (i + 1) & mask_;
+        }
+        used_[i] = 1;
+        keys_[i] = key;
+        vals_[i] = val;
+        ++size_;
+    }
+
+    bool erase(int64_t key) {
+        size_t i = mix64((uint64_t)key) & mask_;
+        while (used_[i]) {
+            if (keys_[i] == key) {
+                // backward-shift deletion keeps probe chains intact without tombstones
+                size_t j = i;
+                for (;;) {
+                    j = (j + 1) & mask_;
+                    if (!used_[j]) break;
+                    const size_t home = mix64((uint64_t)keys_[j]) & mask_;
+                    const bool movable = (i <= j) ? (home <= i || home > j) : (home <= i && home > j);
+                    if (movable) {
+                        keys_[i] = keys_[j];
+                        vals_[i] = vals_[j];
+                        i = j;
+                    }
+                }
+                used_[i] = 0;
+                --size_;
+                return true;
+            }
+            i = (i + 1) & mask_;
+        }
+        return false;
+    }
+
+    size_t size() const { return size_; }
+
+   private:
+    void rehash(size_t cap) {
+        std::vector<int64_t> k = std::move(keys_);
+        std::vector<int32_t> v = std::move(vals_);
+        std::vector<uint8_t> u = std::move(used_);
+        keys_.assign(cap, 0);
+        vals_.assign(cap, 0);
+        used_.assign(cap, 0);
+        mask_ = cap - 1;
+        size_ = 0;
+        for (size_t i = 0; i < u.size(); ++i)
+            if (u[i]) put(k[i], v[i]);
+    }
+
+    std::vector<int64_t> keys_;
+    std::vector<int32_t> vals_;
+    std::vector<uint8_t> used_;
+    size_t mask_ = 0, size_ = 0;
+};
+
+class SigSet {
+   public:
+    SigSet() { slots_.assign(256, -1); }
+
+    // Inserts the (sorted) id list; returns false if it was already present.
+    bool insert(const int64_t* ids, int32_t n) {
+        if ((count_ + 1) * 2 > slots_.size()) grow();
+        const uint64_t h = hash(ids, n);
+        size_t i = h & (slots_.size() - 1);
+        while (slots_[i] >= 0) {
+            const int32_t e = slots_[i];
+            if (hashes_[e] == h && equal(e, ids, n)) return false;
+            i = (i + 1) & (slots_.size() - 1);
+        }
+        const int32_t e = (int32_t)hashes_.size();
+        hashes_.push_back(h);
+        offsets_.push_back((int64_t)arena_.size());
+        arena_.push_back(n);
+        arena_.insert(arena_.end(), ids, ids + n);
+        slots_[i] = e;
+        ++count_;
+        return true;
+    }
+
+   private:
+    static uint64_t hash(const int64_t* ids, int32_t n) {
+        uint64_t h = 0x9E3779B97F4A7C15ull ^ (uint64_t)n;
+        for (int32_t i = 0; i < n; ++i) h = mix64(h ^ (uint64_t)ids[i]);
+        return h;
+    }
+    bool equal(int32_t e, const int64_t* ids, int32_t n) const {
+        const int64_t* p = arena_.data() + offsets_[e];
+        return p[0] == n && std::memcmp(p + 1, ids, sizeof(int64_t) * (size_t)n) == 0;
+    }
+    void grow() {
+        std::vector<int32_t> next(slots_.size() * 2, -1);
+        for (int32_t e = 0; e < (int32_t)hashes_.size(); ++e) {
+            size_t i = hashes_[e] & (next.size() - 1);
+            while (next[i] >= 0) i = (i + 1) & (next.size() - 1);
+            next[i] = e;
+        }
+        slots_.swap(next);
+    }
+
+    std::vector<int32_t> slots_;
+    std::vector<uint64_t> hashes_;
+    std::vector<int64_t> offsets_;
+    std::vector<int64_t> arena_;
+    size_t count_ = 0;
+};
+
+}  // namespace gmx

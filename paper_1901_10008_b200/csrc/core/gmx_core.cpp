@@ -12,6 +12,7 @@
 // Build: g++ -O2 -std=c++17 -ffp-contract=off -fPIC -shared (no -ffast-math).
 
 #include "../../../include/gmx_core.h"
+#include "flatmap.hpp"
 #include "pyexact.hpp"
 
 #include <algorithm>
@@ -251,7 +252,9 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
                           std::vector<Cluster>& clusters) {
     if (!(budget >= 0.0 && budget < 1.0)) return fail(GMX_EINVAL, "pad_budget must be in [0, 1)");
     const int32_t n = (int32_t)recs.size();
-    std::vector<int32_t> idx(n);
+    static thread_local std::vector<int32_t> idx;   // scratch: no allocation after warm-up
+    static thread_local std::vector<char> taken;
+    idx.resize(n);
     for (int32_t i = 0; i < n; ++i) idx[i] = i;
     std::sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) {
         const ShapeRec &a = recs[x], &b = recs[y];
@@ -261,7 +264,7 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
             if (a.dims[i] != b.dims[i]) return a.dims[i] > b.dims[i];
         return a.id < b.id;
     });
-    std::vector<char> taken(n, 0);
+    taken.assign(n, 0);
     order.clear();
     clusters.clear();
     for (int32_t i = 0; i < n; ++i) {
@@ -302,6 +305,10 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
 }
 
 // ---------------------------------------------------------------- scheduler
+//
+// Storage is flat so a steady-state step allocates nothing: kernels and requests live in
+// append-only vectors (a request's kernels are a contiguous slot range), dependency lists in
+// one arena, in-flight dispatches in a recycled pool, id lookups in open-addressing maps.
 
 struct KernelRec {
     int64_t id;
@@ -309,25 +316,26 @@ struct KernelRec {
     int64_t dims[3];
     int64_t arrival, deadline, flops, bytes, predicted;
     int32_t req, pos;
-    int32_t ready_pos = -1;   // index in Sched::ready, -1 if not ready
-    bool blocked = false, done = false;
-    std::vector<int64_t> waiting;  // pending dependency ids while blocked
+    int32_t ready_pos;   // index in Sched::ready, -1 if not ready
+    int32_t dep_off;     // pending dependency ids: dep_arena[dep_off .. dep_off + dep_n)
+    int32_t dep_n;
+    bool blocked, done;
 };
 
 struct RequestRec {
     int64_t id;
     int32_t stream;
     int64_t arrival;
-    std::vector<int32_t> kernels;  // kernel slots in request order (empty if refused)
-    std::vector<int64_t> kernel_ids;
-    int64_t remaining;
-    bool evicted = false, finished = false;
+    int32_t first, count;   // kernel slots [first, first + count) in request order
+    int64_t remaining;      // distinct kernel ids not yet completed
+    bool evicted, finished;
 };
 
 struct DispatchRec {
     gmx_dispatch_rec rec;
-    std::vector<int32_t> kernels;   // slots
+    std::vector<int32_t> kernels;   // slots (capacity retained across pool reuse)
     std::vector<int32_t> streams;   // sorted by name, unique
+    bool live = false;
 };
 
 }  // namespace gmx
@@ -344,19 +352,24 @@ struct gmx_sched {
     std::vector<std::string> stream_names;
     std::unordered_map<std::string, int32_t> stream_ids;
     std::vector<char> evicted_stream;
+    std::vector<int32_t> stream_rank;   // byte-order rank of each stream name
+    bool ranks_dirty = false;
 
     std::vector<gmx::KernelRec> kernels;
-    std::unordered_map<int64_t, int32_t> kernel_slot;
+    gmx::IdMap kernel_slot;
     std::vector<gmx::RequestRec> requests;
-    std::unordered_map<int64_t, int32_t> request_slot;
-    std::vector<int32_t> ready;                 // kernel slots
-    std::map<int64_t, gmx::DispatchRec> in_flight;  // ordered == insertion order
+    std::vector<int64_t> dep_arena;
+    std::vector<int32_t> ready;           // kernel slots
+    std::vector<gmx::DispatchRec> pool;   // in-flight dispatches
+    std::vector<int32_t> pool_free;
+    gmx::IdMap inflight_slot;             // dispatch id -> pool index
+    int64_t n_inflight = 0;
     int64_t free_sms;
     int64_t dispatch_seq = 0;
     bool has_last_ctx = false;
     std::string last_ctx;
     int32_t rr_last = -1;
-    std::set<std::vector<int64_t>> withheld_sigs;
+    gmx::SigSet withheld_sigs;
 
     // view storage
     std::vector<gmx_dispatch_rec> v_disp;
@@ -364,11 +377,25 @@ struct gmx_sched {
     std::vector<int32_t> v_held_off;
     // scratch
     std::vector<gmx::ShapeRec> s_recs;
-    std::vector<int32_t> s_order;
+    std::vector<int32_t> s_order, s_live, s_act, s_members, s_tmp;
     std::vector<gmx::Cluster> s_clusters;
+    std::vector<int64_t> s_slack, s_sig, s_wakeups;
+    std::vector<char> s_seen;
 
     const gmx_tuning_table* tbl() const { return has_table ? &table : nullptr; }
-    bool stream_less(int32_t a, int32_t b) const { return stream_names[a] < stream_names[b]; }
+    int32_t rank(int32_t st) {
+        if (ranks_dirty) {
+            std::vector<int32_t> order(stream_names.size());
+            for (size_t i = 0; i < order.size(); ++i) order[i] = (int32_t)i;
+            std::sort(order.begin(), order.end(),
+                      [this](int32_t a, int32_t b) { return stream_names[a] < stream_names[b]; });
+            stream_rank.assign(order.size(), 0);
+            for (size_t r = 0; r < order.size(); ++r) stream_rank[order[r]] = (int32_t)r;
+            ranks_dirty = false;
+        }
+        return stream_rank[st];
+    }
+    bool stream_less(int32_t a, int32_t b) { return rank(a) < rank(b); }
 };
 
 namespace gmx {
@@ -396,12 +423,12 @@ static void ready_remove(S* s, int32_t slot) {
     k.ready_pos = -1;
 }
 
-// scheduler.py:195-203
+// scheduler.py:195-203: this kernel plus every later, unfinished kernel of its request
 static int64_t predicted_remaining(const S* s, const KernelRec& k) {
     const RequestRec& r = s->requests[k.req];
     int64_t total = 0;
-    for (size_t i = (size_t)k.pos; i < r.kernels.size(); ++i) {
-        const KernelRec& succ = s->kernels[r.kernels[i]];
+    for (int32_t slot = r.first + k.pos; slot < r.first + r.count; ++slot) {
+        const KernelRec& succ = s->kernels[slot];
         if (!succ.done) total += succ.predicted;
     }
     return total;
@@ -421,11 +448,13 @@ static void live_ready(const S* s, std::vector<int32_t>& out) {
 }
 
 // scheduler.py:282-286 (sorted by name, evicted removed)
-static void active_streams(const S* s, std::vector<int32_t>& out) {
-    std::vector<char> seen(s->stream_names.size(), 0);
+static void active_streams(S* s, std::vector<int32_t>& out) {
+    std::vector<char>& seen = s->s_seen;
+    seen.assign(s->stream_names.size(), 0);
     for (int32_t slot : s->ready) seen[s->kernels[slot].stream] = 1;
-    for (const auto& kv : s->in_flight)
-        for (int32_t st : kv.second.streams) seen[st] = 1;
+    for (const DispatchRec& d : s->pool)
+        if (d.live)
+            for (int32_t st : d.streams) seen[st] = 1;
     out.clear();
     for (size_t i = 0; i < seen.size(); ++i)
         if (seen[i] && !s->evicted_stream[i]) out.push_back((int32_t)i);
@@ -441,9 +470,18 @@ static double noise_factor(S* s) {
 
 // scheduler.py:294-316
 static void make_dispatch(S* s, const std::vector<int32_t>& members, int64_t now, int64_t duration,
-                          int64_t predicted, int64_t alloc, int32_t context, const std::string& ctx_name,
+                          int64_t predicted, int64_t alloc, int32_t context, const char* ctx_name,
                           bool ctx_switch, bool is_super, int64_t useful, int64_t padded, bool infeasible) {
-    DispatchRec d;
+    int32_t pi;
+    if (!s->pool_free.empty()) {
+        pi = s->pool_free.back();
+        s->pool_free.pop_back();
+    } else {
+        pi = (int32_t)s->pool.size();
+        s->pool.emplace_back();
+    }
+    DispatchRec& d = s->pool[pi];
+    d.live = true;
     d.rec.dispatch_id = ++s->dispatch_seq;
     d.rec.start = now + (ctx_switch ? s->prof.context_switch_cost : 0);
     d.rec.end = d.rec.start + duration;
@@ -459,7 +497,8 @@ static void make_dispatch(S* s, const std::vector<int32_t>& members, int64_t now
     d.rec.kernel_offset = (int32_t)s->v_disp_kids.size();
     d.rec.n_kernels = (int32_t)members.size();
     d.rec._pad = 0;
-    d.kernels = members;
+    d.kernels.assign(members.begin(), members.end());
+    d.streams.clear();
     for (int32_t slot : members) {
         s->v_disp_kids.push_back(s->kernels[slot].id);
         d.streams.push_back(s->kernels[slot].stream);
@@ -471,7 +510,15 @@ static void make_dispatch(S* s, const std::vector<int32_t>& members, int64_t now
     s->free_sms -= alloc;
     s->has_last_ctx = true;
     s->last_ctx = ctx_name;
-    s->in_flight.emplace(d.rec.dispatch_id, std::move(d));
+    s->inflight_slot.put(d.rec.dispatch_id, pi);
+    ++s->n_inflight;
+}
+
+static void release_dispatch(S* s, int32_t pi) {
+    s->inflight_slot.erase(s->pool[pi].rec.dispatch_id);
+    s->pool[pi].live = false;
+    s->pool_free.push_back(pi);
+    --s->n_inflight;
 }
 
 static int64_t useful_of(const S* s, const std::vector<int32_t>& members) {
@@ -490,9 +537,9 @@ static int solo_duration(const S* s, const KernelRec& k, int64_t* out) {
 
 // scheduler.py:335-347
 static int step_serial(S* s, int64_t now, bool by_deadline) {
-    std::vector<int32_t> live;
+    std::vector<int32_t>& live = s->s_live;
     live_ready(s, live);
-    if (!s->in_flight.empty() || live.empty()) return GMX_OK;
+    if (s->n_inflight > 0 || live.empty()) return GMX_OK;
     int32_t best = live[0];
     for (int32_t slot : live) {
         const KernelRec &a = s->kernels[slot], &b = s->kernels[best];
@@ -505,8 +552,9 @@ static int step_serial(S* s, int64_t now, bool by_deadline) {
     if (rc) return rc;
     const int64_t dur = py_ceil((double)pred * noise_factor(s));
     const bool inf = kernel_slack(s, k, now) < 0;
-    make_dispatch(s, {best}, now, dur, pred, s->prof.sm_count, k.stream, s->stream_names[k.stream],
-                  false, false, k.flops, k.flops, inf);
+    s->s_members.assign(1, best);
+    make_dispatch(s, s->s_members, now, dur, pred, s->prof.sm_count, k.stream,
+                  s->stream_names[k.stream].c_str(), false, false, k.flops, k.flops, inf);
     return GMX_OK;
 }
 
@@ -524,19 +572,17 @@ static int32_t earliest_arrival(const S* s, const std::vector<int32_t>& live, in
 
 // scheduler.py:349-370
 static int step_time_mux(S* s, int64_t now) {
-    if (!s->in_flight.empty()) return GMX_OK;
-    std::vector<int32_t> live;
+    if (s->n_inflight > 0) return GMX_OK;
+    std::vector<int32_t>& live = s->s_live;
     live_ready(s, live);
-    std::vector<int32_t> streams;
+    std::vector<int32_t>& streams = s->s_act;
+    streams.clear();
     for (int32_t slot : live) streams.push_back(s->kernels[slot].stream);
     if (streams.empty()) return GMX_OK;
     std::sort(streams.begin(), streams.end(), [s](int32_t a, int32_t b) { return s->stream_less(a, b); });
     streams.erase(std::unique(streams.begin(), streams.end()), streams.end());
-    int32_t pick;
-    if (s->rr_last < 0 || !s->stream_less(s->rr_last, streams.back())) {
-        pick = streams[0];
-    } else {
-        pick = streams[0];
+    int32_t pick = streams[0];
+    if (s->rr_last >= 0 && s->stream_less(s->rr_last, streams.back())) {
         for (int32_t st : streams)
             if (s->stream_less(s->rr_last, st)) { pick = st; break; }
     }
@@ -550,8 +596,9 @@ static int step_time_mux(S* s, int64_t now) {
     const std::string& name = s->stream_names[pick];
     const bool sw = s->has_last_ctx && s->last_ctx != name;
     const bool inf = kernel_slack(s, k, now) < 0;
-    make_dispatch(s, {slot}, now, dur, pred, s->prof.sm_count, pick, name, sw, false, k.flops,
-                  k.flops, inf);
+    s->s_members.assign(1, slot);
+    make_dispatch(s, s->s_members, now, dur, pred, s->prof.sm_count, pick, name.c_str(), sw, false,
+                  k.flops, k.flops, inf);
     return GMX_OK;
 }
 
@@ -577,17 +624,20 @@ static int shared_duration(const S* s, const KernelRec& k, int64_t tenants, int6
 
 // scheduler.py:393-412
 static int step_space_mux(S* s, int64_t now) {
-    std::vector<int32_t> active;
+    std::vector<int32_t>& active = s->s_act;
     active_streams(s, active);
     const int64_t tenants = (int64_t)active.size();
     if (tenants == 0) return GMX_OK;
     const int64_t alloc = std::max<int64_t>(1, s->prof.sm_count / tenants);
-    std::vector<char> busy(s->stream_names.size(), 0);
-    for (const auto& kv : s->in_flight)
-        for (int32_t st : kv.second.streams) busy[st] = 1;
+    std::vector<char>& busy = s->s_seen;
+    busy.assign(s->stream_names.size(), 0);
+    for (const DispatchRec& d : s->pool)
+        if (d.live)
+            for (int32_t st : d.streams) busy[st] = 1;
     const double width = tenants >= 2 ? s->params.jitter_width * (double)(1 + tenants % 2) : 0.0;
-    std::vector<int32_t> live;
-    for (int32_t st : active) {
+    std::vector<int32_t>& live = s->s_live;
+    const std::vector<int32_t> order(active);   // `active` scratch is reused below
+    for (int32_t st : order) {
         if (busy[st]) continue;
         live_ready(s, live);
         const int32_t slot = earliest_arrival(s, live, st);
@@ -599,7 +649,8 @@ static int step_space_mux(S* s, int64_t now) {
         const double factor = 1.0 + (width != 0.0 ? s->rng.uniform(0.0, width) : 0.0);
         const int64_t dur = py_ceil((double)base * factor * noise_factor(s));
         const bool inf = kernel_slack(s, k, now) < 0;
-        make_dispatch(s, {slot}, now, dur, base, alloc, st, s->stream_names[st], false, false,
+        s->s_members.assign(1, slot);
+        make_dispatch(s, s->s_members, now, dur, base, alloc, st, s->stream_names[st].c_str(), false, false,
                       k.flops, k.flops, inf);
     }
     return GMX_OK;
@@ -615,12 +666,11 @@ struct Scored {
 
 // scheduler.py:414-471
 static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
-    std::vector<int32_t> live;
+    std::vector<int32_t>& live = s->s_live;
     live_ready(s, live);
     if (live.empty()) return GMX_OK;
-    std::vector<int32_t> act;
-    active_streams(s, act);
-    const int64_t tenancy = std::max<int64_t>(1, (int64_t)act.size());
+    active_streams(s, s->s_act);
+    const int64_t tenancy = std::max<int64_t>(1, (int64_t)s->s_act.size());
 
     auto& recs = s->s_recs;
     recs.clear();
@@ -634,9 +684,10 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
     const auto& order = s->s_order;
     const auto& clusters = s->s_clusters;
 
-    std::vector<int64_t> slack(recs.size());
-    std::vector<Scored> scored;
-    scored.reserve(clusters.size());
+    std::vector<int64_t>& slack = s->s_slack;
+    slack.assign(recs.size(), 0);
+    static thread_local std::vector<Scored> scored;
+    scored.clear();
     for (int32_t c = 0; c < (int32_t)clusters.size(); ++c) {
         Scored sc{1, INT64_MAX, INT64_MAX, c, false};
         for (int32_t i = clusters[c].begin; i < clusters[c].end; ++i) {
@@ -656,28 +707,26 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
     });
 
     const double frac = s->params.max_delay_fraction;
-    std::vector<int32_t> members;
-    std::vector<int64_t> sig;
+    std::vector<int32_t>& members = s->s_members;
+    std::vector<int64_t>& sig = s->s_sig;
     for (const Scored& sc : scored) {
         const Cluster& cl = clusters[sc.cluster];
         gmx_cost cost;
-        rc = superkernel_cost(&s->prof, s->tbl(), cl.op, cl.dtype, cl.padded, cl.nd,
-                              cl.end - cl.begin, tenancy, &cost);
+        rc = superkernel_cost(&s->prof, s->tbl(), cl.op, cl.dtype, cl.padded, cl.nd, cl.end - cl.begin, tenancy,
+                              &cost);
         if (rc) return rc;
         members.clear();
         for (int32_t i = cl.begin; i < cl.end; ++i) members.push_back(recs[order[i]].src);
         bool can_delay = !sc.late && cost.efficiency < 1.0;
-        if (can_delay) {
-            for (int32_t i = cl.begin; i < cl.end && can_delay; ++i) {
-                const KernelRec& k = s->kernels[recs[order[i]].src];
-                can_delay = int_ge_float(slack[order[i]], frac * (double)slo_of(s, k));
-            }
+        for (int32_t i = cl.begin; i < cl.end && can_delay; ++i) {
+            const KernelRec& k = s->kernels[recs[order[i]].src];
+            can_delay = int_ge_float(slack[order[i]], frac * (double)slo_of(s, k));
         }
         if (can_delay) {
             sig.clear();
             for (int32_t slot : members) sig.push_back(s->kernels[slot].id);
             std::sort(sig.begin(), sig.end());
-            if (s->withheld_sigs.insert(sig).second) {
+            if (s->withheld_sigs.insert(sig.data(), (int32_t)sig.size())) {
                 // withhold once per member set; wakeup clamps to the slack boundary
                 for (int32_t slot : members) s->v_held_kids.push_back(s->kernels[slot].id);
                 s->v_held_off.push_back((int32_t)s->v_held_kids.size());
@@ -702,14 +751,21 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
     return GMX_OK;
 }
 
-// scheduler.py:210-235
+// scheduler.py:228-235: drop `done_id` from every blocked kernel of the request; kernels
+// whose dependency set empties move to ready (in request order)
 static void unlock_dependents(S* s, int64_t done_id, const RequestRec& r, std::vector<int64_t>& unlocked) {
-    for (int32_t slot : r.kernels) {
+    for (int32_t slot = r.first; slot < r.first + r.count; ++slot) {
         KernelRec& k = s->kernels[slot];
         if (!k.blocked) continue;
-        auto it = std::find(k.waiting.begin(), k.waiting.end(), done_id);
-        if (it != k.waiting.end()) k.waiting.erase(it);
-        if (k.waiting.empty()) {
+        int64_t* deps = s->dep_arena.data() + k.dep_off;
+        for (int32_t j = 0; j < k.dep_n; ++j) {
+            if (deps[j] == done_id) {
+                deps[j] = deps[k.dep_n - 1];
+                --k.dep_n;
+                break;
+            }
+        }
+        if (k.dep_n == 0) {
             k.blocked = false;
             ready_add(s, slot);
             unlocked.push_back(k.id);
@@ -887,6 +943,7 @@ int gmx_sched_intern_stream(gmx_sched* s, const char* name, int32_t* out) {
     s->stream_names.emplace_back(name);
     s->stream_ids.emplace(name, id);
     s->evicted_stream.push_back(0);
+    s->ranks_dirty = true;
     *out = id;
     return GMX_OK;
 }
@@ -901,30 +958,46 @@ int gmx_sched_add_request(gmx_sched* s, int64_t request_id, int32_t stream, int6
         if (rc) return rc;
         if (ks[i].stream < 0 || ks[i].stream >= (int32_t)s->stream_names.size())
             return fail(GMX_EINVAL, "unknown kernel stream");
+        if (ks[i].dtype < 0 || ks[i].dtype > 1) return fail(GMX_EINVAL, "unknown dtype");
     }
-    RequestRec r;
+    RequestRec r{};
     r.id = request_id;
     r.stream = stream;
     r.arrival = arrival;
-    std::unordered_set<int64_t> distinct;
-    for (int32_t i = 0; i < n; ++i) {
-        distinct.insert(ks[i].kernel_id);
-        r.kernel_ids.push_back(ks[i].kernel_id);
+    r.first = (int32_t)s->kernels.size();
+    r.count = 0;
+    {   // distinct kernel ids (the reference's `remaining` is a set)
+        std::vector<int64_t>& ids = s->s_sig;
+        ids.clear();
+        for (int32_t i = 0; i < n; ++i) ids.push_back(ks[i].kernel_id);
+        std::sort(ids.begin(), ids.end());
+        r.remaining = (int64_t)(std::unique(ids.begin(), ids.end()) - ids.begin());
     }
-    r.remaining = (int64_t)distinct.size();
     const int32_t rslot = (int32_t)s->requests.size();
     if (s->evicted_stream[stream]) {
         r.evicted = true;
-        s->requests.push_back(std::move(r));
-        s->request_slot[request_id] = rslot;
+        s->requests.push_back(r);
         *accepted = 0;
         return GMX_OK;
     }
-    // compute predictions first so a failure leaves the state untouched
-    std::vector<KernelRec> recs((size_t)n);
+    // predictions first so a failure leaves the state untouched
+    std::vector<int64_t>& preds = s->s_slack;
+    preds.assign((size_t)n, 0);
+    for (int32_t i = 0; i < n; ++i) {
+        gmx_cost c;
+        const gmx_kernel_desc& d = ks[i];
+        int64_t dims[3] = {0, 0, 0};
+        for (int j = 0; j < d.ndims; ++j) dims[j] = d.dims[j];
+        const gmx_tuning_config& cfg = table_lookup(s->tbl(), make_key(d.op, d.dtype, dims, d.ndims), 1);
+        int rc = kernel_cost(&s->prof, d.op, d.dtype, dims, cfg, &c);
+        if (rc) return rc;
+        preds[i] = c.duration;
+    }
+    r.count = n;
+    s->requests.push_back(r);
     for (int32_t i = 0; i < n; ++i) {
         const gmx_kernel_desc& d = ks[i];
-        KernelRec& k = recs[i];
+        KernelRec k{};
         k.id = d.kernel_id;
         k.stream = d.stream;
         k.op = d.op;
@@ -933,39 +1006,34 @@ int gmx_sched_add_request(gmx_sched* s, int64_t request_id, int32_t stream, int6
         for (int j = 0; j < 3; ++j) k.dims[j] = j < d.ndims ? d.dims[j] : 0;
         k.arrival = d.arrival;
         k.deadline = d.deadline;
-        int rc;
-        if ((rc = flops_of(k.op, k.dims, &k.flops)) || (rc = bytes_of(k.op, k.dims, k.dtype, &k.bytes)))
-            return rc;
-        gmx_cost c;
-        if ((rc = kernel_cost(&s->prof, k.op, k.dtype, k.dims, solo_config(s, k), &c))) return rc;
-        k.predicted = c.duration;
+        flops_of(k.op, k.dims, &k.flops);
+        bytes_of(k.op, k.dims, k.dtype, &k.bytes);
+        k.predicted = preds[i];
         k.req = rslot;
         k.pos = i;
-        for (int32_t j = dep_off[i]; j < dep_off[i + 1]; ++j) {
-            if (std::find(k.waiting.begin(), k.waiting.end(), dep_ids[j]) == k.waiting.end())
-                k.waiting.push_back(dep_ids[j]);
+        k.ready_pos = -1;
+        k.dep_off = (int32_t)s->dep_arena.size();
+        k.dep_n = 0;
+        for (int32_t j = dep_off[i]; j < dep_off[i + 1]; ++j) {   // set semantics: de-duplicate
+            bool dup = false;
+            for (int32_t q = 0; q < k.dep_n; ++q) dup |= s->dep_arena[k.dep_off + q] == dep_ids[j];
+            if (!dup) {
+                s->dep_arena.push_back(dep_ids[j]);
+                ++k.dep_n;
+            }
         }
-    }
-    s->requests.push_back(std::move(r));
-    s->request_slot[request_id] = rslot;
-    for (int32_t i = 0; i < n; ++i) {
         const int32_t slot = (int32_t)s->kernels.size();
-        KernelRec& k = recs[i];
         // a re-used kernel id shadows the old record (dict assignment semantics)
-        auto old = s->kernel_slot.find(k.id);
-        if (old != s->kernel_slot.end()) {
-            ready_remove(s, old->second);
-            s->kernels[old->second].blocked = false;
+        const int32_t old = s->kernel_slot.find(k.id);
+        if (old >= 0) {
+            ready_remove(s, old);
+            s->kernels[old].blocked = false;
         }
-        s->kernel_slot[k.id] = slot;
-        const bool has_deps = !k.waiting.empty();
-        s->kernels.push_back(std::move(k));
-        s->requests[rslot].kernels.push_back(slot);
-        if (out_pred) out_pred[i] = s->kernels[slot].predicted;
-        if (has_deps)
-            s->kernels[slot].blocked = true;
-        else
-            ready_add(s, slot);
+        s->kernel_slot.put(k.id, slot);
+        k.blocked = k.dep_n > 0;
+        s->kernels.push_back(k);
+        if (out_pred) out_pred[i] = k.predicted;
+        if (!k.blocked) ready_add(s, slot);
     }
     *accepted = 1;
     return GMX_OK;
@@ -977,7 +1045,8 @@ int gmx_sched_step(gmx_sched* s, int64_t now, gmx_step_view* out) {
     s->v_disp_kids.clear();
     s->v_held_kids.clear();
     s->v_held_off.assign(1, 0);
-    std::vector<int64_t> wakeups;
+    std::vector<int64_t>& wakeups = s->s_wakeups;
+    wakeups.clear();
     int rc = GMX_OK;
     switch (s->policy) {
         case GMX_POLICY_FIFO: rc = step_serial(s, now, false); break;
@@ -999,11 +1068,11 @@ int gmx_sched_step(gmx_sched* s, int64_t now, gmx_step_view* out) {
 }
 
 int gmx_sched_complete(gmx_sched* s, int64_t did, int64_t now, gmx_complete_view* out) {
+    (void)now;
     if (!s || !out) return fail(GMX_EINVAL, "null argument");
-    auto it = s->in_flight.find(did);
-    if (it == s->in_flight.end()) return fail(GMX_ENOTFOUND, "unknown dispatch id");
-    DispatchRec d = std::move(it->second);
-    s->in_flight.erase(it);
+    const int32_t pi = s->inflight_slot.find(did);
+    if (pi < 0) return fail(GMX_ENOTFOUND, "unknown dispatch id");
+    DispatchRec& d = s->pool[pi];
     s->free_sms += d.rec.sm_allocation;
     s->v_ids_a.clear();  // kernel ids
     s->v_ids_b.clear();  // finished requests
@@ -1028,6 +1097,7 @@ int gmx_sched_complete(gmx_sched* s, int64_t did, int64_t now, gmx_complete_view
     out->finished_request_ids = s->v_ids_b.data();
     out->n_unlocked = (int32_t)s->v_ids_c.size();
     out->unlocked_kernel_ids = s->v_ids_c.data();
+    release_dispatch(s, pi);
     return GMX_OK;
 }
 
@@ -1036,17 +1106,16 @@ int gmx_sched_evict_stream(gmx_sched* s, int32_t stream, int64_t now, gmx_evict_
     if (!s || !out) return fail(GMX_EINVAL, "null argument");
     if (stream < 0 || stream >= (int32_t)s->stream_names.size()) return fail(GMX_EINVAL, "unknown stream");
     s->evicted_stream[stream] = 1;
-    s->v_ids_a.clear();  // cancelled dispatches
+    s->v_ids_a.clear();  // cancelled dispatches (dispatch-id order == insertion order)
     s->v_ids_b.clear();  // evicted requests
     s->v_ids_c.clear();  // dropped kernels
-    for (auto it = s->in_flight.begin(); it != s->in_flight.end();) {
-        if (it->second.streams.size() == 1 && it->second.streams[0] == stream) {
-            s->v_ids_a.push_back(it->first);
-            s->free_sms += it->second.rec.sm_allocation;
-            it = s->in_flight.erase(it);
-        } else {
-            ++it;
-        }
+    for (const DispatchRec& d : s->pool)
+        if (d.live && d.streams.size() == 1 && d.streams[0] == stream) s->v_ids_a.push_back(d.rec.dispatch_id);
+    std::sort(s->v_ids_a.begin(), s->v_ids_a.end());
+    for (int64_t did : s->v_ids_a) {
+        const int32_t pi = s->inflight_slot.find(did);
+        s->free_sms += s->pool[pi].rec.sm_allocation;
+        release_dispatch(s, pi);
     }
     for (RequestRec& r : s->requests) {
         if (r.stream != stream || r.finished) continue;
@@ -1054,12 +1123,12 @@ int gmx_sched_evict_stream(gmx_sched* s, int32_t stream, int64_t now, gmx_evict_
             r.evicted = true;
             s->v_ids_b.push_back(r.id);
         }
-        for (int32_t slot : r.kernels) {
+        for (int32_t slot = r.first; slot < r.first + r.count; ++slot) {
             KernelRec& k = s->kernels[slot];
             if (k.ready_pos >= 0 || k.blocked) s->v_ids_c.push_back(k.id);
             ready_remove(s, slot);
             k.blocked = false;
-            k.waiting.clear();
+            k.dep_n = 0;
         }
     }
     std::sort(s->v_ids_b.begin(), s->v_ids_b.end());
@@ -1073,8 +1142,8 @@ int gmx_sched_evict_stream(gmx_sched* s, int32_t stream, int64_t now, gmx_evict_
 }
 
 static const KernelRec* find_kernel(const gmx_sched* s, int64_t id) {
-    auto it = s->kernel_slot.find(id);
-    return it == s->kernel_slot.end() ? nullptr : &s->kernels[it->second];
+    const int32_t slot = s->kernel_slot.find(id);
+    return slot < 0 ? nullptr : &s->kernels[slot];
 }
 
 int gmx_sched_predicted_remaining(const gmx_sched* s, int64_t id, int64_t* out) {

@@ -25,6 +25,7 @@
 
 #include "../../../include/gmx_exec.h"
 #include "sm100_ptx.cuh"
+#include "../core/flatmap.hpp"
 
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -40,6 +41,7 @@
 #include <numeric>
 #include <queue>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 namespace gmx {
@@ -107,7 +109,8 @@ struct KernelArgs {
     const int32_t* cta_flags;
     float* ws;
     int32_t* counters;
-    uint64_t* trace;         // optional: 4 globaltimer stamps per item (debug/profiling)
+    uint64_t* trace;         // optional: 8 globaltimer stamps per item (debug/profiling)
+    int32_t dbg;             // experiment flags (reserved)
 };
 
 __device__ __forceinline__ float apply_act(float x, int32_t act) {
@@ -224,136 +227,171 @@ __device__ __forceinline__ void store_tile_chunk(const EpiParams& E, int row0, i
     }
 }
 
-// Split-K workspace layout of one output tile: [split][column][row (128)] fp32, so a warp's
-// access for one column is one coalesced 128-byte line (lanes = consecutive tile rows).
-__device__ __forceinline__ float* ws_chunk(float* tile_base, int bn, int sp, int c, int trow) {
-    return tile_base + (int64_t)sp * kTileRows * bn + (int64_t)(c * 32) * kTileRows + trow;
+// ---- staged output: chunk values -> output staging (TMA box layout) -> TMA store ---------
+//   non-swap: tile rows = m (128), chunk = 32 n-columns; box {128 B of n, 128 m-rows}
+//   swap:     tile rows = n (128), chunk = 32 m-rows;    box {128 B of n, 32 m-rows}
+// Staging slots hold 128 x 32 output elements (8 KB bf16 / 16 KB fp32), SWIZZLE_128B.
+__device__ __forceinline__ int out_chunks_per_pass(const EpiParams& E) {
+    return kStageOut / (128 * 32 * (E.out_dt == GMX_ST_BF16 ? 2 : 4));
 }
 
-__device__ __forceinline__ void ws_store_chunk(float* dst, const float (&v)[32]) {
+__device__ __forceinline__ void stage_out_chunk(const EpiParams& E, const float (&v)[32], int slot, int trow,
+                                                uint32_t stg_u32) {
+    const int esz = E.out_dt == GMX_ST_BF16 ? 2 : 4;
+    if (!E.swap) {
+        const uint32_t row_base = (uint32_t)trow * 128u;
+        const uint32_t sw = (uint32_t)(trow & 7);
+        if (esz == 2) {
+            const uint32_t sub = stg_u32 + (uint32_t)(slot >> 1) * 16384u + row_base;
+            const uint32_t h = (uint32_t)(slot & 1) * 4u;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) __stcg(dst + j * kTileRows, v[j]);
-}
-
-// Sum the chunk over all splits in split order (deterministic) with two splits' loads in
-// flight per round (64 independent coalesced loads per thread).
-__device__ __forceinline__ void ws_reduce_chunk(const float* tile_base, int bn, int nsplit, int c, int trow,
-                                                float (&v)[32]) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = 0.0f;
-    for (int sp = 0; sp < nsplit; sp += 2) {
-        const float* pa = ws_chunk(const_cast<float*>(tile_base), bn, sp, c, trow);
-        float a[32], b[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) a[j] = __ldcg(pa + j * kTileRows);
-        if (sp + 1 < nsplit) {
-            const float* pb = pa + (int64_t)kTileRows * bn;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) b[j] = __ldcg(pb + j * kTileRows);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = (v[j] + a[j]) + b[j];
+            for (int q = 0; q < 4; ++q)
+                st_shared_v4(sub + (((h + q) ^ sw) << 4), pack_bf16x2(v[8 * q], v[8 * q + 1]),
+                             pack_bf16x2(v[8 * q + 2], v[8 * q + 3]), pack_bf16x2(v[8 * q + 4], v[8 * q + 5]),
+                             pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
         } else {
+            const uint32_t sub = stg_u32 + (uint32_t)slot * 16384u + row_base;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += a[j];
+            for (int q = 0; q < 8; ++q)
+                st_shared_v4(sub + (((uint32_t)q ^ sw) << 4), __float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]),
+                             __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
+        }
+    } else {
+        const int inner = 128 / esz;
+        const uint32_t sb = (uint32_t)(trow / inner);
+        const uint32_t byte = (uint32_t)(trow % inner) * (uint32_t)esz;
+        const uint32_t base = stg_u32 + (uint32_t)slot * (uint32_t)(128 * 32 * esz) + sb * 4096u + (byte & 15u);
+        const uint32_t unit = byte >> 4;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t addr = base + (uint32_t)j * 128u + ((unit ^ (uint32_t)(j & 7)) << 4);
+            if (esz == 2)
+                st_shared_u16(addr, __bfloat16_as_ushort(__float2bfloat16_rn(v[j])));
+            else
+                st_shared_f32(addr, v[j]);
         }
     }
 }
 
-// Staged epilogue: accumulator chunks (32 columns each) -> bias/activation -> bf16/fp32 ->
-// SWIZZLE_128B smem staging laid out exactly as the output TMA box -> cp.async.bulk.tensor
-// store. Chunks come from TMEM (kFromTmem: the accumulator is released to the MMA warp right
-// after its last tcgen05.ld) or from the split-K workspace (reduced in split order).
-//   non-swap: tile rows = m (128), chunk = 32 n-columns; box {128 B of n, 128 m-rows}
-//   swap:     tile rows = n (128), chunk = 32 m-rows;    box {128 B of n, 32 m-rows}
-template <bool kFromTmem>
-__device__ __forceinline__ void epilogue_staged(const EpiParams& E, int row0, int col0, uint8_t* stg, int trow,
-                                                int etid, uint32_t taddr, const float* ws_base, int nsplit,
-                                                uint64_t* tempty_bar, uint64_t* tr = nullptr) {
+// One thread: TMA-store the staged chunks c0..cend-1 of the tile at (row0, col0).
+__device__ __forceinline__ void issue_out_stores(const EpiParams& E, int row0, int col0, int c0, int cend,
+                                                 uint8_t* stg) {
     const int esz = E.out_dt == GMX_ST_BF16 ? 2 : 4;
-    const int inner = 128 / esz;                      // elements per 128-byte box row
+    const int inner = 128 / esz;
+    for (int c = c0; c < cend; ++c) {
+        const int slot = c - c0;
+        if (!E.swap) {
+            if (esz == 2) {
+                if ((slot & 1) == 0) tma_store_2d(E.tm_out, stg + (slot >> 1) * 16384, col0 + c * 32, row0);
+            } else {
+                tma_store_2d(E.tm_out, stg + slot * 16384, col0 + c * 32, row0);
+            }
+        } else {
+            for (int sb = 0; sb < 128 / inner; ++sb)
+                tma_store_2d(E.tm_out, stg + slot * (128 * 32 * esz) + sb * 4096, row0 + sb * inner, col0 + c * 32);
+        }
+    }
+    bulk_commit();
+}
+
+// Epilogue of an unsplit tile: TMEM chunks -> bias/activation -> staging -> TMA store. The
+// accumulator is released to the MMA warp right after its last tcgen05.ld.
+__device__ __forceinline__ void epilogue_staged(const EpiParams& E, int row0, int col0, uint8_t* stg, int trow,
+                                                int etid, uint32_t taddr, uint64_t* tempty_bar,
+                                                uint64_t* tr = nullptr) {
     const int nchunks = E.bn / 32;
-    const int chunk_bytes = 128 * 32 * esz;
-    const int per_pass = kStageOut / chunk_bytes;     // 4 (bf16) or 2 (fp32)
-    const int64_t tile_floats = (int64_t)kTileRows * E.bn;
+    const int per_pass = out_chunks_per_pass(E);
     const uint32_t stg_u32 = smem_u32(stg);
     const int lane = lane_id();
     for (int c0 = 0; c0 < nchunks; c0 += per_pass) {
         const int cend = min(nchunks, c0 + per_pass);
-        float vbuf[32];
-        // staging must be free: the previous TMA store has finished reading it
-        if (etid == 0) bulk_wait_read0();
+        if (etid == 0) bulk_wait_read0();   // staging free: previous store has read it
         named_bar_sync(3, 128);
         if (tr && etid == 0 && c0 == 0) tr[4] = global_timer_ns();
         for (int c = c0; c < cend; ++c) {
-            float (&v)[32] = vbuf;
-            if constexpr (kFromTmem) {
-                tmem_ld32(taddr + (uint32_t)(c * 32), v);
-                if (c == nchunks - 1) {
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(tempty_bar);
-                }
-            } else {
-                ws_reduce_chunk(ws_base, E.bn, nsplit, c, trow, v);
+            float v[32];
+            tmem_ld32(taddr + (uint32_t)(c * 32), v);
+            if (c == nchunks - 1) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty_bar);
             }
-            const int slot = c - c0;
             transform_chunk(v, E, E.swap ? col0 + c * 32 : row0 + trow, E.swap);
-            if (!E.swap) {
-                const uint32_t row_base = (uint32_t)trow * 128u;
-                const uint32_t sw = (uint32_t)(trow & 7);
-                if (esz == 2) {
-                    const uint32_t sub = stg_u32 + (uint32_t)(slot >> 1) * 16384u + row_base;
-                    const uint32_t h = (uint32_t)(slot & 1) * 4u;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        st_shared_v4(sub + (((h + q) ^ sw) << 4), pack_bf16x2(v[8 * q], v[8 * q + 1]),
-                                     pack_bf16x2(v[8 * q + 2], v[8 * q + 3]), pack_bf16x2(v[8 * q + 4], v[8 * q + 5]),
-                                     pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
-                } else {
-                    const uint32_t sub = stg_u32 + (uint32_t)slot * 16384u + row_base;
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        st_shared_v4(sub + (((uint32_t)q ^ sw) << 4), __float_as_uint(v[4 * q]),
-                                     __float_as_uint(v[4 * q + 1]), __float_as_uint(v[4 * q + 2]),
-                                     __float_as_uint(v[4 * q + 3]));
-                }
-            } else {
-                const uint32_t sb = (uint32_t)(trow / inner);
-                const uint32_t byte = (uint32_t)(trow % inner) * (uint32_t)esz;
-                const uint32_t base = stg_u32 + (uint32_t)slot * (uint32_t)chunk_bytes + sb * 4096u + (byte & 15u);
-                const uint32_t unit = byte >> 4;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const uint32_t addr = base + (uint32_t)j * 128u + ((unit ^ (uint32_t)(j & 7)) << 4);
-                    if (esz == 2)
-                        st_shared_u16(addr, __bfloat16_as_ushort(__float2bfloat16_rn(v[j])));
-                    else
-                        st_shared_f32(addr, v[j]);
-                }
-            }
+            stage_out_chunk(E, v, c - c0, trow, stg_u32);
         }
         if (tr && etid == 0 && c0 == 0) tr[5] = global_timer_ns();
         fence_async_smem();
         named_bar_sync(3, 128);
         if (tr && etid == 0 && c0 == 0) tr[6] = global_timer_ns();
         if (etid == 0) {
-            for (int c = c0; c < cend; ++c) {
-                const int slot = c - c0;
-                if (!E.swap) {
-                    if (esz == 2) {
-                        if ((slot & 1) == 0)
-                            tma_store_2d(E.tm_out, stg + (slot >> 1) * 16384, col0 + c * 32, row0);
-                    } else {
-                        tma_store_2d(E.tm_out, stg + slot * 16384, col0 + c * 32, row0);
-                    }
-                } else {
-                    for (int sb = 0; sb < 128 / inner; ++sb)
-                        tma_store_2d(E.tm_out, stg + slot * chunk_bytes + sb * 4096, row0 + sb * inner, col0 + c * 32);
-                }
-            }
-            bulk_commit();
+            issue_out_stores(E, row0, col0, c0, cend, stg);
             if (tr && c0 == 0) tr[7] = global_timer_ns();
         }
+    }
+}
+
+// ---- split-K: fp32 reductions into an L2-resident accumulator tile ---------------------
+// Accumulator layout of a tile: [column (bn)][row (128)] fp32 — for a fixed column a warp
+// touches one 128-byte line (lanes = consecutive tile rows), so the RED/LD/ST traffic is fully
+// coalesced. Splits add their partials with fire-and-forget `red.global.add.f32`; the last
+// arrival (per-tile counter) reads the sum once, re-zeroes it and runs the output epilogue.
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+__device__ __forceinline__ void split_partial_reduce(const EpiParams& E, float* acc_tile, int trow,
+                                                     uint32_t taddr, uint64_t* tempty_bar) {
+    const int nchunks = E.bn / 32;
+    const int lane = lane_id();
+    for (int c = 0; c < nchunks; ++c) {
+        float v[32];
+        tmem_ld32(taddr + (uint32_t)(c * 32), v);
+        if (c == nchunks - 1) {   // accumulator free for the next tile's MMAs
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty_bar);
+        }
+        float* col = acc_tile + (int64_t)(c * 32) * kTileRows + trow;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) red_add_f32(col + j * kTileRows, v[j]);
+    }
+}
+
+__device__ __forceinline__ void split_finalize(const EpiParams& E, int row0, int col0, float* acc_tile,
+                                               uint8_t* stg, int trow, int etid) {
+    const int nchunks = E.bn / 32;
+    const int per_pass = out_chunks_per_pass(E);
+    const uint32_t stg_u32 = smem_u32(stg);
+    for (int c0 = 0; c0 < nchunks; c0 += per_pass) {
+        const int cend = min(nchunks, c0 + per_pass);
+        if (etid == 0) bulk_wait_read0();
+        named_bar_sync(3, 128);
+        for (int c = c0; c < cend; c += 2) {
+            float v0[32], v1[32];
+            float* col0p = acc_tile + (int64_t)(c * 32) * kTileRows + trow;
+            const bool two = c + 1 < cend;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v0[j] = __ldcg(col0p + j * kTileRows);
+            if (two) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v1[j] = __ldcg(col0p + (32 + j) * kTileRows);
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) __stcg(col0p + j * kTileRows, 0.0f);   // re-arm
+            if (two) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) __stcg(col0p + (32 + j) * kTileRows, 0.0f);
+            }
+            transform_chunk(v0, E, E.swap ? col0 + c * 32 : row0 + trow, E.swap);
+            stage_out_chunk(E, v0, c - c0, trow, stg_u32);
+            if (two) {
+                transform_chunk(v1, E, E.swap ? col0 + (c + 1) * 32 : row0 + trow, E.swap);
+                stage_out_chunk(E, v1, c + 1 - c0, trow, stg_u32);
+            }
+        }
+        fence_async_smem();
+        named_bar_sync(3, 128);
+        if (etid == 0) issue_out_stores(E, row0, col0, c0, cend, stg);
     }
 }
 
@@ -462,7 +500,8 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
     uint64_t* empty = full + kStages;
     uint64_t* tfull = empty + kStages;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* ebar = tempty + 2;                                       // epilogue bulk loads
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 1);
     int32_t* split_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5;
@@ -481,6 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 4);   // one arrival per epilogue warp
         }
+        mbar_init(ebar, 1);
         mbar_fence_init();
     }
     if (warp == 1 && has_gemm) tmem_alloc(tmem_slot, kTmemCols);
@@ -500,6 +540,8 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
                 const DevProblem* P = args.probs + it.problem;
                 const uint32_t bytes = kStageA + (uint32_t)P->bn * (kBlockK * 2);
                 if (args.trace) args.trace[8 * i + 0] = global_timer_ns();
+                tma_prefetch_desc(&P->tm_rows);   // descriptor fetch overlaps the slot wait
+                tma_prefetch_desc(&P->tm_cols);
                 for (int kb = it.kb0; kb < it.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* tile = smem + stage * kStageBytes;
@@ -547,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
         const int trow = lgrp * 32 + lane;       // tile row owned by this thread
         const int etid = ew * 32 + lane;         // 0..127
         int acc = 0;
-        uint32_t acc_phase = 0;
+        uint32_t acc_phase = 0, ephase = 0;
         for (int i = beg; i < end; ++i) {
             const WorkItem it = args.items[i];
             const DevProblem* Pg = args.probs + it.problem;
@@ -560,58 +602,45 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
                 const uint32_t taddr = tmem_base + ((uint32_t)(lgrp * 32) << 16) + (uint32_t)acc * kMaxBN;
                 const int nchunks = E.bn / 32;
                 const bool split = it.nsplit > 1;
-                const int64_t tile_floats = (int64_t)kTileRows * E.bn;
                 if (!split && E.tma_out) {
-                    epilogue_staged<true>(E, it.row0, it.col0, stg, trow, etid, taddr, nullptr, 1, &tempty[acc],
-                                          args.trace ? args.trace + 8 * i : nullptr);
-                } else {
-                    float* tile_ws = split ? args.ws + (int64_t)it.ws_blk * kWsBlock : nullptr;
+                    epilogue_staged(E, it.row0, it.col0, stg, trow, etid, taddr, &tempty[acc],
+                                    args.trace ? args.trace + 8 * i : nullptr);
+                } else if (!split) {
                     for (int c = 0; c < nchunks; ++c) {
                         float v[32];
                         tmem_ld32(taddr + (uint32_t)(c * 32), v);
-                        if (!split)
-                            store_tile_chunk(E, it.row0, it.col0, trow, c, v);
-                        else
-                            ws_store_chunk(ws_chunk(tile_ws, E.bn, it.split, c, trow), v);
+                        store_tile_chunk(E, it.row0, it.col0, trow, c, v);
                     }
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[acc]);
-                }
-                acc ^= 1;
-                if (acc == 0) acc_phase ^= 1;
-                if (split) {
-                    // Serial split-K fixup: the CTA that completes a tile's arrival count reduces
-                    // all partials in split order (deterministic). One thread publishes with a
-                    // release fence + relaxed atomic after a CTA barrier; the winner acquires.
+                } else {
+                    // split-K (planner only splits TMA-store problems): reduce-add this split's
+                    // partial into the tile's fp32 accumulator; the last arrival finalizes.
+                    float* acc_tile = args.ws + (int64_t)it.ws_blk * kWsBlock;
                     uint64_t* tr = args.trace ? args.trace + 8 * i : nullptr;
+                    split_partial_reduce(E, acc_tile, trow, taddr, &tempty[acc]);
                     if (tr && etid == 0) tr[4] = global_timer_ns();
-                    named_bar_sync(1, 128);
-                    if (tr && etid == 0) tr[5] = global_timer_ns();
+                    named_bar_sync(1, 128);   // all of this CTA's REDs issued
                     if (etid == 0) {
-                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                        asm volatile("fence.acq_rel.gpu;" ::: "memory");   // release: REDs before the count
                         const int prev = atomicAdd(args.counters + it.tile_slot, 1);
                         const int last = prev == it.nsplit - 1;
-                        if (last) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                        if (last) {
+                            asm volatile("fence.acq_rel.gpu;" ::: "memory");   // acquire the others' REDs
+                            args.counters[it.tile_slot] = 0;   // re-arm for the next launch
+                        }
                         *split_flag = last;
                     }
                     named_bar_sync(1, 128);
-                    if (tr && etid == 0) tr[6] = global_timer_ns();
+                    if (tr && etid == 0) tr[5] = global_timer_ns();
                     if (*split_flag) {
-                        const float* base = args.ws + (int64_t)it.ws_blk * kWsBlock;
-                        if (E.tma_out) {
-                            epilogue_staged<false>(E, it.row0, it.col0, stg, trow, etid, 0, base, it.nsplit, nullptr);
-                        } else {
-                            for (int c = 0; c < nchunks; ++c) {
-                                float v[32];
-                                ws_reduce_chunk(base, E.bn, it.nsplit, c, trow, v);
-                                store_tile_chunk(E, it.row0, it.col0, trow, c, v);
-                            }
-                        }
-                        if (etid == 0) args.counters[it.tile_slot] = 0;   // re-arm for the next launch
-                        if (tr && etid == 0) tr[7] = global_timer_ns();
+                        split_finalize(E, it.row0, it.col0, acc_tile, stg, trow, etid);
+                        if (tr && etid == 0) tr[6] = global_timer_ns();
                     }
                 }
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
             } else if (it.type == kItemGemv) {
                 if (Pg->in_dt == GMX_ST_F32)
                     gemv_rows<float>(Pg, it.row0, it.col0, ew);
@@ -694,6 +723,7 @@ struct HostProblem {
 };
 
 struct Plan {
+    std::vector<int32_t> key;       // sorted slot list this plan was built for
     std::vector<WorkItem> items;
     std::vector<int32_t> cta_off;
     WorkItem* d_items = nullptr;
@@ -717,7 +747,9 @@ struct gmx_exec {
     gmx::DevProblem* d_probs = nullptr;
     size_t d_cap = 0;
     bool table_dirty = false;
-    std::map<std::vector<int32_t>, std::unique_ptr<gmx::Plan>> plans;
+    std::unordered_map<uint64_t, std::vector<std::unique_ptr<gmx::Plan>>> plans;   // hash(slots) -> plans
+    size_t n_plans = 0;
+    std::vector<int32_t> key_scratch;
     gmx::Plan* last = nullptr;
     std::unique_ptr<gmx::Plan> uncached;
     float* ws = nullptr;
@@ -728,6 +760,7 @@ struct gmx_exec {
     bool cache_plans = true;
     bool attr_set = false;
     bool tracing = false;
+    int32_t dbg = 0;
     uint64_t* trace = nullptr;
     int64_t trace_cap = 0;
     int64_t trace_items = 0;
@@ -793,14 +826,14 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
     for (const TileRef& t : tiles) {
         const DevProblem& P = ex->probs[t.slot].dev;
         int nsplit = 1;
-        if (t.cost > target && P.kblocks >= 2)
+        if (t.cost > target && P.kblocks >= 2 && P.tma_out)
             nsplit = (int)std::min<int64_t>({(int64_t)std::ceil(t.cost / target), (int64_t)P.kblocks, ex->max_split, 255});
         ++st.n_gemm_tiles;
         int32_t slot = -1, blk = 0;
         if (nsplit > 1) {
             slot = n_counters++;
             blk = (int32_t)ws_blocks;
-            ws_blocks += ((int64_t)nsplit * kTileRows * P.bn + kWsBlock - 1) / kWsBlock;
+            ws_blocks += ((int64_t)kTileRows * P.bn + kWsBlock - 1) / kWsBlock;   // one fp32 accumulator tile
         }
         for (int sp = 0; sp < nsplit; ++sp) {
             WorkItem it{};
@@ -911,6 +944,7 @@ static int ensure_workspace(gmx_exec* ex, const Plan& plan) {
     if (plan.ws_floats > ex->ws_cap) {
         if (ex->ws) GMX_CUDA(cudaFree(ex->ws));
         GMX_CUDA(cudaMalloc(&ex->ws, plan.ws_floats * sizeof(float)));
+        GMX_CUDA(cudaMemset(ex->ws, 0, plan.ws_floats * sizeof(float)));   // accumulators start at zero
         ex->ws_cap = plan.ws_floats;
     }
     if (plan.n_counters > ex->counters_cap) {
@@ -1069,12 +1103,16 @@ int gmx_exec_unregister(gmx_exec* ex, int32_t slot) {
         return fail(GMX_EINVAL, "bad slot");
     ex->probs[slot].live = false;
     // plans referencing the slot become invalid
-    for (auto it = ex->plans.begin(); it != ex->plans.end();) {
-        if (std::find(it->first.begin(), it->first.end(), slot) != it->first.end()) {
-            if (ex->last == it->second.get()) ex->last = nullptr;
-            it = ex->plans.erase(it);
-        } else {
-            ++it;
+    for (auto& kv : ex->plans) {
+        auto& bucket = kv.second;
+        for (size_t i = 0; i < bucket.size();) {
+            if (std::binary_search(bucket[i]->key.begin(), bucket[i]->key.end(), slot)) {
+                if (ex->last == bucket[i].get()) ex->last = nullptr;
+                bucket.erase(bucket.begin() + i);
+                --ex->n_plans;
+            } else {
+                ++i;
+            }
         }
     }
     return GMX_OK;
@@ -1084,25 +1122,38 @@ int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream_
     if (!ex || (n > 0 && !slots)) return fail(GMX_EINVAL, "null argument");
     if (n == 0) return GMX_OK;
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
-    std::vector<int32_t> key(slots, slots + n);
+    std::vector<int32_t>& key = ex->key_scratch;
+    key.assign(slots, slots + n);
     std::sort(key.begin(), key.end());
-    for (int32_t s : key)
+    uint64_t h = 0x6A09E667F3BCC909ull ^ (uint64_t)n;
+    for (int32_t s : key) {
         if (s < 0 || s >= (int32_t)ex->probs.size() || !ex->probs[s].live) return fail(GMX_EINVAL, "bad slot");
+        h = mix64(h ^ (uint64_t)(uint32_t)s);
+    }
     int rc;
     if ((rc = ensure_table(ex, stream))) return rc;
     Plan* plan = nullptr;
     bool cached = false;
     if (ex->cache_plans) {
-        auto it = ex->plans.find(key);
-        if (it != ex->plans.end()) {
-            plan = it->second.get();
-            cached = true;
-        } else {
-            if (ex->plans.size() >= 512) ex->plans.clear(), ex->last = nullptr;
+        auto& bucket = ex->plans[h];
+        for (auto& p : bucket)
+            if (p->key == key) {
+                plan = p.get();
+                cached = true;
+                break;
+            }
+        if (!plan) {
+            if (ex->n_plans >= 512) {
+                ex->plans.clear();
+                ex->n_plans = 0;
+                ex->last = nullptr;
+            }
             auto p = std::make_unique<Plan>();
             if ((rc = build_plan(ex, key, *p))) return rc;
+            p->key = key;
             plan = p.get();
-            ex->plans.emplace(key, std::move(p));
+            ex->plans[h].push_back(std::move(p));
+            ++ex->n_plans;
         }
     } else {
         ex->uncached = std::make_unique<Plan>();
@@ -1124,7 +1175,7 @@ int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream_
         ex->trace_items = (int64_t)plan->items.size();
     }
     KernelArgs args{ex->d_probs, plan->d_items, plan->d_off, plan->d_off + plan->stats.grid + 1, ex->ws,
-                    ex->counters, ex->tracing ? ex->trace : nullptr};
+                    ex->counters, ex->tracing ? ex->trace : nullptr, ex->dbg};
     coalesced_step_kernel<<<plan->stats.grid, kThreads, kSmemBytes, stream>>>(args);
     GMX_CUDA(cudaGetLastError());
     plan->stats.cached = cached;
@@ -1142,6 +1193,7 @@ int gmx_exec_last_plan(const gmx_exec* ex, gmx_plan_stats* out) {
 int gmx_exec_clear_plans(gmx_exec* ex) {
     if (!ex) return fail(GMX_EINVAL, "null argument");
     ex->plans.clear();
+    ex->n_plans = 0;
     ex->last = nullptr;
     return GMX_OK;
 }
@@ -1154,6 +1206,9 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
         ex->max_split = value;
     } else if (n == "cache_plans") {
         ex->cache_plans = value != 0;
+    } else if (n == "dbg") {
+        ex->dbg = (int32_t)value;
+        return GMX_OK;
     } else if (n == "trace") {
         ex->tracing = value != 0;
         return GMX_OK;
@@ -1161,6 +1216,7 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
         return fail(GMX_EINVAL, "unknown option " + n);
     }
     ex->plans.clear();
+    ex->n_plans = 0;
     ex->last = nullptr;
     return GMX_OK;
 }

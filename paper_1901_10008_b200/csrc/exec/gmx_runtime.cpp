@@ -1,14 +1,16 @@
 // gmx_runtime.cpp — native event loop driving the decision core and the executor.
 //
 // engine.py:320-367 restated: one scheduler step per distinct timestamp after draining every
-// event at that time; each step's dispatches become ONE coalesced launch.
+// event at that time (COMPLETE < ARRIVAL < WAKEUP, ascending id); each step's dispatches become
+// ONE coalesced launch. Storage is flat (pooled request records, kernel/dependency arenas,
+// open-addressing id maps) so a steady-state round performs no heap allocation.
 
 #include "../../../include/gmx_runtime.h"
+#include "../core/flatmap.hpp"
 
 #include <algorithm>
 #include <queue>
 #include <string>
-#include <unordered_map>
 #include <vector>
 
 namespace {
@@ -33,12 +35,13 @@ struct Event {
     }
 };
 
-struct PendingRequest {
+struct Pending {                 // one submitted request, pooled
+    int64_t request_id;
     int32_t stream;
     int64_t arrival, deadline;
-    std::vector<gmx_kernel_desc> kernels;
-    std::vector<int64_t> dep_ids;
-    std::vector<int32_t> dep_off;
+    int32_t k_off, n;            // kernels in the kernel arena
+    int32_t d_off;               // dependency CSR: offsets in off_arena[d_off .. d_off + n]
+    bool arrived;
 };
 
 }  // namespace
@@ -48,15 +51,32 @@ struct gmx_runtime {
     gmx_exec* ex;
     int32_t mode;
     std::priority_queue<Event, std::vector<Event>, std::greater<Event>> heap;
-    std::unordered_map<int64_t, PendingRequest> pending;     // request id -> not yet arrived
-    std::unordered_map<int64_t, int32_t> slot_of;            // kernel id -> executor slot
-    std::unordered_map<int64_t, int64_t> deadline_of;        // request id -> absolute deadline
-    std::unordered_map<int64_t, int64_t> flops_of;           // dispatch id -> useful flops
+    std::vector<Pending> pool;
+    std::vector<int32_t> pool_free;
+    gmx::IdMap req_index;                 // request id -> pool index (until the request finishes)
+    gmx::IdMap slot_of;                   // kernel id -> executor slot (until dispatched)
+    std::vector<gmx_kernel_desc> k_arena; // compacted when the pool drains
+    std::vector<int64_t> dep_arena;
+    std::vector<int32_t> off_arena;
     std::vector<int64_t> done_ids, done_times;
-    int64_t wake_seq = 0;
-    gmx_runtime_stats st{};
+    std::vector<int64_t> pred;
     std::vector<int32_t> launch_slots;
+    int64_t wake_seq = 0;
+    int64_t live_requests = 0;
+    gmx_runtime_stats st{};
 };
+
+static void release_request(gmx_runtime* rt, int64_t rid) {
+    const int32_t pi = rt->req_index.find(rid);
+    if (pi < 0) return;
+    rt->req_index.erase(rid);
+    rt->pool_free.push_back(pi);
+    if (--rt->live_requests == 0) {   // nothing outstanding: recycle the arenas
+        rt->k_arena.clear();
+        rt->dep_arena.clear();
+        rt->off_arena.clear();
+    }
+}
 
 extern "C" {
 
@@ -79,23 +99,40 @@ int gmx_runtime_submit(gmx_runtime* rt, int64_t rid, int32_t stream, int64_t arr
                        const gmx_kernel_desc* ks, int32_t n, const int64_t* dep_ids, const int32_t* dep_off,
                        const int32_t* slots) {
     if (!rt || (n > 0 && (!ks || !dep_off || !slots))) return fail(GMX_EINVAL, "null argument");
-    PendingRequest p;
+    if (rt->req_index.find(rid) >= 0) return fail(GMX_EINVAL, "request id already pending");
+    int32_t pi;
+    if (!rt->pool_free.empty()) {
+        pi = rt->pool_free.back();
+        rt->pool_free.pop_back();
+    } else {
+        pi = (int32_t)rt->pool.size();
+        rt->pool.emplace_back();
+    }
+    Pending& p = rt->pool[pi];
+    p.request_id = rid;
     p.stream = stream;
     p.arrival = arrival;
     p.deadline = deadline;
-    p.kernels.assign(ks, ks + n);
-    p.dep_off.assign(dep_off, dep_off + n + 1);
-    if (n > 0 && dep_off[n] > 0) p.dep_ids.assign(dep_ids, dep_ids + dep_off[n]);
-    for (int32_t i = 0; i < n; ++i) rt->slot_of[ks[i].kernel_id] = slots[i];
-    rt->pending[rid] = std::move(p);
-    rt->deadline_of[rid] = deadline;
+    p.k_off = (int32_t)rt->k_arena.size();
+    p.n = n;
+    p.d_off = (int32_t)rt->off_arena.size();
+    p.arrived = false;
+    rt->k_arena.insert(rt->k_arena.end(), ks, ks + n);
+    const int32_t dep_base = (int32_t)rt->dep_arena.size();
+    for (int32_t i = 0; i <= n; ++i) rt->off_arena.push_back(n > 0 ? dep_off[i] : 0);
+    if (n > 0 && dep_off[n] > 0) rt->dep_arena.insert(rt->dep_arena.end(), dep_ids, dep_ids + dep_off[n]);
+    // the n+1 CSR offsets are relative to this request's first dependency; a trailing
+    // sentinel records where those dependencies start in dep_arena
+    rt->off_arena.push_back(dep_base);
+    for (int32_t i = 0; i < n; ++i) rt->slot_of.put(ks[i].kernel_id, slots[i]);
+    rt->req_index.put(rid, pi);
+    ++rt->live_requests;
     rt->heap.push({arrival, kArrival, rid});
     return GMX_OK;
 }
 
 int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* stream, gmx_runtime_stats* out) {
     if (!rt) return fail(GMX_EINVAL, "null argument");
-    std::vector<int64_t> pred;
     while (!rt->heap.empty() && rt->heap.top().time <= until) {
         const int64_t now = rt->heap.top().time;
         while (!rt->heap.empty() && rt->heap.top().time == now) {
@@ -110,24 +147,25 @@ int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* stream, gmx_runtime_st
                     rt->done_ids.push_back(r);
                     rt->done_times.push_back(now);
                     ++rt->st.completed_requests;
-                    auto it = rt->deadline_of.find(r);
-                    if (it != rt->deadline_of.end()) {
-                        if (now > it->second) ++rt->st.slo_misses;
-                        rt->deadline_of.erase(it);
+                    const int32_t pi = rt->req_index.find(r);
+                    if (pi >= 0) {
+                        if (now > rt->pool[pi].deadline) ++rt->st.slo_misses;
+                        release_request(rt, r);
                     }
                 }
             } else if (e.kind == kArrival) {
-                auto it = rt->pending.find(e.id);
-                if (it == rt->pending.end()) continue;
-                PendingRequest& p = it->second;
-                const int32_t n = (int32_t)p.kernels.size();
-                pred.resize(std::max(1, n));
+                const int32_t pi = rt->req_index.find(e.id);
+                if (pi < 0 || rt->pool[pi].arrived) continue;
+                Pending& p = rt->pool[pi];
+                p.arrived = true;
+                rt->pred.resize((size_t)std::max(1, p.n));
+                const int32_t dep_base = rt->off_arena[p.d_off + p.n + 1];
                 int32_t accepted = 0;
-                int rc = gmx_sched_add_request(rt->sched, e.id, p.stream, p.arrival, p.kernels.data(), n,
-                                               p.dep_ids.empty() ? nullptr : p.dep_ids.data(), p.dep_off.data(),
-                                               pred.data(), &accepted);
+                int rc = gmx_sched_add_request(rt->sched, e.id, p.stream, p.arrival, rt->k_arena.data() + p.k_off,
+                                               p.n, rt->dep_arena.data() + dep_base, rt->off_arena.data() + p.d_off,
+                                               rt->pred.data(), &accepted);
                 if (rc) return fail(rc, std::string("add_request: ") + gmx_last_error());
-                rt->pending.erase(it);
+                if (!accepted) release_request(rt, e.id);
             }
         }
         gmx_step_view v;
@@ -140,10 +178,11 @@ int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* stream, gmx_runtime_st
             for (int32_t d = 0; d < v.n_dispatches; ++d) {
                 const gmx_dispatch_rec& r = v.dispatches[d];
                 for (int32_t j = 0; j < r.n_kernels; ++j) {
-                    auto it = rt->slot_of.find(v.dispatch_kernel_ids[r.kernel_offset + j]);
-                    if (it == rt->slot_of.end()) return fail(GMX_ESTATE, "dispatched kernel has no operands bound");
-                    rt->launch_slots.push_back(it->second);
-                    rt->slot_of.erase(it);
+                    const int64_t kid = v.dispatch_kernel_ids[r.kernel_offset + j];
+                    const int32_t slot = rt->slot_of.find(kid);
+                    if (slot < 0) return fail(GMX_ESTATE, "dispatched kernel has no operands bound");
+                    rt->launch_slots.push_back(slot);
+                    rt->slot_of.erase(kid);
                 }
                 rt->heap.push({r.end, kComplete, r.dispatch_id});
                 rt->st.useful_flops += r.useful_flops;

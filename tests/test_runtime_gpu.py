@@ -1,0 +1,84 @@
+"""The native serving loop (gmx_runtime) against the oracle engine, on the GPU.
+
+Lockstep mode keeps the reference's virtual clock, so every request's
+completion time from the native loop must equal the one the restated
+reference engine (oracle/sim.py, itself pinned to gpumux) computes for the
+same workload — while the dispatched members really execute on the B200 and
+their outputs match the numerics oracle.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import decisions as od  # noqa: E402
+from oracle import numerics as on  # noqa: E402
+from oracle import sim  # noqa: E402
+
+from .conftest import load_golden  # noqa: E402
+
+
+def _run_workload(workload, library, profile_name="b200", params=None, check_numerics=True):
+    import paper_1901_10008_b200 as gm
+    from paper_1901_10008_b200.executor import Executor, OperandSet
+    from paper_1901_10008_b200.runtime import Runtime
+
+    prof_raw = load_golden("profiles.json")[profile_name]
+    prof = gm.DeviceProfile(**prof_raw)
+    pp = gm.PolicyParams(**(params or {}))
+    ex = Executor()
+    rt = Runtime(ex, prof, gm.SchedulerPolicy("ooo", pp), jitter_state=od.derive_seed(0, "jitter"))
+    reqs = sim.materialize(workload, library, 0)
+    ops = {}
+    for r in reqs:
+        slots = []
+        for k in r.kernels:
+            o = OperandSet(k.op_kind, k.dims, dtype=k.dtype, seed=k.kernel_id % 997)
+            slots.append(o.register(ex))
+            ops[k.kernel_id] = o
+        rt.submit(gm.InferenceRequest(r.request_id, r.stream_id,
+                                      tuple(gm.KernelSpec(k.kernel_id, k.stream_id, k.op_kind, k.dims, k.dtype,
+                                                          k.deps, k.arrival, k.deadline) for k in r.kernels),
+                                      r.arrival, gm.LatencyConstraint.batch()), slots)
+    stats = rt.run()
+    torch.cuda.synchronize()
+    got = dict(rt.drain_completions())
+    # oracle: completion time per request from the restated reference engine
+    _trace, _metrics, _tl, osched = sim.simulate(workload, library, od.Prof(**prof_raw), "ooo",
+                                                 params=od.DEFAULT_PARAMS._replace(**(params or {})))
+    want = {rid: st["done_at"] for rid, st in osched.reqs.items() if st["done_at"] is not None}
+    assert got == want
+    if check_numerics:
+        for kid, o in ops.items():
+            a = o.a.float().cpu().numpy()
+            if o.op_kind == "gemm":
+                ref = on.gemm(a, o.b.float().cpu().numpy(), o.dims[2])
+            elif o.op_kind == "gemv":
+                ref = on.gemv(a, o.b.float().cpu().numpy())
+            else:
+                ref = on.elementwise(a)
+            got_c = o.c.float().cpu().numpy()
+            assert on.within(got_c, ref, o.c.dtype == torch.bfloat16), (kid, o.dims)
+    return stats
+
+
+def test_runtime_c2_matches_oracle_engine():
+    traces = load_golden("traces.json")
+    wl = traces["workloads"]["c2_resnet50_16"]
+    wl = dict(wl, streams=[dict(s, model_name="resnet50_like_fp16") for s in wl["streams"]])
+    lib = dict(load_golden("models.json"))
+    lib["resnet50_like_fp16"] = [dict(p, dtype="fp16") for p in lib["resnet50_like"]]
+    stats = _run_workload(wl, lib)
+    assert stats["completed_requests"] == 16 and stats["launches"] >= 1
+
+
+def test_runtime_mixed_chains_match_oracle_engine():
+    lib = dict(load_golden("models.json"))
+    wl = {"duration_ns": 2_000_000, "streams": [
+        {"stream_id": f"m{i}", "model_name": m, "slo_ns": 10_000_000,
+         "arrival": {"kind": "fixed", "schedule": [0, 150_000 * (i + 1)]}}
+        for i, m in enumerate(["mixed_fp16", "tiny_chain", "resnet50_fc", "eltwise_fp32", "mixed_fp16"])]}
+    stats = _run_workload(wl, lib, params={"stagger_horizon": 50_000})
+    assert stats["completed_requests"] == 10

@@ -39,21 +39,19 @@ for name, op, dims in (("tiny_elt", "elementwise", (1024,)), ("tiny_gemm", "gemm
 cases = [("square4096", [(4096, 4096, 4096)]), ("stream148x128", [(148 * 128, 128, 4096)]),
          ("stream148x64", [(148 * 128, 64, 4096)]), ("c2_512_49_4608", [(512, 49, 4608)]),
          ("wide_k64", [(256, 3136, 64)]), ("swap_64_3136_576", [(64, 3136, 576)])]
-for name, shapes in cases:
+for dbg in (0, 1):
+  ex.set_option("dbg", dbg)
+  print("dbg", dbg)
+  for name, shapes in cases:
     ops = [OperandSet("gemm", d, seed=1) for d in shapes]
     slots = [o.register(ex) for o in ops]
-    t = timeit(ex, slots)
-    plan = ex.last_plan()
-    fl = sum(2 * m * n * k for m, n, k in shapes)
-    by = plan["operand_bytes"]
-    print(f"{name:18s} {t*1e6:9.2f} us  {fl/t/1e12:8.1f} TFLOP/s  {by/t/1e9:8.1f} GB/s alg  "
-          f"{plan['tile_load_bytes']/t/1e9:8.1f} GB/s tile-load  grid {plan['grid']} items {plan['n_items']}")
     ex.set_option("trace", 1)
+    ex.launch(slots)
     ex.launch(slots)
     items, off = ex.read_trace()
     ex.set_option("trace", 0)
     t0 = min(it["t_prod"] for it in items if it["t_prod"])
     per_kb = [((it["t_mma_done"] - it["t_prod"]) / 1e3 / max(1, it["kb1"] - it["kb0"])) for it in items if it["t_mma_done"]]
-    print(f"    per-kblock us: median {statistics.median(per_kb):.3f}  end max {(max(it['t_end'] for it in items)-t0)/1e3:.2f} us")
+    print(f"  {name:18s} per-kblock us: median {statistics.median(per_kb):.3f}  span {(max(it['t_end'] for it in items)-t0)/1e3:.2f} us")
     for s in slots:
         ex.unregister(s)
