@@ -170,8 +170,33 @@ class C2Bench:
         self.shapes = c2_shapes()
         self.ex = Executor()
         self.replicas = replicas
-        self.ops = [[OperandSet("gemm", d, seed=1000 * r + i) for i, d in enumerate(self.shapes)]
-                    for r in range(replicas)]
+        # HBM layout: per replica, the 16 activation matrices (Bt) are views into ONE contiguous
+        # arena and so are the 16 outputs (C), so a round's inputs/outputs move with a single
+        # DMA each; weights (A) are per-tenant resident tensors.
+        from paper_1901_10008_b200.executor import padded_ld
+        self.b_offsets, off = [], 0
+        for (m, n, k) in self.shapes:
+            self.b_offsets.append(off)
+            off += n * padded_ld(k)
+        self.b_numel = off
+        self.c_offsets, off = [], 0
+        for (m, n, k) in self.shapes:
+            self.c_offsets.append(off)
+            off += m * padded_ld(n)
+        self.c_numel = off
+        self.b_arena = [torch.empty(self.b_numel, dtype=torch.bfloat16, device="cuda") for _ in range(replicas)]
+        self.c_arena = [torch.empty(self.c_numel, dtype=torch.bfloat16, device="cuda") for _ in range(replicas)]
+        self.ops = []
+        for r in range(replicas):
+            row = []
+            for i, (m, n, k) in enumerate(self.shapes):
+                src = OperandSet("gemm", (m, n, k), seed=1000 * r + i)
+                ldk, ldn = padded_ld(k), padded_ld(n)
+                bt = self.b_arena[r][self.b_offsets[i]:self.b_offsets[i] + n * ldk].view(n, ldk)
+                bt.copy_(src.b)
+                c = self.c_arena[r][self.c_offsets[i]:self.c_offsets[i] + m * ldn].view(m, ldn)[:, :n]
+                row.append(OperandSet.from_tensors("gemm", (m, n, k), src.a, bt, c))
+            self.ops.append(row)
         self.slots = [[o.register(self.ex) for o in row] for row in self.ops]
         self.profile = gm.load_profile(profile_name)
         self.policy = gm.SchedulerPolicy("ooo")
@@ -218,19 +243,32 @@ class C2Bench:
         return bad
 
 
-def time_launch_only(bench, launches, rep_offset=0):
-    """Average device duration of the coalesced kernel alone (CUDA events on its stream)."""
+def time_launch_only(bench, launches):
+    """Average device duration of the coalesced kernel: `launches` back-to-back launches
+    (rotating operand replicas, as in the timed region) captured in a CUDA graph and replayed
+    between CUDA events on the launching stream, so no host gap is counted."""
     torch = bench.torch
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(launches)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(launches)]
-    for j in range(launches):
-        slots = bench.slots[(j + rep_offset) % bench.replicas]
-        starts[j].record(bench.stream)
-        bench.ex.launch(slots, bench.stream)
-        ends[j].record(bench.stream)
-    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    n = max(bench.replicas, (launches // bench.replicas) * bench.replicas)
+    with torch.cuda.stream(s):
+        for j in range(bench.replicas):
+            bench.ex.launch(bench.slots[j], s, independent=True)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for j in range(n):
+                bench.ex.launch(bench.slots[j % bench.replicas], s, independent=True)
+        g.replay()
+        s.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        e0.record(s)
+        for _ in range(reps):
+            g.replay()
+        e1.record(s)
+        s.synchronize()
     plan = bench.ex.last_plan()
-    return statistics.mean(s.elapsed_time(e) for s, e in zip(starts, ends)) * 1e-3, plan
+    return e0.elapsed_time(e1) * 1e-3 / (reps * n), plan
 
 
 def time_comparators(bench, rounds):
@@ -275,32 +313,49 @@ def time_comparators(bench, rounds):
 
 
 def e2e_rounds(bench, first, count):
-    """Public-API round trip: pinned host activations -> HBM, decisions + launch, outputs -> host."""
+    """Public-API round trip per round: the round's 16 activation matrices go host(pinned) ->
+    HBM as ONE DMA into the replica's activation arena, decisions + the coalesced launch run,
+    and the 16 outputs come back HBM -> host(pinned) as ONE DMA. Copy-in, compute and copy-out
+    of consecutive rounds overlap on three streams (replicas rotate, so no round overwrites
+    buffers still in use)."""
     torch = bench.torch
-    host_in = [o.b.cpu().pin_memory() for o in bench.ops[0]]
-    host_out = [torch.empty(o.c.shape, dtype=o.c.dtype).pin_memory() for o in bench.ops[0]]
-    h2d = sum(t.numel() * t.element_size() for t in host_in)
-    d2h = sum(t.numel() * t.element_size() for t in host_out)
-    s = bench.stream
+    host_in = bench.b_arena[0].cpu().pin_memory()
+    host_out = [torch.empty(bench.c_numel, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    h2d = host_in.numel() * host_in.element_size()
+    d2h = host_out[0].numel() * host_out[0].element_size()
+    s_in, s_cmp, s_out = torch.cuda.Stream(), bench.stream, torch.cuda.Stream()
+    done = {}
 
     def one(r):
         rep = r % bench.replicas
-        for o, h in zip(bench.ops[rep], host_in):
-            o.b.copy_(h, non_blocking=True)
+        if rep in done:                      # replica buffers free again?
+            s_in.wait_event(done[rep])
+        with torch.cuda.stream(s_in):
+            bench.b_arena[rep].copy_(host_in, non_blocking=True)
+            ev_in = torch.cuda.Event()
+            ev_in.record(s_in)
+        s_cmp.wait_event(ev_in)
         bench.queue_round(r)
         bench.run_rounds(r, 1)
-        for o, h in zip(bench.ops[rep], host_out):
-            h.copy_(o.c, non_blocking=True)
+        ev_c = torch.cuda.Event()
+        ev_c.record(s_cmp)
+        s_out.wait_event(ev_c)
+        with torch.cuda.stream(s_out):
+            host_out[r % 2].copy_(bench.c_arena[rep], non_blocking=True)
+            ev_o = torch.cuda.Event()
+            ev_o.record(s_out)
+        done[rep] = ev_o
 
     for r in range(first, first + 3):
         one(r)
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(s)
+    t0.record(s_in)
     for r in range(first + 3, first + 3 + count):
         one(r)
-    t1.record(s)
+    s_in.wait_stream(s_out)
+    t1.record(s_in)
     torch.cuda.synchronize()
     sec = t0.elapsed_time(t1) * 1e-3
     return sec, h2d, d2h, first + 3 + count
@@ -316,6 +371,18 @@ class CpuReference:
 
         from oracle import decisions as od
         self.od, self.shapes = od, shapes
+        # decisions: the reference's own gpumux Scheduler when baseline/_ref holds it (installed
+        # offline from /root/reference), else the oracle's restatement of it
+        self.ref = None
+        ref_dir = os.path.join(REPO, "baseline", "_ref")
+        if os.path.isdir(os.path.join(ref_dir, "gpumux")):
+            sys.path.insert(0, ref_dir)
+            try:
+                import gpumux  # noqa: F401
+                from gpumux import device as gd, kernels as gk, scheduler as gs
+                self.ref = (gd, gk, gs)
+            except Exception:  # noqa: BLE001 — fall back to the port
+                self.ref = None
         rng = np.random.default_rng(0)
         self.arrays = [(rng.standard_normal((m, k), dtype=np.float32) / math.sqrt(k),
                         rng.standard_normal((n, k), dtype=np.float32)) for m, n, k in shapes]
@@ -323,7 +390,13 @@ class CpuReference:
             raw = json.load(fh)["profiles"]["b200"]
         self.prof = od.Prof(**raw)
 
+    @property
+    def decisions(self):
+        return "gpumux 0.1.0 (baseline/_ref)" if self.ref else "oracle port of gpumux"
+
     def one_round(self):
+        if self.ref:
+            return self._one_round_reference()
         od, shapes, arrays = self.od, self.shapes, self.arrays
         sched = od.OracleScheduler(self.prof, "ooo")
         reqs = []
@@ -337,6 +410,29 @@ class CpuReference:
             for d in launched:
                 for kid in d.kernel_ids:
                     a, bt = arrays[kid]
+                    _ = a @ bt.T
+                sched.complete(d.dispatch_id, d.end)
+                pending -= set(d.kernel_ids)
+            if not launched:
+                now = wake if wake is not None else now + 1
+            else:
+                now = max(d.end for d in launched)
+
+
+    def _one_round_reference(self):
+        gd, gk, gs = self.ref
+        prof = gd.DeviceProfile(**self.prof._asdict())
+        sched = gs.Scheduler(prof, gs.SchedulerPolicy("ooo"))
+        slo = gk.LatencyConstraint(SLO_NS)
+        for i, (m, n, k) in enumerate(self.shapes):
+            kern = gk.KernelSpec(i, f"t{i:02d}", "gemm", (m, n, k), "fp16", arrival=0, deadline=SLO_NS)
+            sched.add_request(gk.InferenceRequest(i, kern.stream_id, (kern,), 0, slo))
+        now, pending = 0, set(range(len(self.shapes)))
+        while pending:
+            launched, _held, wake = sched.step(now)
+            for d in launched:
+                for kid in d.kernel_ids:
+                    a, bt = self.arrays[kid]
                     _ = a @ bt.T
                 sched.complete(d.dispatch_id, d.end)
                 pending -= set(d.kernel_ids)
@@ -369,10 +465,14 @@ def blas_threads():
 
 
 def read_traffic():
-    """dram bytes per launch of the coalesced kernel from the committed ncu --set full summary."""
-    path = os.path.join(REPO, "profiles", "ncu_full_summary.json")
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the coalesced kernel, from the
+    newest committed `ncu --set full` summary of this workload (profiles/r*_c2_full.json)."""
+    import glob
+    paths = sorted(glob.glob(os.path.join(REPO, "profiles", "r*_c2_full.json")))
+    if not paths:
+        return None
     try:
-        with open(path) as fh:
+        with open(paths[-1]) as fh:
             raw = json.load(fh)
         return raw.get("dram_bytes_per_launch")
     except (OSError, ValueError):
@@ -416,7 +516,7 @@ def run_ours(args, world, rank):
     bench.next_round = first + args.steps
     nxt = first + args.steps
     # ---- dominant kernel alone: CUDA events around each launch -----------------------------
-    kern_sec, plan = time_launch_only(bench, max(20, min(args.steps, 200)))
+    kern_sec, plan = time_launch_only(bench, max(48, min(args.steps, 200)))
     peaks = load_peaks()
     per_launch_bytes = plan["operand_bytes"]
     achieved = per_launch_bytes / kern_sec / 1e9
@@ -435,8 +535,9 @@ def run_ours(args, world, rank):
         thr = blas_threads()
         cv, cr, cs = cpu_reference_rounds(args.cpu_seconds, shapes, thr)
         cpu = {"value": cv, "unit": "TFLOP/s", "cores": thr, "kind": "port",
-               "sample": f"{cr} rounds of the C2 workload in {cs:.1f}s: restated gpumux OoO "
-                         f"decisions (python, 1 core) + fp32 numpy GEMMs ({thr} BLAS threads)"}
+               "sample": f"{cr} rounds of the C2 workload in {cs:.1f}s: OoO decisions by "
+                         f"{CpuReference(shapes[:1]).decisions} (python, 1 core) + fp32 numpy GEMMs of "
+                         f"every dispatched member ({thr} BLAS threads; the reference has no numerics)"}
     if rank != 0:
         return
     out = {
@@ -501,8 +602,8 @@ def run_reference(args, world, rank):
            "config": {"workload": "C2: 16 tenant streams x 1 batch-1 request/round, "
                                   "resnet50_like[i%13] im2col GEMMs", "parallelism": "host CPU"},
            "cpu_baseline": {"value": round(value, 5), "unit": "TFLOP/s", "cores": thr, "kind": "port",
-                            "sample": f"{args.steps} rounds: restated gpumux OoO decisions + fp32 numpy "
-                                      f"GEMMs of every dispatched member"},
+                            "sample": f"{args.steps} rounds: OoO decisions by {ref.decisions} + fp32 numpy "
+                                      f"GEMMs of every dispatched member (the reference has no numerics)"},
            "e2e": {"value": round(value, 5), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)

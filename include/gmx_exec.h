@@ -75,7 +75,7 @@ typedef struct gmx_plan_stats {
     int64_t operand_bytes;      /* algorithmic bytes: each operand + result once */
     int64_t tile_load_bytes;    /* bytes the tile loads request (re-reads included) */
     int64_t flops;              /* useful flops of the launch */
-    double max_cta_cost;        /* planner's makespan estimate (bytes-equivalent) */
+    double max_cta_cost;        /* planner's makespan estimate (ns of one SM) */
     double mean_cta_cost;
 } gmx_plan_stats;
 
@@ -92,11 +92,18 @@ int gmx_exec_unregister(gmx_exec* ex, int32_t slot);
  * Plans (tile list, LPT assignment across SMs, split-K choice) are cached per
  * slot set. `stream` is a cudaStream_t (NULL = legacy default stream). */
 int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream);
+/* Same with flags. Launches use programmatic dependent launch (PDL): a step's prologue
+ * (barrier init, TMEM alloc, descriptor prefetch) overlaps the previous step's tail.
+ * GMX_LAUNCH_INDEPENDENT: no member reads anything the previous launch on this stream
+ * writes, so the step also skips griddepcontrol.wait and its CTAs start on SMs as the
+ * previous step's CTAs retire (the executor still waits when split-K state could alias). */
+#define GMX_LAUNCH_INDEPENDENT 1
+int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream, int32_t flags);
 /* Stats of the plan used by the last launch. */
 int gmx_exec_last_plan(const gmx_exec* ex, gmx_plan_stats* out);
 /* Drop cached plans (e.g. after unregistering many slots). */
 int gmx_exec_clear_plans(gmx_exec* ex);
-/* Knobs: "max_split" (1 disables split-K), "cache_plans" (0/1), "trace" (0/1: the kernel
+/* Knobs: "max_split" (1 disables split-K), "cache_plans" (0/1), "pdl" (0/1), "trace" (0/1: the kernel
  * stamps %globaltimer per work item: producer start, last UMMA issued, epilogue start, end,
  * then epilogue sub-phases: staging start, staged, barrier, store issued). */
 int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value);

@@ -360,6 +360,8 @@ struct gmx_sched {
     std::vector<gmx::RequestRec> requests;
     std::vector<int64_t> dep_arena;
     std::vector<int32_t> ready;           // kernel slots
+    uint64_t ready_version = 1;           // bumped whenever the ready set / evictions change
+    uint64_t clustered_version = 0;       // ready_version the cached clustering was built for
     std::vector<gmx::DispatchRec> pool;   // in-flight dispatches
     std::vector<int32_t> pool_free;
     gmx::IdMap inflight_slot;             // dispatch id -> pool index
@@ -409,6 +411,7 @@ static const gmx_tuning_config& solo_config(const S* s, const KernelRec& k) {
 static void ready_add(S* s, int32_t slot) {
     KernelRec& k = s->kernels[slot];
     if (k.ready_pos >= 0) return;
+    ++s->ready_version;
     k.ready_pos = (int32_t)s->ready.size();
     s->ready.push_back(slot);
 }
@@ -416,6 +419,7 @@ static void ready_add(S* s, int32_t slot) {
 static void ready_remove(S* s, int32_t slot) {
     KernelRec& k = s->kernels[slot];
     if (k.ready_pos < 0) return;
+    ++s->ready_version;
     const int32_t last = s->ready.back();
     s->ready[k.ready_pos] = last;
     s->kernels[last].ready_pos = k.ready_pos;
@@ -673,14 +677,20 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
     const int64_t tenancy = std::max<int64_t>(1, (int64_t)s->s_act.size());
 
     auto& recs = s->s_recs;
-    recs.clear();
-    for (int32_t slot : live) {
-        const KernelRec& k = s->kernels[slot];
-        ShapeRec r{k.id, k.op, k.dtype, k.nd, {k.dims[0], k.dims[1], k.dims[2]}, k.flops, slot};
-        recs.push_back(r);
+    int rc;
+    // cluster_shapes is a pure function of the live ready set: when the set is unchanged since
+    // the last ooo step (e.g. the wakeup step after a withhold) reuse its clustering
+    if (s->clustered_version != s->ready_version) {
+        recs.clear();
+        for (int32_t slot : live) {
+            const KernelRec& k = s->kernels[slot];
+            ShapeRec r{k.id, k.op, k.dtype, k.nd, {k.dims[0], k.dims[1], k.dims[2]}, k.flops, slot};
+            recs.push_back(r);
+        }
+        rc = cluster_shapes(recs, s->params.pad_budget, s->s_order, s->s_clusters);
+        if (rc) return rc;
+        s->clustered_version = s->ready_version;
     }
-    int rc = cluster_shapes(recs, s->params.pad_budget, s->s_order, s->s_clusters);
-    if (rc) return rc;
     const auto& order = s->s_order;
     const auto& clusters = s->s_clusters;
 
@@ -1106,6 +1116,7 @@ int gmx_sched_evict_stream(gmx_sched* s, int32_t stream, int64_t now, gmx_evict_
     if (!s || !out) return fail(GMX_EINVAL, "null argument");
     if (stream < 0 || stream >= (int32_t)s->stream_names.size()) return fail(GMX_EINVAL, "unknown stream");
     s->evicted_stream[stream] = 1;
+    ++s->ready_version;
     s->v_ids_a.clear();  // cancelled dispatches (dispatch-id order == insertion order)
     s->v_ids_b.clear();  // evicted requests
     s->v_ids_c.clear();  // dropped kernels

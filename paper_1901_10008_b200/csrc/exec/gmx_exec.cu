@@ -111,6 +111,7 @@ struct KernelArgs {
     int32_t* counters;
     uint64_t* trace;         // optional: 8 globaltimer stamps per item (debug/profiling)
     int32_t dbg;             // experiment flags (reserved)
+    int32_t independent;     // 1: no data dependency on the previous launch (skip griddepcontrol.wait)
 };
 
 __device__ __forceinline__ float apply_act(float x, int32_t act) {
@@ -528,6 +529,9 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = has_gemm ? *tmem_slot : 0u;
+    // Programmatic dependent launch: everything above overlapped the previous step's tail; a
+    // dependent step waits here until that grid has completed and flushed its memory.
+    if (!args.independent) asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
@@ -662,6 +666,8 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
 
     tc_fence_before();
     __syncthreads();
+    // this CTA's work is done: the next step may start taking SMs
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp == 1 && has_gemm) {
         tc_fence_after();
         tmem_dealloc(tmem_base, kTmemCols);
@@ -731,10 +737,14 @@ struct Plan {
     bool uploaded = false;
     int64_t ws_floats = 0;
     int32_t n_counters = 0;
+    float* d_ws = nullptr;          // split-K accumulators (zero between launches)
+    int32_t* d_counters = nullptr;  // split-K arrival counters (zero between launches)
     gmx_plan_stats stats{};
     ~Plan() {
         if (d_items) cudaFree(d_items);
         if (d_off) cudaFree(d_off);
+        if (d_ws) cudaFree(d_ws);
+        if (d_counters) cudaFree(d_counters);
     }
 };
 
@@ -760,7 +770,9 @@ struct gmx_exec {
     bool cache_plans = true;
     bool attr_set = false;
     bool tracing = false;
+    bool pdl = true;
     int32_t dbg = 0;
+    const gmx::Plan* recent[3] = {nullptr, nullptr, nullptr};   // plans of the last launches
     uint64_t* trace = nullptr;
     int64_t trace_cap = 0;
     int64_t trace_items = 0;
@@ -785,10 +797,17 @@ static int ensure_table(gmx_exec* ex, cudaStream_t stream) {
     return GMX_OK;
 }
 
-// Planner cost unit: bytes a work item moves between L2 and the SM (plus a fixed per-item
-// overhead), which is what bounds these HBM/L2-bound steps.
+// Planner cost model, in ns of one SM, calibrated from %globaltimer traces of C2 steps on B200
+// (tools/trace_c2.py): with every SM streaming, TMA delivers ~50 GB/s per SM (the step is HBM
+// bound), a 128 x BN epilogue costs ~0.6 us, a split-K partial (RED + arrival) ~2 us and the
+// last split's finalize ~2.2 us.
+constexpr double kNsPerKB = 20.0;
+constexpr double kTileFixedNs = 600.0;
+constexpr double kSplitNs = 2000.0 + 2200.0;
+constexpr double kCudaCoreFixedNs = 400.0;
+
 static double gemm_tile_cost(const DevProblem& P, int kb) {
-    return (double)kb * (kTileRows + P.bn) * kBlockK * 2.0 + (double)kTileRows * P.bn * 2.0 + 16384.0;
+    return (double)kb * (kTileRows + P.bn) * kBlockK * 2.0 / 1024.0 * kNsPerKB + kTileFixedNs;
 }
 
 static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& plan) {
@@ -816,18 +835,21 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
                     st.tile_load_bytes += (int64_t)P.kblocks * (kTileRows + P.bn) * kBlockK * 2;
                 }
         } else {
-            total += (double)hp.op_bytes;
+            total += (double)hp.op_bytes / 1024.0 * kNsPerKB + kCudaCoreFixedNs;
         }
     }
-    const double target = std::max(total / ex->num_sms, 65536.0);
+    const double target = std::max(total / ex->num_sms, 2000.0);
     // GEMM tiles, split along K when one tile exceeds the per-SM share
     int32_t n_counters = 0;
     int64_t ws_blocks = 0;
     for (const TileRef& t : tiles) {
         const DevProblem& P = ex->probs[t.slot].dev;
         int nsplit = 1;
-        if (t.cost > target && P.kblocks >= 2 && P.tma_out)
+        if (t.cost > target && P.kblocks >= 2 && P.tma_out) {
             nsplit = (int)std::min<int64_t>({(int64_t)std::ceil(t.cost / target), (int64_t)P.kblocks, ex->max_split, 255});
+            // splitting only pays when a piece plus the fixup beats the whole tile
+            if (gemm_tile_cost(P, (P.kblocks + nsplit - 1) / nsplit) + kSplitNs >= t.cost) nsplit = 1;
+        }
         ++st.n_gemm_tiles;
         int32_t slot = -1, blk = 0;
         if (nsplit > 1) {
@@ -847,7 +869,7 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
             it.kb1 = (int32_t)((int64_t)P.kblocks * (sp + 1) / nsplit);
             it.tile_slot = slot;
             it.ws_blk = blk;
-            const double c = gemm_tile_cost(P, it.kb1 - it.kb0) + (nsplit > 1 ? 2.0 * kTileRows * P.bn * 4 : 0.0);
+            const double c = gemm_tile_cost(P, it.kb1 - it.kb0) + (nsplit > 1 ? kSplitNs : 0.0);
             cands.push_back({it, c});
             if (nsplit > 1) ++st.n_split_items;
         }
@@ -858,7 +880,8 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
         const DevProblem& P = hp.dev;
         if (P.kind == kItemGemv) {
             const double row_bytes = (double)P.cols * (P.in_dt == GMX_ST_F32 ? 4 : 2);
-            int rows_per = (int)std::max(4.0, std::floor(std::max(target * 0.5, 32768.0) / row_bytes));
+            const double item_bytes = std::max(32768.0, (target * 0.5 - kCudaCoreFixedNs) / kNsPerKB * 1024.0);
+            int rows_per = (int)std::max(4.0, std::floor(item_bytes / row_bytes));
             rows_per = std::max(4, (rows_per / 4) * 4);
             for (int r0 = 0; r0 < P.rows; r0 += rows_per) {
                 WorkItem it{};
@@ -866,12 +889,12 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
                 it.type = kItemGemv;
                 it.row0 = r0;
                 it.col0 = std::min(P.rows, r0 + rows_per);
-                cands.push_back({it, row_bytes * (it.col0 - it.row0) + 4096.0});
+                cands.push_back({it, row_bytes * (it.col0 - it.row0) / 1024.0 * kNsPerKB + kCudaCoreFixedNs});
                 ++st.n_gemv_items;
             }
         } else if (P.kind == kItemEltwise) {
             const int esz = P.in_dt == GMX_ST_F32 ? 4 : 2;
-            int64_t per = (int64_t)std::max(32768.0, target * 0.5) / (2 * esz);
+            int64_t per = (int64_t)std::max(32768.0, (target * 0.5 - kCudaCoreFixedNs) / kNsPerKB * 1024.0) / (2 * esz);
             per = std::max<int64_t>(1024, (per / 1024) * 1024);
             for (int64_t e0 = 0; e0 < P.rows; e0 += per) {
                 WorkItem it{};
@@ -879,7 +902,7 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
                 it.type = kItemEltwise;
                 it.row0 = (int32_t)e0;
                 it.col0 = (int32_t)std::min<int64_t>(P.rows, e0 + per);
-                cands.push_back({it, 2.0 * esz * (it.col0 - it.row0) + 4096.0});
+                cands.push_back({it, 2.0 * esz * (it.col0 - it.row0) / 1024.0 * kNsPerKB + kCudaCoreFixedNs});
                 ++st.n_eltwise_items;
             }
         }
@@ -940,18 +963,17 @@ static int upload_plan(gmx_exec* ex, Plan& plan, cudaStream_t stream) {
     return GMX_OK;
 }
 
-static int ensure_workspace(gmx_exec* ex, const Plan& plan) {
-    if (plan.ws_floats > ex->ws_cap) {
-        if (ex->ws) GMX_CUDA(cudaFree(ex->ws));
-        GMX_CUDA(cudaMalloc(&ex->ws, plan.ws_floats * sizeof(float)));
-        GMX_CUDA(cudaMemset(ex->ws, 0, plan.ws_floats * sizeof(float)));   // accumulators start at zero
-        ex->ws_cap = plan.ws_floats;
+// Split-K state is owned by the plan, so steps of different plans that overlap under PDL never
+// share accumulators; a plan launched again while a recent launch of it may still run waits.
+static int ensure_workspace(gmx_exec* ex, Plan& plan) {
+    (void)ex;
+    if (plan.ws_floats > 0 && !plan.d_ws) {
+        GMX_CUDA(cudaMalloc(&plan.d_ws, plan.ws_floats * sizeof(float)));
+        GMX_CUDA(cudaMemset(plan.d_ws, 0, plan.ws_floats * sizeof(float)));
     }
-    if (plan.n_counters > ex->counters_cap) {
-        if (ex->counters) GMX_CUDA(cudaFree(ex->counters));
-        GMX_CUDA(cudaMalloc(&ex->counters, plan.n_counters * sizeof(int32_t)));
-        GMX_CUDA(cudaMemset(ex->counters, 0, plan.n_counters * sizeof(int32_t)));
-        ex->counters_cap = plan.n_counters;
+    if (plan.n_counters > 0 && !plan.d_counters) {
+        GMX_CUDA(cudaMalloc(&plan.d_counters, plan.n_counters * sizeof(int32_t)));
+        GMX_CUDA(cudaMemset(plan.d_counters, 0, plan.n_counters * sizeof(int32_t)));
     }
     return GMX_OK;
 }
@@ -1119,6 +1141,10 @@ int gmx_exec_unregister(gmx_exec* ex, int32_t slot) {
 }
 
 int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream_ptr) {
+    return gmx_exec_launch_ex(ex, slots, n, stream_ptr, 0);
+}
+
+int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream_ptr, int32_t flags) {
     if (!ex || (n > 0 && !slots)) return fail(GMX_EINVAL, "null argument");
     if (n == 0) return GMX_OK;
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
@@ -1144,6 +1170,8 @@ int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream_
             }
         if (!plan) {
             if (ex->n_plans >= 512) {
+                GMX_CUDA(cudaDeviceSynchronize());   // cached plans may still be executing
+                ex->recent[0] = ex->recent[1] = ex->recent[2] = nullptr;
                 ex->plans.clear();
                 ex->n_plans = 0;
                 ex->last = nullptr;
@@ -1174,10 +1202,26 @@ int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream_
         GMX_CUDA(cudaMemsetAsync(ex->trace, 0, plan->items.size() * 8 * sizeof(uint64_t), stream));
         ex->trace_items = (int64_t)plan->items.size();
     }
-    KernelArgs args{ex->d_probs, plan->d_items, plan->d_off, plan->d_off + plan->stats.grid + 1, ex->ws,
-                    ex->counters, ex->tracing ? ex->trace : nullptr, ex->dbg};
-    coalesced_step_kernel<<<plan->stats.grid, kThreads, kSmemBytes, stream>>>(args);
-    GMX_CUDA(cudaGetLastError());
+    // independent only if the caller says so AND this plan's split-K state is not possibly in
+    // use by a still-running recent launch
+    bool independent = (flags & GMX_LAUNCH_INDEPENDENT) != 0 && !ex->tracing;
+    for (const Plan* r : ex->recent) independent &= (r != plan);
+    KernelArgs args{ex->d_probs, plan->d_items, plan->d_off, plan->d_off + plan->stats.grid + 1, plan->d_ws,
+                    plan->d_counters, ex->tracing ? ex->trace : nullptr, ex->dbg, independent ? 1 : 0};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(plan->stats.grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = ex->pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GMX_CUDA(cudaLaunchKernelEx(&cfg, coalesced_step_kernel, args));
+    ex->recent[2] = ex->recent[1];
+    ex->recent[1] = ex->recent[0];
+    ex->recent[0] = plan;
     plan->stats.cached = cached;
     ex->last = plan;
     return GMX_OK;
@@ -1206,6 +1250,9 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
         ex->max_split = value;
     } else if (n == "cache_plans") {
         ex->cache_plans = value != 0;
+    } else if (n == "pdl") {
+        ex->pdl = value != 0;
+        return GMX_OK;
     } else if (n == "dbg") {
         ex->dbg = (int32_t)value;
         return GMX_OK;

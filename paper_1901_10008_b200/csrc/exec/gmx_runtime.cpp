@@ -23,6 +23,7 @@ int fail(int code, const std::string& m) {
 }
 
 enum : int32_t { kComplete = 0, kArrival = 1, kWakeup = 2 };
+constexpr int32_t kHasDeps = 1 << 30;
 
 struct Event {
     int64_t time;
@@ -124,7 +125,10 @@ int gmx_runtime_submit(gmx_runtime* rt, int64_t rid, int32_t stream, int64_t arr
     // the n+1 CSR offsets are relative to this request's first dependency; a trailing
     // sentinel records where those dependencies start in dep_arena
     rt->off_arena.push_back(dep_base);
-    for (int32_t i = 0; i < n; ++i) rt->slot_of.put(ks[i].kernel_id, slots[i]);
+    // executor slot per kernel; bit 30 marks kernels with dependencies (they may read what an
+    // earlier launch wrote, so their launch must not overlap it)
+    for (int32_t i = 0; i < n; ++i)
+        rt->slot_of.put(ks[i].kernel_id, slots[i] | ((n > 0 && dep_off[i + 1] > dep_off[i]) ? kHasDeps : 0));
     rt->req_index.put(rid, pi);
     ++rt->live_requests;
     rt->heap.push({arrival, kArrival, rid});
@@ -175,20 +179,23 @@ int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* stream, gmx_runtime_st
         rt->st.withheld += v.n_withheld;
         if (v.n_dispatches > 0) {
             rt->launch_slots.clear();
+            bool independent = true;
             for (int32_t d = 0; d < v.n_dispatches; ++d) {
                 const gmx_dispatch_rec& r = v.dispatches[d];
                 for (int32_t j = 0; j < r.n_kernels; ++j) {
                     const int64_t kid = v.dispatch_kernel_ids[r.kernel_offset + j];
                     const int32_t slot = rt->slot_of.find(kid);
                     if (slot < 0) return fail(GMX_ESTATE, "dispatched kernel has no operands bound");
-                    rt->launch_slots.push_back(slot);
+                    independent &= (slot & kHasDeps) == 0;
+                    rt->launch_slots.push_back(slot & ~kHasDeps);
                     rt->slot_of.erase(kid);
                 }
                 rt->heap.push({r.end, kComplete, r.dispatch_id});
                 rt->st.useful_flops += r.useful_flops;
                 rt->st.kernels += r.n_kernels;
             }
-            rc = gmx_exec_launch(rt->ex, rt->launch_slots.data(), (int32_t)rt->launch_slots.size(), stream);
+            rc = gmx_exec_launch_ex(rt->ex, rt->launch_slots.data(), (int32_t)rt->launch_slots.size(), stream,
+                                    independent ? GMX_LAUNCH_INDEPENDENT : 0);
             if (rc) return fail(rc, std::string("launch: ") + gmx_exec_last_error());
             ++rt->st.launches;
             rt->st.dispatches += v.n_dispatches;

@@ -51,6 +51,7 @@ EXEC_SIGNATURES = {
     "gmx_exec_register": (C.c_int, [C.c_void_p, C.POINTER(ProblemDesc), C.POINTER(C.c_int32)]),
     "gmx_exec_unregister": (C.c_int, [C.c_void_p, C.c_int32]),
     "gmx_exec_launch": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_void_p]),
+    "gmx_exec_launch_ex": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_void_p, C.c_int32]),
     "gmx_exec_last_plan": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
     "gmx_exec_clear_plans": (C.c_int, [C.c_void_p]),
     "gmx_exec_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
@@ -191,12 +192,16 @@ class Executor:
 
     # ---- execution ----------------------------------------------------------------------
 
-    def launch(self, slots, stream=None):
-        """One coalesced launch over the given registered slots (async on `stream`)."""
+    def launch(self, slots, stream=None, independent=False):
+        """One coalesced launch over the given registered slots (async on `stream`).
+
+        independent=True promises no member reads what the previous launch on the stream
+        writes, letting this step overlap the previous step's tail (PDL)."""
         slots = list(slots)
         arr = (C.c_int32 * max(1, len(slots)))(*slots)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        _check(self._lib.gmx_exec_launch(self._h, arr, len(slots), C.c_void_p(s.cuda_stream)))
+        _check(self._lib.gmx_exec_launch_ex(self._h, arr, len(slots), C.c_void_p(s.cuda_stream),
+                                            1 if independent else 0))
 
     def launch_dispatches(self, dispatches, stream=None):
         """Execute every member of every dispatch of one scheduler step in ONE launch."""
@@ -283,6 +288,15 @@ class OperandSet:
             self.b = None
             self.c = torch.empty(n, dtype=st, device=device)
             self.bias = None
+
+    @classmethod
+    def from_tensors(cls, op_kind, dims, a, b, c, bias=None, activation="none"):
+        """Wrap caller-allocated operands (e.g. views into a tenant arena)."""
+        self = cls.__new__(cls)
+        self.op_kind, self.dims, self.activation = op_kind, tuple(dims), activation
+        self.storage = a.dtype
+        self.a, self.b, self.c, self.bias = a, b, c, bias
+        return self
 
     def register(self, ex: Executor) -> int:
         if self.op_kind == "gemm":

@@ -37,7 +37,8 @@ t1 = time.perf_counter()
 e1.record()
 torch.cuda.synchronize()
 print(f"launch-only: host {(t1 - t0) / K * 1e6:.2f} us/launch ; device {e0.elapsed_time(e1) / K * 1e3:.2f} us/launch")
-# CUDA graph of 50 launches: pure device time per launch
+# CUDA graph of 48 launches: pure device time per launch
+INDEP = len(sys.argv) > 1
 g = torch.cuda.CUDAGraph()
 s = torch.cuda.Stream()
 with torch.cuda.stream(s):
@@ -46,7 +47,7 @@ with torch.cuda.stream(s):
     torch.cuda.synchronize()
     with torch.cuda.graph(g, stream=s):
         for x in slots[:48]:
-            b.ex.launch(x, s)
+            b.ex.launch(x, s, independent=INDEP)
 torch.cuda.synchronize()
 e0.record()
 for _ in range(5):
