@@ -26,47 +26,47 @@ class IdMap {
 
     int32_t find(int64_t key) const {
         size_t i = mix64((uint64_t)key) & mask_;
-        while (used_[i]) {
-            if (keys_[i] == key) return vals_[i];
+        while (slots_[i].used) {
+            if (slots_[i].key == key) return slots_[i].val;
             i = (i + 1) & mask_;
         }
         return -1;
     }
 
-    void put(int64_t key, int32_t val) {
+    // Insert or overwrite; returns the previous value or -1 (one probe sequence).
+    int32_t put(int64_t key, int32_t val) {
         if ((size_ + 1) * 4 > (mask_ + 1) * 3) rehash((mask_ + 1) * 2);
         size_t i = mix64((uint64_t)key) & mask_;
-        while (used_[i]) {
-            if (keys_[i] == key) {
-                vals_[i] = val;
-                return;
+        while (slots_[i].used) {
+            if (slots_[i].key == key) {
+                const int32_t old = slots_[i].val;
+                slots_[i].val = val;
+                return old;
             }
             i = (i + 1) & mask_;
         }
-        used_[i] = 1;
-        keys_[i] = key;
-        vals_[i] = val;
+        slots_[i] = Slot{key, val, 1};
         ++size_;
+        return -1;
     }
 
     bool erase(int64_t key) {
         size_t i = mix64((uint64_t)key) & mask_;
-        while (used_[i]) {
-            if (keys_[i] == key) {
+        while (slots_[i].used) {
+            if (slots_[i].key == key) {
                 // backward-shift deletion keeps probe chains intact without tombstones
                 size_t j = i;
                 for (;;) {
                     j = (j + 1) & mask_;
-                    if (!used_[j]) break;
-                    const size_t home = mix64((uint64_t)keys_[j]) & mask_;
+                    if (!slots_[j].used) break;
+                    const size_t home = mix64((uint64_t)slots_[j].key) & mask_;
                     const bool movable = (i <= j) ? (home <= i || home > j) : (home <= i && home > j);
                     if (movable) {
-                        keys_[i] = keys_[j];
-                        vals_[i] = vals_[j];
+                        slots_[i] = slots_[j];
                         i = j;
                     }
                 }
-                used_[i] = 0;
+                slots_[i].used = 0;
                 --size_;
                 return true;
             }
@@ -78,22 +78,22 @@ class IdMap {
     size_t size() const { return size_; }
 
    private:
+    struct Slot {           // key, value and occupancy in one 16-byte entry (one cache line probe)
+        int64_t key;
+        int32_t val;
+        int32_t used;
+    };
+
     void rehash(size_t cap) {
-        std::vector<int64_t> k = std::move(keys_);
-        std::vector<int32_t> v = std::move(vals_);
-        std::vector<uint8_t> u = std::move(used_);
-        keys_.assign(cap, 0);
-        vals_.assign(cap, 0);
-        used_.assign(cap, 0);
+        std::vector<Slot> old = std::move(slots_);
+        slots_.assign(cap, Slot{0, 0, 0});
         mask_ = cap - 1;
         size_ = 0;
-        for (size_t i = 0; i < u.size(); ++i)
-            if (u[i]) put(k[i], v[i]);
+        for (const Slot& e : old)
+            if (e.used) put(e.key, e.val);
     }
 
-    std::vector<int64_t> keys_;
-    std::vector<int32_t> vals_;
-    std::vector<uint8_t> used_;
+    std::vector<Slot> slots_;
     size_t mask_ = 0, size_ = 0;
 };
 

@@ -254,16 +254,64 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
     const int32_t n = (int32_t)recs.size();
     static thread_local std::vector<int32_t> idx;   // scratch: no allocation after warm-up
     static thread_local std::vector<char> taken;
-    idx.resize(n);
-    for (int32_t i = 0; i < n; ++i) idx[i] = i;
-    std::sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) {
-        const ShapeRec &a = recs[x], &b = recs[y];
+    static thread_local std::vector<int32_t> gid, gfirst, gcount, gorder, slot_of_group;
+    static thread_local std::vector<int32_t> htab;
+    // Sort order (op, dtype, dims descending, id) built in two levels: kernels are grouped by
+    // identical shape (exact-key hash table), only the distinct shapes are comparison-sorted,
+    // and ids are sorted within each shape group — same order as one global sort, far fewer
+    // comparisons when many tenants share a shape.
+    gid.resize(n);
+    gfirst.clear();
+    gcount.clear();
+    size_t cap = 16;
+    while (cap < (size_t)n * 2) cap <<= 1;
+    htab.assign(cap, -1);
+    auto same = [&](const ShapeRec& a, const ShapeRec& b) {
+        return a.op == b.op && a.dtype == b.dtype && a.dims[0] == b.dims[0] && a.dims[1] == b.dims[1] &&
+               a.dims[2] == b.dims[2];
+    };
+    for (int32_t i = 0; i < n; ++i) {
+        const ShapeRec& r = recs[i];
+        uint64_t h = mix64(((uint64_t)r.op << 8 | (uint64_t)r.dtype) ^ mix64((uint64_t)r.dims[0]) ^
+                           mix64((uint64_t)r.dims[1] * 31) ^ mix64((uint64_t)r.dims[2] * 131));
+        size_t q = h & (cap - 1);
+        while (htab[q] >= 0 && !same(recs[gfirst[htab[q]]], r)) q = (q + 1) & (cap - 1);
+        if (htab[q] < 0) {
+            htab[q] = (int32_t)gfirst.size();
+            gfirst.push_back(i);
+            gcount.push_back(0);
+        }
+        gid[i] = htab[q];
+        ++gcount[htab[q]];
+    }
+    const int32_t ng = (int32_t)gfirst.size();
+    gorder.resize(ng);
+    for (int32_t g = 0; g < ng; ++g) gorder[g] = g;
+    std::sort(gorder.begin(), gorder.end(), [&](int32_t x, int32_t y) {
+        const ShapeRec &a = recs[gfirst[x]], &b = recs[gfirst[y]];
         if (a.op != b.op) return a.op < b.op;
         if (a.dtype != b.dtype) return a.dtype < b.dtype;
         for (int i = 0; i < a.nd; ++i)  // dims descending
             if (a.dims[i] != b.dims[i]) return a.dims[i] > b.dims[i];
-        return a.id < b.id;
+        return false;
     });
+    slot_of_group.resize(ng);   // start offset of each group in idx
+    int32_t pos = 0;
+    for (int32_t g : gorder) {
+        slot_of_group[g] = pos;
+        pos += gcount[g];
+    }
+    idx.resize(n);
+    {
+        static thread_local std::vector<int32_t> fill;
+        fill.assign(slot_of_group.begin(), slot_of_group.end());
+        for (int32_t i = 0; i < n; ++i) idx[fill[gid[i]]++] = i;
+    }
+    for (int32_t g = 0; g < ng; ++g) {
+        if (gcount[g] > 1)
+            std::sort(idx.begin() + slot_of_group[g], idx.begin() + slot_of_group[g] + gcount[g],
+                      [&](int32_t x, int32_t y) { return recs[x].id < recs[y].id; });
+    }
     taken.assign(n, 0);
     order.clear();
     clusters.clear();
@@ -463,6 +511,22 @@ static void active_streams(S* s, std::vector<int32_t>& out) {
     for (size_t i = 0; i < seen.size(); ++i)
         if (seen[i] && !s->evicted_stream[i]) out.push_back((int32_t)i);
     std::sort(out.begin(), out.end(), [s](int32_t a, int32_t b) { return s->stream_less(a, b); });
+}
+
+// len(_active_streams()) without sorting (all the ooo step needs)
+static int64_t count_active_streams(S* s) {
+    std::vector<char>& seen = s->s_seen;
+    seen.assign(s->stream_names.size(), 0);
+    int64_t n = 0;
+    auto mark = [&](int32_t st) {
+        if (!seen[st] && !s->evicted_stream[st]) ++n;
+        seen[st] = 1;
+    };
+    for (int32_t slot : s->ready) mark(s->kernels[slot].stream);
+    for (const DispatchRec& d : s->pool)
+        if (d.live)
+            for (int32_t st : d.streams) mark(st);
+    return n;
 }
 
 // scheduler.py:288-292
@@ -673,8 +737,7 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
     std::vector<int32_t>& live = s->s_live;
     live_ready(s, live);
     if (live.empty()) return GMX_OK;
-    active_streams(s, s->s_act);
-    const int64_t tenancy = std::max<int64_t>(1, (int64_t)s->s_act.size());
+    const int64_t tenancy = std::max<int64_t>(1, count_active_streams(s));
 
     auto& recs = s->s_recs;
     int rc;
@@ -1034,12 +1097,11 @@ int gmx_sched_add_request(gmx_sched* s, int64_t request_id, int32_t stream, int6
         }
         const int32_t slot = (int32_t)s->kernels.size();
         // a re-used kernel id shadows the old record (dict assignment semantics)
-        const int32_t old = s->kernel_slot.find(k.id);
+        const int32_t old = s->kernel_slot.put(k.id, slot);
         if (old >= 0) {
             ready_remove(s, old);
             s->kernels[old].blocked = false;
         }
-        s->kernel_slot.put(k.id, slot);
         k.blocked = k.dep_n > 0;
         s->kernels.push_back(k);
         if (out_pred) out_pred[i] = k.predicted;

@@ -728,23 +728,28 @@ struct HostProblem {
     int64_t flops = 0;
 };
 
+// Device buffers of a plan come from the stream-ordered allocator (cudaMallocAsync) and are
+// released with cudaFreeAsync on the stream of the plan's last launch, so evicting a plan
+// whose launch is still queued is safe and no eviction ever synchronizes the device.
 struct Plan {
     std::vector<int32_t> key;       // sorted slot list this plan was built for
     std::vector<WorkItem> items;
-    std::vector<int32_t> cta_off;
+    std::vector<int32_t> cta_off;   // cta_off[grid + 1] then cta_flags[grid]
+    void* d_buf = nullptr;          // items + offsets/flags
+    void* d_state = nullptr;        // split-K accumulators + counters (zeroed, re-armed by the kernel)
     WorkItem* d_items = nullptr;
     int32_t* d_off = nullptr;
+    float* d_ws = nullptr;
+    int32_t* d_counters = nullptr;
     bool uploaded = false;
     int64_t ws_floats = 0;
     int32_t n_counters = 0;
-    float* d_ws = nullptr;          // split-K accumulators (zero between launches)
-    int32_t* d_counters = nullptr;  // split-K arrival counters (zero between launches)
+    cudaStream_t stream = nullptr;  // stream of the last launch
+    uint64_t last_use = 0;          // LRU clock
     gmx_plan_stats stats{};
     ~Plan() {
-        if (d_items) cudaFree(d_items);
-        if (d_off) cudaFree(d_off);
-        if (d_ws) cudaFree(d_ws);
-        if (d_counters) cudaFree(d_counters);
+        if (d_buf) cudaFreeAsync(d_buf, stream);
+        if (d_state) cudaFreeAsync(d_state, stream);
     }
 };
 
@@ -759,6 +764,8 @@ struct gmx_exec {
     bool table_dirty = false;
     std::unordered_map<uint64_t, std::vector<std::unique_ptr<gmx::Plan>>> plans;   // hash(slots) -> plans
     size_t n_plans = 0;
+    size_t plan_capacity = 4096;
+    uint64_t clock = 0;
     std::vector<int32_t> key_scratch;
     gmx::Plan* last = nullptr;
     std::unique_ptr<gmx::Plan> uncached;
@@ -948,34 +955,57 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
     return GMX_OK;
 }
 
+// Upload the plan (one stream-ordered allocation + one copy) and allocate its split-K state.
+// Split-K state is owned by the plan, so steps of different plans that overlap under PDL never
+// share accumulators; a plan launched again while a recent launch of it may still run waits.
 static int upload_plan(gmx_exec* ex, Plan& plan, cudaStream_t stream) {
-    if (plan.uploaded) return GMX_OK;
-    const size_t ni = std::max<size_t>(1, plan.items.size());
-    GMX_CUDA(cudaMalloc(&plan.d_items, ni * sizeof(WorkItem)));
-    GMX_CUDA(cudaMalloc(&plan.d_off, plan.cta_off.size() * sizeof(int32_t)));
-    if (!plan.items.empty())
-        GMX_CUDA(cudaMemcpyAsync(plan.d_items, plan.items.data(), plan.items.size() * sizeof(WorkItem),
-                                 cudaMemcpyHostToDevice, stream));
-    GMX_CUDA(cudaMemcpyAsync(plan.d_off, plan.cta_off.data(), plan.cta_off.size() * sizeof(int32_t),
-                             cudaMemcpyHostToDevice, stream));
-    plan.uploaded = true;
     (void)ex;
+    if (plan.uploaded) return GMX_OK;
+    const size_t items_bytes = std::max<size_t>(1, plan.items.size()) * sizeof(WorkItem);
+    const size_t off_bytes = plan.cta_off.size() * sizeof(int32_t);
+    std::vector<uint8_t> staging(items_bytes + off_bytes);
+    if (!plan.items.empty()) std::memcpy(staging.data(), plan.items.data(), plan.items.size() * sizeof(WorkItem));
+    std::memcpy(staging.data() + items_bytes, plan.cta_off.data(), off_bytes);
+    GMX_CUDA(cudaMallocAsync(&plan.d_buf, staging.size(), stream));
+    GMX_CUDA(cudaMemcpyAsync(plan.d_buf, staging.data(), staging.size(), cudaMemcpyHostToDevice, stream));
+    plan.d_items = reinterpret_cast<WorkItem*>(plan.d_buf);
+    plan.d_off = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(plan.d_buf) + items_bytes);
+    if (plan.ws_floats > 0 || plan.n_counters > 0) {
+        const size_t ws_bytes = (size_t)plan.ws_floats * sizeof(float);
+        const size_t state = ws_bytes + (size_t)std::max(1, plan.n_counters) * sizeof(int32_t);
+        GMX_CUDA(cudaMallocAsync(&plan.d_state, state, stream));
+        GMX_CUDA(cudaMemsetAsync(plan.d_state, 0, state, stream));
+        plan.d_ws = reinterpret_cast<float*>(plan.d_state);
+        plan.d_counters = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(plan.d_state) + ws_bytes);
+    }
+    plan.stream = stream;
+    plan.uploaded = true;
     return GMX_OK;
 }
 
-// Split-K state is owned by the plan, so steps of different plans that overlap under PDL never
-// share accumulators; a plan launched again while a recent launch of it may still run waits.
-static int ensure_workspace(gmx_exec* ex, Plan& plan) {
-    (void)ex;
-    if (plan.ws_floats > 0 && !plan.d_ws) {
-        GMX_CUDA(cudaMalloc(&plan.d_ws, plan.ws_floats * sizeof(float)));
-        GMX_CUDA(cudaMemset(plan.d_ws, 0, plan.ws_floats * sizeof(float)));
+// Least-recently-used eighth of the cache goes when it is full (stream-ordered frees).
+static void evict_plans(gmx_exec* ex) {
+    std::vector<std::pair<uint64_t, Plan*>> all;
+    for (auto& kv : ex->plans)
+        for (auto& p : kv.second) all.push_back({p->last_use, p.get()});
+    std::sort(all.begin(), all.end());
+    const size_t drop = std::max<size_t>(1, all.size() / 8);
+    std::unordered_map<const Plan*, bool> doomed;
+    for (size_t i = 0; i < drop && i < all.size(); ++i) doomed[all[i].second] = true;
+    for (auto& kv : ex->plans) {
+        auto& bucket = kv.second;
+        for (size_t i = 0; i < bucket.size();) {
+            if (doomed.count(bucket[i].get())) {
+                if (ex->last == bucket[i].get()) ex->last = nullptr;
+                for (auto& r : ex->recent)
+                    if (r == bucket[i].get()) r = nullptr;
+                bucket.erase(bucket.begin() + i);
+                --ex->n_plans;
+            } else {
+                ++i;
+            }
+        }
     }
-    if (plan.n_counters > 0 && !plan.d_counters) {
-        GMX_CUDA(cudaMalloc(&plan.d_counters, plan.n_counters * sizeof(int32_t)));
-        GMX_CUDA(cudaMemset(plan.d_counters, 0, plan.n_counters * sizeof(int32_t)));
-    }
-    return GMX_OK;
 }
 
 }  // namespace gmx
@@ -993,6 +1023,13 @@ int gmx_exec_create(int32_t device, gmx_exec** out) {
     GMX_CUDA(cudaGetDeviceProperties(&prop, device));
     if (prop.major != 10) return fail(GMX_ECUDA, std::string("executor targets sm_100a; device is ") + prop.name);
     GMX_CUDA(cudaSetDevice(device));
+    {   // keep freed plan memory in the stream-ordered pool (plans churn on dynamic workloads)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t threshold = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+        }
+    }
     auto* ex = new gmx_exec();
     ex->device = device;
     ex->num_sms = prop.multiProcessorCount;
@@ -1169,13 +1206,7 @@ int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stre
                 break;
             }
         if (!plan) {
-            if (ex->n_plans >= 512) {
-                GMX_CUDA(cudaDeviceSynchronize());   // cached plans may still be executing
-                ex->recent[0] = ex->recent[1] = ex->recent[2] = nullptr;
-                ex->plans.clear();
-                ex->n_plans = 0;
-                ex->last = nullptr;
-            }
+            if (ex->n_plans >= ex->plan_capacity) evict_plans(ex);
             auto p = std::make_unique<Plan>();
             if ((rc = build_plan(ex, key, *p))) return rc;
             p->key = key;
@@ -1184,11 +1215,13 @@ int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stre
             ++ex->n_plans;
         }
     } else {
-        ex->uncached = std::make_unique<Plan>();
+        ex->uncached = std::make_unique<Plan>();   // the previous one is freed stream-ordered
         if ((rc = build_plan(ex, key, *ex->uncached))) return rc;
         plan = ex->uncached.get();
     }
-    if ((rc = upload_plan(ex, *plan, stream)) || (rc = ensure_workspace(ex, *plan))) return rc;
+    if ((rc = upload_plan(ex, *plan, stream))) return rc;
+    plan->stream = stream;
+    plan->last_use = ++ex->clock;
     if (!ex->attr_set) {
         GMX_CUDA(cudaFuncSetAttribute(coalesced_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
         ex->attr_set = true;
@@ -1250,6 +1283,9 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
         ex->max_split = value;
     } else if (n == "cache_plans") {
         ex->cache_plans = value != 0;
+    } else if (n == "plan_capacity") {
+        if (value < 1) return fail(GMX_EINVAL, "plan_capacity must be >= 1");
+        ex->plan_capacity = (size_t)value;
     } else if (n == "pdl") {
         ex->pdl = value != 0;
         return GMX_OK;

@@ -35,15 +35,27 @@ int main(int argc, char** argv) {
         }
         double q1 = now_us();
         int64_t t = base; int left = tenants;
-        int64_t pend[4096]; int npend = 0;
+        /* lockstep virtual time: dispatches complete at their model end; SM-gated clusters
+           dispatch after completions free SMs (engine.py:320-367 order) */
+        int64_t pend_id[4096], pend_end[4096]; int npend = 0; int64_t wake = -1;
         while (left > 0) {
             gmx_step_view v;
             gmx_sched_step(s, t, &v);
-            for (int d = 0; d < v.n_dispatches; ++d) { pend[npend++] = v.dispatches[d].dispatch_id; left -= v.dispatches[d].n_kernels; dispatched++; }
-            if (v.has_wakeup) t = v.wakeup; else t += 1;
+            for (int d = 0; d < v.n_dispatches; ++d) {
+                pend_id[npend] = v.dispatches[d].dispatch_id; pend_end[npend++] = v.dispatches[d].end;
+                left -= v.dispatches[d].n_kernels; dispatched++;
+            }
+            wake = v.has_wakeup ? v.wakeup : -1;
+            if (left <= 0) break;
+            int64_t next = wake;
+            for (int d = 0; d < npend; ++d) if (pend_id[d] >= 0 && (next < 0 || pend_end[d] < next)) next = pend_end[d];
+            if (next < 0) next = t + 1;
+            t = next;
+            for (int d = 0; d < npend; ++d) if (pend_id[d] >= 0 && pend_end[d] <= t) {
+                gmx_complete_view cv; gmx_sched_complete(s, pend_id[d], t, &cv); pend_id[d] = -1; }
         }
         double q2 = now_us();
-        for (int d = 0; d < npend; ++d) { gmx_complete_view cv; gmx_sched_complete(s, pend[d], t + 100000, &cv); }
+        for (int d = 0; d < npend; ++d) if (pend_id[d] >= 0) { gmx_complete_view cv; gmx_sched_complete(s, pend_id[d], t + 100000, &cv); }
         double q3 = now_us();
         if (r >= 100) { ta += q1 - q0; ts += q2 - q1; tc += q3 - q2; }
     }
