@@ -101,6 +101,9 @@ int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream)
 int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream, int32_t flags);
 /* Stats of the plan used by the last launch. */
 int gmx_exec_last_plan(const gmx_exec* ex, gmx_plan_stats* out);
+/* A caller-owned stream is about to be destroyed: wait for its work and stop using it for
+ * the stream-ordered release of plan memory. */
+int gmx_exec_stream_retired(gmx_exec* ex, void* stream);
 /* Drop cached plans (e.g. after unregistering many slots). */
 int gmx_exec_clear_plans(gmx_exec* ex);
 /* Knobs: "max_split" (1 disables split-K), "cache_plans" (0/1), "pdl" (0/1), "trace" (0/1: the kernel

@@ -29,6 +29,11 @@ extern "C" {
 #endif
 
 #define GMX_RT_LOCKSTEP 0
+/* Wall-clock mode: `now` is the host clock in ns since the runtime's
+ * origin; arrivals fire when their time has passed; a launch's dispatches complete when the
+ * CUDA event recorded after the launch has completed (observed time); wakeups fire on the
+ * clock. Every step is logged (time, events applied, decisions) for replay parity. */
+#define GMX_RT_REALTIME 1
 
 typedef struct gmx_runtime gmx_runtime;
 
@@ -59,6 +64,29 @@ int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* cuda_stream, gmx_runti
 int gmx_runtime_drain_completions(gmx_runtime* rt, int64_t* request_ids, int64_t* times,
                                   int32_t capacity, int32_t* n_out);
 const char* gmx_runtime_last_error(void);
+/* Realtime mode: set the clock origin (ns since the process steady-clock epoch); the first
+ * run() sets it if unset. gmx_runtime_clock_ns returns the current runtime time. */
+int gmx_runtime_set_origin(gmx_runtime* rt, int64_t steady_ns);
+/* Realtime mode: launch round-robin over `n` runtime-owned CUDA streams so independent small
+ * steps co-run on idle SMs (dependencies are already enforced by the scheduler: a kernel is
+ * dispatched only after its predecessors' launches completed). n = 1 uses the run() stream. */
+int gmx_runtime_set_streams(gmx_runtime* rt, int32_t n);
+int64_t gmx_runtime_clock_ns(const gmx_runtime* rt);
+/* Replay log (realtime mode). Records, in order:
+ *   kind 0: complete(dispatch_id=a) at time t      kind 1: add_request(request_id=a) at t
+ *   kind 2: step(t) -> dispatch a with kernels [off, off+n) of kernel_ids
+ *   kind 3: step(t) withheld group [off, off+n)       kind 4: step(t) wakeup a (-1: none)
+ *   kind 5: step(t) (marks the step boundary; precedes its kind 2/3/4 records)
+ * Copies up to `capacity` records; *n_out = total available. */
+typedef struct gmx_replay_rec {
+    int32_t kind;
+    int32_t n;
+    int64_t t;
+    int64_t a;
+    int64_t off;
+} gmx_replay_rec;
+int gmx_runtime_replay_log(const gmx_runtime* rt, gmx_replay_rec* recs, int64_t capacity, int64_t* n_out,
+                           int64_t* kernel_ids, int64_t kid_capacity, int64_t* n_kids);
 
 #ifdef __cplusplus
 }

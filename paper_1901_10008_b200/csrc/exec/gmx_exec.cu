@@ -745,11 +745,13 @@ struct Plan {
     int64_t ws_floats = 0;
     int32_t n_counters = 0;
     cudaStream_t stream = nullptr;  // stream of the last launch
+    cudaEvent_t done_ev = nullptr;  // multi-stream mode: recorded after each launch of the plan
     uint64_t last_use = 0;          // LRU clock
     gmx_plan_stats stats{};
     ~Plan() {
         if (d_buf) cudaFreeAsync(d_buf, stream);
         if (d_state) cudaFreeAsync(d_state, stream);
+        if (done_ev) cudaEventDestroy(done_ev);
     }
 };
 
@@ -778,6 +780,7 @@ struct gmx_exec {
     bool attr_set = false;
     bool tracing = false;
     bool pdl = true;
+    bool multi_stream = false;   // launches may come from several streams (realtime runtime)
     int32_t dbg = 0;
     const gmx::Plan* recent[3] = {nullptr, nullptr, nullptr};   // plans of the last launches
     uint64_t* trace = nullptr;
@@ -1219,6 +1222,9 @@ int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stre
         if ((rc = build_plan(ex, key, *ex->uncached))) return rc;
         plan = ex->uncached.get();
     }
+    // multi-stream: a plan's split-K state and outputs must not be used by two launches at once
+    if (ex->multi_stream && plan->done_ev && plan->stream != stream)
+        GMX_CUDA(cudaStreamWaitEvent(stream, plan->done_ev, 0));
     if ((rc = upload_plan(ex, *plan, stream))) return rc;
     plan->stream = stream;
     plan->last_use = ++ex->clock;
@@ -1252,6 +1258,10 @@ int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stre
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     GMX_CUDA(cudaLaunchKernelEx(&cfg, coalesced_step_kernel, args));
+    if (ex->multi_stream) {
+        if (!plan->done_ev) GMX_CUDA(cudaEventCreateWithFlags(&plan->done_ev, cudaEventDisableTiming));
+        GMX_CUDA(cudaEventRecord(plan->done_ev, stream));
+    }
     ex->recent[2] = ex->recent[1];
     ex->recent[1] = ex->recent[0];
     ex->recent[0] = plan;
@@ -1286,6 +1296,9 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
     } else if (n == "plan_capacity") {
         if (value < 1) return fail(GMX_EINVAL, "plan_capacity must be >= 1");
         ex->plan_capacity = (size_t)value;
+    } else if (n == "multi_stream") {
+        ex->multi_stream = value != 0;
+        return GMX_OK;
     } else if (n == "pdl") {
         ex->pdl = value != 0;
         return GMX_OK;
@@ -1305,6 +1318,17 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
 }
 
 const char* gmx_exec_last_error(void) { return g_err.c_str(); }
+
+int gmx_exec_stream_retired(gmx_exec* ex, void* stream_ptr) {
+    if (!ex) return fail(GMX_EINVAL, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream_ptr);
+    GMX_CUDA(cudaStreamSynchronize(st));
+    for (auto& kv : ex->plans)
+        for (auto& p : kv.second)
+            if (p->stream == st) p->stream = nullptr;   // later frees go to the legacy stream
+    if (ex->uncached && ex->uncached->stream == st) ex->uncached->stream = nullptr;
+    return GMX_OK;
+}
 
 int gmx_exec_read_trace(const gmx_exec* ex, uint64_t* stamps, int32_t* items, int32_t* cta_off,
                         int32_t capacity, int32_t* n_items, int32_t* grid) {

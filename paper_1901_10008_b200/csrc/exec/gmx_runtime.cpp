@@ -8,7 +8,11 @@
 #include "../../../include/gmx_runtime.h"
 #include "../core/flatmap.hpp"
 
+#include <cuda_runtime.h>
+
 #include <algorithm>
+#include <chrono>
+#include <deque>
 #include <queue>
 #include <string>
 #include <vector>
@@ -65,7 +69,30 @@ struct gmx_runtime {
     int64_t wake_seq = 0;
     int64_t live_requests = 0;
     gmx_runtime_stats st{};
+    // realtime mode
+    bool origin_set = false;
+    int64_t origin_ns = 0;
+    struct InFlight {
+        cudaEvent_t ev;
+        std::vector<int64_t> dispatch_ids;
+    };
+    std::deque<InFlight> inflight;
+    std::vector<cudaStream_t> streams;   // realtime: launches round-robin over these
+    size_t next_stream = 0;
+    std::vector<cudaEvent_t> event_pool;
+    std::vector<gmx_replay_rec> log;
+    std::vector<int64_t> log_kids;
 };
+
+static int64_t steady_ns() {
+    return (int64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+static void log_rec(gmx_runtime* rt, int32_t kind, int64_t t, int64_t a, int32_t n = 0, int64_t off = 0) {
+    rt->log.push_back(gmx_replay_rec{kind, n, t, a, off});
+}
 
 static void release_request(gmx_runtime* rt, int64_t rid) {
     const int32_t pi = rt->req_index.find(rid);
@@ -85,7 +112,7 @@ const char* gmx_runtime_last_error(void) { return g_err.c_str(); }
 
 int gmx_runtime_create(gmx_sched* sched, gmx_exec* ex, int32_t mode, gmx_runtime** out) {
     if (!sched || !ex || !out) return fail(GMX_EINVAL, "null argument");
-    if (mode != GMX_RT_LOCKSTEP) return fail(GMX_EINVAL, "unsupported runtime mode");
+    if (mode != GMX_RT_LOCKSTEP && mode != GMX_RT_REALTIME) return fail(GMX_EINVAL, "unsupported runtime mode");
     auto* rt = new gmx_runtime();
     rt->sched = sched;
     rt->ex = ex;
@@ -94,7 +121,44 @@ int gmx_runtime_create(gmx_sched* sched, gmx_exec* ex, int32_t mode, gmx_runtime
     return GMX_OK;
 }
 
-void gmx_runtime_destroy(gmx_runtime* rt) { delete rt; }
+void gmx_runtime_destroy(gmx_runtime* rt) {
+    if (!rt) return;
+    for (cudaStream_t st : rt->streams) {
+        gmx_exec_stream_retired(rt->ex, st);
+        cudaStreamDestroy(st);
+    }
+    for (auto& f : rt->inflight) cudaEventDestroy(f.ev);
+    for (cudaEvent_t e : rt->event_pool) cudaEventDestroy(e);
+    delete rt;
+}
+
+int gmx_runtime_set_streams(gmx_runtime* rt, int32_t n) {
+    if (!rt || n < 1 || n > 64) return fail(GMX_EINVAL, "stream count must be in [1, 64]");
+    for (cudaStream_t st : rt->streams) {
+        gmx_exec_stream_retired(rt->ex, st);
+        cudaStreamDestroy(st);
+    }
+    rt->streams.clear();
+    for (int32_t i = 0; i < n; ++i) {
+        cudaStream_t st;
+        if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+            return fail(GMX_ECUDA, "cudaStreamCreate failed");
+        rt->streams.push_back(st);
+    }
+    return gmx_exec_set_option(rt->ex, "multi_stream", n > 1 ? 1 : 0);
+}
+
+int gmx_runtime_set_origin(gmx_runtime* rt, int64_t ns) {
+    if (!rt) return fail(GMX_EINVAL, "null argument");
+    rt->origin_ns = ns;
+    rt->origin_set = true;
+    return GMX_OK;
+}
+
+int64_t gmx_runtime_clock_ns(const gmx_runtime* rt) {
+    if (!rt || !rt->origin_set) return 0;
+    return steady_ns() - rt->origin_ns;
+}
 
 int gmx_runtime_submit(gmx_runtime* rt, int64_t rid, int32_t stream, int64_t arrival, int64_t deadline,
                        const gmx_kernel_desc* ks, int32_t n, const int64_t* dep_ids, const int32_t* dep_off,
@@ -135,8 +199,168 @@ int gmx_runtime_submit(gmx_runtime* rt, int64_t rid, int32_t stream, int64_t arr
     return GMX_OK;
 }
 
+static int on_finished(gmx_runtime* rt, const gmx_complete_view& cv, int64_t now) {
+    for (int32_t i = 0; i < cv.n_finished; ++i) {
+        const int64_t r = cv.finished_request_ids[i];
+        rt->done_ids.push_back(r);
+        rt->done_times.push_back(now);
+        ++rt->st.completed_requests;
+        const int32_t pi = rt->req_index.find(r);
+        if (pi >= 0) {
+            if (now > rt->pool[pi].deadline) ++rt->st.slo_misses;
+            release_request(rt, r);
+        }
+    }
+    return GMX_OK;
+}
+
+static int on_arrival(gmx_runtime* rt, int64_t rid) {
+    const int32_t pi = rt->req_index.find(rid);
+    if (pi < 0 || rt->pool[pi].arrived) return GMX_OK;
+    Pending& p = rt->pool[pi];
+    p.arrived = true;
+    rt->pred.resize((size_t)std::max(1, p.n));
+    const int32_t dep_base = rt->off_arena[p.d_off + p.n + 1];
+    int32_t accepted = 0;
+    int rc = gmx_sched_add_request(rt->sched, rid, p.stream, p.arrival, rt->k_arena.data() + p.k_off, p.n,
+                                   rt->dep_arena.data() + dep_base, rt->off_arena.data() + p.d_off,
+                                   rt->pred.data(), &accepted);
+    if (rc) return fail(rc, std::string("add_request: ") + gmx_last_error());
+    if (!accepted) release_request(rt, rid);
+    return GMX_OK;
+}
+
+// One scheduler step at `now` and ONE launch for all of its dispatches. In realtime mode the
+// dispatch ids of the launch are returned in `ids` (completion is observed, not scheduled).
+static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool realtime, std::vector<int64_t>* ids) {
+    gmx_step_view v;
+    int rc = gmx_sched_step(rt->sched, now, &v);
+    if (rc) return fail(rc, std::string("step: ") + gmx_last_error());
+    ++rt->st.steps;
+    rt->st.withheld += v.n_withheld;
+    if (realtime) {
+        log_rec(rt, 5, now, 0);
+        for (int32_t d = 0; d < v.n_dispatches; ++d) {
+            const gmx_dispatch_rec& r = v.dispatches[d];
+            log_rec(rt, 2, now, r.dispatch_id, r.n_kernels, (int64_t)rt->log_kids.size());
+            rt->log_kids.insert(rt->log_kids.end(), v.dispatch_kernel_ids + r.kernel_offset,
+                                v.dispatch_kernel_ids + r.kernel_offset + r.n_kernels);
+        }
+        for (int32_t w = 0; w < v.n_withheld; ++w) {
+            const int32_t a = v.withheld_offsets[w], b = v.withheld_offsets[w + 1];
+            log_rec(rt, 3, now, 0, b - a, (int64_t)rt->log_kids.size());
+            rt->log_kids.insert(rt->log_kids.end(), v.withheld_kernel_ids + a, v.withheld_kernel_ids + b);
+        }
+        log_rec(rt, 4, now, v.has_wakeup ? v.wakeup : -1);
+    }
+    if (v.n_dispatches > 0) {
+        rt->launch_slots.clear();
+        bool independent = true;
+        for (int32_t d = 0; d < v.n_dispatches; ++d) {
+            const gmx_dispatch_rec& r = v.dispatches[d];
+            for (int32_t j = 0; j < r.n_kernels; ++j) {
+                const int64_t kid = v.dispatch_kernel_ids[r.kernel_offset + j];
+                const int32_t slot = rt->slot_of.find(kid);
+                if (slot < 0) return fail(GMX_ESTATE, "dispatched kernel has no operands bound");
+                independent &= (slot & kHasDeps) == 0;
+                rt->launch_slots.push_back(slot & ~kHasDeps);
+                rt->slot_of.erase(kid);
+            }
+            if (realtime)
+                ids->push_back(r.dispatch_id);
+            else
+                rt->heap.push({r.end, kComplete, r.dispatch_id});
+            rt->st.useful_flops += r.useful_flops;
+            rt->st.kernels += r.n_kernels;
+        }
+        rc = gmx_exec_launch_ex(rt->ex, rt->launch_slots.data(), (int32_t)rt->launch_slots.size(), stream,
+                                independent ? GMX_LAUNCH_INDEPENDENT : 0);
+        if (rc) return fail(rc, std::string("launch: ") + gmx_exec_last_error());
+        ++rt->st.launches;
+        rt->st.dispatches += v.n_dispatches;
+    }
+    if (v.has_wakeup) rt->heap.push({v.wakeup, kWakeup, ++rt->wake_seq});
+    rt->st.now = now;
+    return GMX_OK;
+}
+
+// Wall-clock loop: returns when every submitted request has finished and nothing is in flight,
+// or when the clock passes `until`.
+static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtime_stats* out) {
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    if (!rt->origin_set) {
+        rt->origin_ns = steady_ns();
+        rt->origin_set = true;
+    }
+    std::vector<int64_t> ids;
+    for (;;) {
+        const int64_t now = steady_ns() - rt->origin_ns;
+        bool any = false;
+        // COMPLETE: any launch whose event has completed (launches on several streams may
+        // retire out of order; each launch's dispatches complete in dispatch-id order)
+        for (size_t i = 0; i < rt->inflight.size();) {
+            const cudaError_t q = cudaEventQuery(rt->inflight[i].ev);
+            if (q == cudaErrorNotReady) {
+                ++i;
+                continue;
+            }
+            if (q != cudaSuccess) return fail(GMX_ECUDA, std::string("launch failed: ") + cudaGetErrorString(q));
+            for (int64_t did : rt->inflight[i].dispatch_ids) {
+                gmx_complete_view cv;
+                int rc = gmx_sched_complete(rt->sched, did, now, &cv);
+                if (rc) return fail(rc, std::string("complete: ") + gmx_last_error());
+                log_rec(rt, 0, now, did);
+                on_finished(rt, cv, now);
+            }
+            rt->event_pool.push_back(rt->inflight[i].ev);
+            rt->inflight.erase(rt->inflight.begin() + (long)i);
+            any = true;
+        }
+        // ARRIVAL then WAKEUP events that are due (heap order: time, kind, id)
+        while (!rt->heap.empty() && rt->heap.top().time <= now) {
+            const Event e = rt->heap.top();
+            rt->heap.pop();
+            if (e.kind == kArrival) {
+                log_rec(rt, 1, now, e.id);
+                int rc = on_arrival(rt, e.id);
+                if (rc) return rc;
+            }
+            any = true;
+        }
+        if (any) {
+            ids.clear();
+            void* launch_stream = stream;
+            if (!rt->streams.empty()) {
+                cs = rt->streams[rt->next_stream];
+                launch_stream = cs;
+            }
+            int rc = step_and_launch(rt, now, launch_stream, true, &ids);
+            if (rc) return rc;
+            if (!ids.empty()) {
+                cudaEvent_t ev;
+                if (!rt->event_pool.empty()) {
+                    ev = rt->event_pool.back();
+                    rt->event_pool.pop_back();
+                } else if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+                    return fail(GMX_ECUDA, "cudaEventCreate failed");
+                }
+                if (cudaEventRecord(ev, cs) != cudaSuccess) return fail(GMX_ECUDA, "cudaEventRecord failed");
+                rt->inflight.push_back({ev, ids});
+                if (!rt->streams.empty()) rt->next_stream = (rt->next_stream + 1) % rt->streams.size();
+            }
+            continue;
+        }
+        if (rt->heap.empty() && rt->inflight.empty()) break;   // drained
+        if (now > until) break;
+    }
+    rt->st.now = steady_ns() - rt->origin_ns;
+    if (out) *out = rt->st;
+    return GMX_OK;
+}
+
 int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* stream, gmx_runtime_stats* out) {
     if (!rt) return fail(GMX_EINVAL, "null argument");
+    if (rt->mode == GMX_RT_REALTIME) return run_realtime(rt, until, stream, out);
     while (!rt->heap.empty() && rt->heap.top().time <= until) {
         const int64_t now = rt->heap.top().time;
         while (!rt->heap.empty() && rt->heap.top().time == now) {
@@ -146,64 +370,26 @@ int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* stream, gmx_runtime_st
                 gmx_complete_view cv;
                 int rc = gmx_sched_complete(rt->sched, e.id, now, &cv);
                 if (rc) return fail(rc, std::string("complete: ") + gmx_last_error());
-                for (int32_t i = 0; i < cv.n_finished; ++i) {
-                    const int64_t r = cv.finished_request_ids[i];
-                    rt->done_ids.push_back(r);
-                    rt->done_times.push_back(now);
-                    ++rt->st.completed_requests;
-                    const int32_t pi = rt->req_index.find(r);
-                    if (pi >= 0) {
-                        if (now > rt->pool[pi].deadline) ++rt->st.slo_misses;
-                        release_request(rt, r);
-                    }
-                }
+                on_finished(rt, cv, now);
             } else if (e.kind == kArrival) {
-                const int32_t pi = rt->req_index.find(e.id);
-                if (pi < 0 || rt->pool[pi].arrived) continue;
-                Pending& p = rt->pool[pi];
-                p.arrived = true;
-                rt->pred.resize((size_t)std::max(1, p.n));
-                const int32_t dep_base = rt->off_arena[p.d_off + p.n + 1];
-                int32_t accepted = 0;
-                int rc = gmx_sched_add_request(rt->sched, e.id, p.stream, p.arrival, rt->k_arena.data() + p.k_off,
-                                               p.n, rt->dep_arena.data() + dep_base, rt->off_arena.data() + p.d_off,
-                                               rt->pred.data(), &accepted);
-                if (rc) return fail(rc, std::string("add_request: ") + gmx_last_error());
-                if (!accepted) release_request(rt, e.id);
+                int rc = on_arrival(rt, e.id);
+                if (rc) return rc;
             }
         }
-        gmx_step_view v;
-        int rc = gmx_sched_step(rt->sched, now, &v);
-        if (rc) return fail(rc, std::string("step: ") + gmx_last_error());
-        ++rt->st.steps;
-        rt->st.withheld += v.n_withheld;
-        if (v.n_dispatches > 0) {
-            rt->launch_slots.clear();
-            bool independent = true;
-            for (int32_t d = 0; d < v.n_dispatches; ++d) {
-                const gmx_dispatch_rec& r = v.dispatches[d];
-                for (int32_t j = 0; j < r.n_kernels; ++j) {
-                    const int64_t kid = v.dispatch_kernel_ids[r.kernel_offset + j];
-                    const int32_t slot = rt->slot_of.find(kid);
-                    if (slot < 0) return fail(GMX_ESTATE, "dispatched kernel has no operands bound");
-                    independent &= (slot & kHasDeps) == 0;
-                    rt->launch_slots.push_back(slot & ~kHasDeps);
-                    rt->slot_of.erase(kid);
-                }
-                rt->heap.push({r.end, kComplete, r.dispatch_id});
-                rt->st.useful_flops += r.useful_flops;
-                rt->st.kernels += r.n_kernels;
-            }
-            rc = gmx_exec_launch_ex(rt->ex, rt->launch_slots.data(), (int32_t)rt->launch_slots.size(), stream,
-                                    independent ? GMX_LAUNCH_INDEPENDENT : 0);
-            if (rc) return fail(rc, std::string("launch: ") + gmx_exec_last_error());
-            ++rt->st.launches;
-            rt->st.dispatches += v.n_dispatches;
-        }
-        if (v.has_wakeup) rt->heap.push({v.wakeup, kWakeup, ++rt->wake_seq});
-        rt->st.now = now;
+        int rc = step_and_launch(rt, now, stream, false, nullptr);
+        if (rc) return rc;
     }
     if (out) *out = rt->st;
+    return GMX_OK;
+}
+
+int gmx_runtime_replay_log(const gmx_runtime* rt, gmx_replay_rec* recs, int64_t cap, int64_t* n_out,
+                           int64_t* kids, int64_t kid_cap, int64_t* n_kids) {
+    if (!rt || !n_out || !n_kids) return fail(GMX_EINVAL, "null argument");
+    *n_out = (int64_t)rt->log.size();
+    *n_kids = (int64_t)rt->log_kids.size();
+    if (recs) std::copy(rt->log.begin(), rt->log.begin() + std::min<int64_t>(cap, *n_out), recs);
+    if (kids) std::copy(rt->log_kids.begin(), rt->log_kids.begin() + std::min<int64_t>(kid_cap, *n_kids), kids);
     return GMX_OK;
 }
 

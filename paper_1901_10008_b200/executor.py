@@ -259,7 +259,9 @@ class OperandSet:
     """
 
     def __init__(self, op_kind, dims, dtype="fp16", device="cuda", seed=0, out_dtype=None,
-                 bias=False, activation="none"):
+                 bias=False, activation="none", on_device=False):
+        if on_device:   # large synthetic workloads: generate on the GPU (no host RNG / copies)
+            return self._init_on_device(op_kind, dims, dtype, device, seed, out_dtype, activation)
         g = torch.Generator(device="cpu").manual_seed(seed)
         self.op_kind, self.dims, self.activation = op_kind, tuple(dims), activation
         st = torch.bfloat16 if dtype == "fp16" else torch.float32
@@ -288,6 +290,29 @@ class OperandSet:
             self.b = None
             self.c = torch.empty(n, dtype=st, device=device)
             self.bias = None
+
+    def _init_on_device(self, op_kind, dims, dtype, device, seed, out_dtype, activation):
+        g = torch.Generator(device=device).manual_seed(seed)
+        self.op_kind, self.dims, self.activation, self.bias = op_kind, tuple(dims), activation, None
+        st = torch.bfloat16 if dtype == "fp16" else torch.float32
+        self.storage = st
+        if op_kind == "gemm":
+            m, n, k = dims
+            ld = padded_ld(k)
+            self.a = (torch.randn(m, ld, generator=g, device=device) / k ** 0.5).to(torch.bfloat16)
+            self.b = torch.randn(n, ld, generator=g, device=device).to(torch.bfloat16)
+            odt = out_dtype or torch.bfloat16
+            self.c = torch.empty(m, padded_ld(n, odt), dtype=odt, device=device)[:, :n]
+        elif op_kind == "gemv":
+            m, n = dims
+            self.a = (torch.rand(m, n, generator=g, device=device) * 2 - 1).to(st)
+            self.b = (torch.rand(n, generator=g, device=device) * 2 - 1).to(st)
+            self.c = torch.empty(m, dtype=out_dtype or st, device=device)
+        else:
+            (n,) = dims
+            self.a = torch.randn(n, generator=g, device=device).to(st)
+            self.b = None
+            self.c = torch.empty(n, dtype=st, device=device)
 
     @classmethod
     def from_tensors(cls, op_kind, dims, a, b, c, bias=None, activation="none"):

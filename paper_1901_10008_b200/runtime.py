@@ -25,6 +25,11 @@ from .kernels import kernel_desc
 from .tuning import native_table
 
 
+class ReplayRec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int32), ("t", C.c_int64), ("a", C.c_int64),
+                ("off", C.c_int64)]
+
+
 class RuntimeStats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("now", "steps", "launches", "dispatches", "kernels",
                                          "withheld", "completed_requests", "useful_flops",
@@ -42,7 +47,14 @@ RT_SIGNATURES = {
     "gmx_runtime_drain_completions": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64),
                                                 C.POINTER(C.c_int64), C.c_int32,
                                                 C.POINTER(C.c_int32)]),
+    "gmx_runtime_set_origin": (C.c_int, [C.c_void_p, C.c_int64]),
+    "gmx_runtime_set_streams": (C.c_int, [C.c_void_p, C.c_int32]),
+    "gmx_runtime_clock_ns": (C.c_int64, [C.c_void_p]),
+    "gmx_runtime_replay_log": (C.c_int, [C.c_void_p, C.POINTER(ReplayRec), C.c_int64,
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_int64,
+                                         C.POINTER(C.c_int64)]),
 }
+MODES = {"lockstep": 0, "realtime": 1}
 
 _bound = False
 
@@ -66,7 +78,11 @@ def _check(rc):
 
 
 class Runtime:
-    def __init__(self, executor, profile, policy, tuning_table=None, jitter_state=0):
+    """mode="lockstep": the reference's virtual clock (decisions bit-identical to
+    gpumux.engine.run); mode="realtime": wall clock, completions observed from CUDA events,
+    every step logged for replay parity (`replay_log`)."""
+
+    def __init__(self, executor, profile, policy, tuning_table=None, jitter_state=0, mode="lockstep"):
         self.ex = executor
         core = _lib.core()
         p = policy.params
@@ -84,7 +100,8 @@ class Runtime:
                                          C.byref(h)))
         self._sched = h
         rt = C.c_void_p()
-        _check(_rt_lib().gmx_runtime_create(h, executor._h, 0, C.byref(rt)))
+        _check(_rt_lib().gmx_runtime_create(h, executor._h, MODES[mode], C.byref(rt)))
+        self.mode = mode
         self._rt = rt
         self._codes = {}
         self._stats = RuntimeStats()
@@ -135,6 +152,29 @@ class Runtime:
         _check(_rt_lib().gmx_runtime_run(self._rt, int(until), C.c_void_p(s.cuda_stream),
                                          C.byref(self._stats)))
         return {n: getattr(self._stats, n) for n, _ in RuntimeStats._fields_}
+
+    def set_streams(self, n: int):
+        """Realtime mode: launch over n runtime-owned CUDA streams (small steps co-run)."""
+        _check(_rt_lib().gmx_runtime_set_streams(self._rt, int(n)))
+
+    def set_origin_now(self):
+        """Realtime mode: start the runtime clock now (arrival times are relative to it)."""
+        import time
+        _check(_rt_lib().gmx_runtime_set_origin(self._rt, time.monotonic_ns()))
+
+    def clock_ns(self) -> int:
+        return _rt_lib().gmx_runtime_clock_ns(self._rt)
+
+    def replay_log(self):
+        """[(kind, t, a, kernel_ids)] — see include/gmx_runtime.h for the record kinds."""
+        lib = _rt_lib()
+        n, nk = C.c_int64(), C.c_int64()
+        _check(lib.gmx_runtime_replay_log(self._rt, None, 0, C.byref(n), None, 0, C.byref(nk)))
+        recs = (ReplayRec * max(1, n.value))()
+        kids = (C.c_int64 * max(1, nk.value))()
+        _check(lib.gmx_runtime_replay_log(self._rt, recs, n.value, C.byref(n), kids, nk.value, C.byref(nk)))
+        return [(r.kind, r.t, r.a, tuple(kids[r.off:r.off + r.n]) if r.kind in (2, 3) else ())
+                for r in recs[:n.value]]
 
     def drain_completions(self, capacity=65536):
         ids = (C.c_int64 * capacity)()

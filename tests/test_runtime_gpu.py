@@ -82,3 +82,60 @@ def test_runtime_mixed_chains_match_oracle_engine():
         for i, m in enumerate(["mixed_fp16", "tiny_chain", "resnet50_fc", "eltwise_fp32", "mixed_fp16"])]}
     stats = _run_workload(wl, lib, params={"stagger_horizon": 50_000})
     assert stats["completed_requests"] == 10
+
+
+def test_realtime_mode_replays_through_the_reference_scheduler():
+    """Wall-clock mode: arrivals at real times, completions from CUDA events. Replaying the
+    logged (time, event) sequence through the oracle scheduler (pinned to gpumux) must
+    reproduce every step's decisions: dispatch ids + members, withheld groups, wakeups."""
+    import paper_1901_10008_b200 as gm
+    from paper_1901_10008_b200.executor import Executor, OperandSet
+    from paper_1901_10008_b200.runtime import Runtime
+
+    prof_raw = load_golden("profiles.json")["b200"]
+    ex = Executor()
+    rt = Runtime(ex, gm.DeviceProfile(**prof_raw), gm.SchedulerPolicy("ooo"), mode="realtime")
+    lib = dict(load_golden("models.json"))
+    wl = {"duration_ns": 3_000_000, "streams": [
+        {"stream_id": f"r{i:02d}", "model_name": ["mixed_fp16", "conv_fp16_a", "conv_fp16_b", "tiny_chain"][i % 4],
+         "slo_ns": 10_000_000, "arrival": {"kind": "fixed", "schedule": [200_000 + 37_000 * i, 1_500_000 + 11_000 * i]}}
+        for i in range(12)]}
+    reqs = sim.materialize(wl, lib, 0)
+    for r in reqs:
+        slots = [OperandSet(k.op_kind, k.dims, dtype=k.dtype, seed=k.kernel_id).register(ex) for k in r.kernels]
+        rt.submit(gm.InferenceRequest(r.request_id, r.stream_id,
+                                      tuple(gm.KernelSpec(k.kernel_id, k.stream_id, k.op_kind, k.dims, k.dtype,
+                                                          k.deps, k.arrival, k.deadline) for k in r.kernels),
+                                      r.arrival, gm.LatencyConstraint(10_000_000)), slots)
+    rt.set_origin_now()
+    stats = rt.run(until=2_000_000_000)
+    assert stats["completed_requests"] == len(reqs)
+    log = rt.replay_log()
+    by_rid = {r.request_id: r for r in reqs}
+    osched = od.OracleScheduler(od.Prof(**prof_raw), "ooo")
+    i, steps = 0, 0
+    while i < len(log):
+        kind, t, a, kids = log[i]
+        if kind == 0:
+            osched.complete(a, t)
+        elif kind == 1:
+            osched.add_request(by_rid[a])
+        elif kind == 5:
+            launched, held, wake = osched.step(t)
+            got_d, got_h, got_w = [], [], None
+            i += 1
+            while i < len(log) and log[i][0] in (2, 3, 4):
+                k2, _t2, a2, kids2 = log[i]
+                if k2 == 2:
+                    got_d.append((a2, kids2))
+                elif k2 == 3:
+                    got_h.append(kids2)
+                else:
+                    got_w = None if a2 < 0 else a2
+                i += 1
+            assert got_d == [(d.dispatch_id, d.kernel_ids) for d in launched], t
+            assert got_h == list(held) and got_w == wake, t
+            steps += 1
+            continue
+        i += 1
+    assert steps >= 4
