@@ -51,16 +51,31 @@ namespace gmx {
 enum : int32_t { kItemGemm = 0, kItemGemv = 1, kItemEltwise = 2 };
 
 constexpr int kThreads = 192;
-constexpr int kStages = 6;
+// Two build shapes of the same kernel (selected per executor, option "ctas_per_sm"):
+//   1 CTA/SM : 6-stage ring, 32 KB output staging (one resident CTA streams alone)
+//   2 CTAs/SM: 3-stage ring each, 16 KB staging; two CTAs (of one launch, or of consecutive
+//              launches) share an SM, so one's epilogue / pipeline fill overlaps the other's loads
+template <int kCtasPerSm>
+struct SmemCfg {
+    static constexpr int stages = kCtasPerSm == 1 ? 6 : 3;
+    static constexpr int stage_out = kCtasPerSm == 1 ? 32 * 1024 : 16 * 1024;
+    static constexpr int align_pad = kCtasPerSm == 1 ? 1024 : 0;   // 2/SM: base must already be aligned
+    static constexpr int acc_bufs = kCtasPerSm == 1 ? 4 : 2;        // TMEM accumulators (128 cols each)
+    static constexpr int tmem_cols = acc_bufs * 128;                // 512 per SM either way
+    static constexpr int stage_bufs = kCtasPerSm == 1 ? 2 : 1;      // output staging ping-pong
+};
 constexpr int kTileRows = 128;             // UMMA M
 constexpr int kBlockK = 64;                // 64 bf16 = 128 B = one swizzle atom row
 constexpr int kMaxBN = 128;
 constexpr int kStageA = kTileRows * kBlockK * 2;   // 16 KB
 constexpr int kStageB = kMaxBN * kBlockK * 2;      // 16 KB
 constexpr int kStageBytes = kStageA + kStageB;
-constexpr int kTmemCols = 256;             // 2 accumulators x 128 fp32 columns
-constexpr int kStageOut = 32 * 1024;       // epilogue staging tile for TMA stores
-constexpr int kSmemBytes = kStages * kStageBytes + kStageOut + 1024 /*align*/ + 256 /*barriers*/;
+template <int kCtasPerSm>
+constexpr int smem_bytes() {
+    using C = SmemCfg<kCtasPerSm>;
+    return C::stages * kStageBytes + C::stage_out + C::align_pad + 256 /*barriers*/;
+}
+static_assert(2 * (smem_bytes<2>() + 1024) <= 233472, "two CTAs must fit one SM's shared memory");
 constexpr int kWsBlock = 4096;             // split-K workspace allocation unit (floats)
 
 struct alignas(64) DevProblem {
@@ -112,6 +127,7 @@ struct KernelArgs {
     uint64_t* trace;         // optional: 8 globaltimer stamps per item (debug/profiling)
     int32_t dbg;             // experiment flags (reserved)
     int32_t independent;     // 1: no data dependency on the previous launch (skip griddepcontrol.wait)
+    int32_t early_trigger;   // 1: let the next launch start as soon as all our CTAs are resident
 };
 
 __device__ __forceinline__ float apply_act(float x, int32_t act) {
@@ -232,8 +248,8 @@ __device__ __forceinline__ void store_tile_chunk(const EpiParams& E, int row0, i
 //   non-swap: tile rows = m (128), chunk = 32 n-columns; box {128 B of n, 128 m-rows}
 //   swap:     tile rows = n (128), chunk = 32 m-rows;    box {128 B of n, 32 m-rows}
 // Staging slots hold 128 x 32 output elements (8 KB bf16 / 16 KB fp32), SWIZZLE_128B.
-__device__ __forceinline__ int out_chunks_per_pass(const EpiParams& E) {
-    return kStageOut / (128 * 32 * (E.out_dt == GMX_ST_BF16 ? 2 : 4));
+__device__ __forceinline__ int out_chunks_per_pass(const EpiParams& E, int stage_out) {
+    return stage_out / (128 * 32 * (E.out_dt == GMX_ST_BF16 ? 2 : 4));
 }
 
 __device__ __forceinline__ void stage_out_chunk(const EpiParams& E, const float (&v)[32], int slot, int trow,
@@ -274,6 +290,27 @@ __device__ __forceinline__ void stage_out_chunk(const EpiParams& E, const float 
     }
 }
 
+// Output staging ring: `nbuf` buffers of `half` bytes used round-robin, one TMA-store bulk
+// group per pass, so a pass only waits for the store issued nbuf passes ago to have read its
+// buffer. Every epilogue thread walks the ring identically (uniform control flow).
+struct Staging {
+    uint8_t* base;
+    int half;
+    int nbuf;
+    uint32_t pass;
+    // wait (one thread) until the next buffer is free; the caller then syncs the epilogue warps
+    __device__ __forceinline__ uint8_t* next(int etid) {
+        if (etid == 0) {
+            if (nbuf == 2)
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            else
+                bulk_wait_read0();
+        }
+        return base + (nbuf == 2 ? (int)(pass & 1u) * half : 0);
+    }
+    __device__ __forceinline__ void done() { ++pass; }
+};
+
 // One thread: TMA-store the staged chunks c0..cend-1 of the tile at (row0, col0).
 __device__ __forceinline__ void issue_out_stores(const EpiParams& E, int row0, int col0, int c0, int cend,
                                                  uint8_t* stg) {
@@ -297,16 +334,17 @@ __device__ __forceinline__ void issue_out_stores(const EpiParams& E, int row0, i
 
 // Epilogue of an unsplit tile: TMEM chunks -> bias/activation -> staging -> TMA store. The
 // accumulator is released to the MMA warp right after its last tcgen05.ld.
-__device__ __forceinline__ void epilogue_staged(const EpiParams& E, int row0, int col0, uint8_t* stg, int trow,
+__device__ __forceinline__ uint32_t epilogue_staged(const EpiParams& E, int row0, int col0, Staging& S, int trow,
                                                 int etid, uint32_t taddr, uint64_t* tempty_bar,
                                                 uint64_t* tr = nullptr) {
     const int nchunks = E.bn / 32;
-    const int per_pass = out_chunks_per_pass(E);
-    const uint32_t stg_u32 = smem_u32(stg);
+    const int per_pass = out_chunks_per_pass(E, S.half);
     const int lane = lane_id();
+    uint32_t groups = 0;
     for (int c0 = 0; c0 < nchunks; c0 += per_pass) {
         const int cend = min(nchunks, c0 + per_pass);
-        if (etid == 0) bulk_wait_read0();   // staging free: previous store has read it
+        uint8_t* stg = S.next(etid);   // staging free: the store that last used it has read it
+        const uint32_t stg_u32 = smem_u32(stg);
         named_bar_sync(3, 128);
         if (tr && etid == 0 && c0 == 0) tr[4] = global_timer_ns();
         for (int c = c0; c < cend; ++c) {
@@ -328,20 +366,34 @@ __device__ __forceinline__ void epilogue_staged(const EpiParams& E, int row0, in
             issue_out_stores(E, row0, col0, c0, cend, stg);
             if (tr && c0 == 0) tr[7] = global_timer_ns();
         }
+        S.done();
+        ++groups;
     }
+    return groups;
 }
 
-// ---- split-K: fp32 reductions into an L2-resident accumulator tile ---------------------
-// Accumulator layout of a tile: [column (bn)][row (128)] fp32 — for a fixed column a warp
-// touches one 128-byte line (lanes = consecutive tile rows), so the RED/LD/ST traffic is fully
-// coalesced. Splits add their partials with fire-and-forget `red.global.add.f32`; the last
-// arrival (per-tile counter) reads the sum once, re-zeroes it and runs the output epilogue.
-__device__ __forceinline__ void red_add_f32(float* p, float v) {
-    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+// ---- split-K: partials reduced in L2, completion deferred, last arrival finalizes -----------
+// Every split of a tile adds into the same fp32 accumulator tile in an L2-resident workspace,
+// blocked [chunk (32 cols)][quad (4 cols)][row (128)][4] so that (a) one warp-wide 16-byte
+// reduction covers 512 contiguous bytes and (b) a chunk is one contiguous 16 KB block.
+//   1. reduce: TMEM -> registers -> `red.global.add.v4.f32` (no smem, no TMA-engine time, so
+//      the producer's loads are not delayed); the TMEM accumulator is released right away.
+//   2. complete (deferred until the epilogue warps finished the CTA's NEXT item, so the L2
+//      round trip overlaps useful work): every thread fences its reductions, then one acq_rel
+//      ticket on the tile counter. The split drawing the last ticket sees all the sums and
+//   3. finalizes: bulk-loads the summed chunks into smem, bias/activation, staged TMA store,
+//      and re-zeroes the workspace + counter for the next launch of the plan.
+// No split ever waits for another CTA, so no placement of items across CTAs (or concurrent
+// launches on other streams) can deadlock. fp32 add order is arrival order (within tolerance;
+// `max_split=1` is bitwise-stable).
+
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
 }
 
-__device__ __forceinline__ void split_partial_reduce(const EpiParams& E, float* acc_tile, int trow,
-                                                     uint32_t taddr, uint64_t* tempty_bar) {
+__device__ __forceinline__ void split_reduce(const EpiParams& E, float* acc_tile, int trow, uint32_t taddr,
+                                             uint64_t* tempty_bar) {
     const int nchunks = E.bn / 32;
     const int lane = lane_id();
     for (int c = 0; c < nchunks; ++c) {
@@ -352,37 +404,49 @@ __device__ __forceinline__ void split_partial_reduce(const EpiParams& E, float* 
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty_bar);
         }
-        float* col = acc_tile + (int64_t)(c * 32) * kTileRows + trow;
+        float* base = acc_tile + ((int64_t)c * 8 * kTileRows + trow) * 4;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) red_add_f32(col + j * kTileRows, v[j]);
+        for (int q = 0; q < 8; ++q)
+            red_add_v4(base + q * kTileRows * 4, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
 }
 
-__device__ __forceinline__ void split_finalize(const EpiParams& E, int row0, int col0, float* acc_tile,
-                                               uint8_t* stg, int trow, int etid) {
+// Last split: summed chunks L2 -> registers (16-byte loads, 512 contiguous bytes per warp
+// instruction, two chunks in flight) -> epilogue; re-zero the workspace for the next launch.
+__device__ __forceinline__ void ld_sum_chunk(float* acc_tile, int c, int trow, float (&v)[32]) {
+    float4* base = reinterpret_cast<float4*>(acc_tile) + (int64_t)c * 8 * kTileRows + trow;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const float4 x = __ldcg(base + q * kTileRows);
+        v[4 * q] = x.x;
+        v[4 * q + 1] = x.y;
+        v[4 * q + 2] = x.z;
+        v[4 * q + 3] = x.w;
+    }
+}
+__device__ __forceinline__ void zero_sum_chunk(float* acc_tile, int c, int trow) {
+    float4* base = reinterpret_cast<float4*>(acc_tile) + (int64_t)c * 8 * kTileRows + trow;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) st_global_cg_v4(base + q * kTileRows, make_uint4(0u, 0u, 0u, 0u));
+}
+
+__device__ __forceinline__ uint32_t split_finalize(const EpiParams& E, int row0, int col0, float* acc_tile,
+                                                  Staging& S, int trow, int etid) {
     const int nchunks = E.bn / 32;
-    const int per_pass = out_chunks_per_pass(E);
-    const uint32_t stg_u32 = smem_u32(stg);
+    const int per_pass = out_chunks_per_pass(E, S.half);
+    uint32_t groups = 0;
     for (int c0 = 0; c0 < nchunks; c0 += per_pass) {
         const int cend = min(nchunks, c0 + per_pass);
-        if (etid == 0) bulk_wait_read0();
+        uint8_t* stg = S.next(etid);   // output staging free
+        const uint32_t stg_u32 = smem_u32(stg);
         named_bar_sync(3, 128);
         for (int c = c0; c < cend; c += 2) {
-            float v0[32], v1[32];
-            float* col0p = acc_tile + (int64_t)(c * 32) * kTileRows + trow;
             const bool two = c + 1 < cend;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v0[j] = __ldcg(col0p + j * kTileRows);
-            if (two) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v1[j] = __ldcg(col0p + (32 + j) * kTileRows);
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) __stcg(col0p + j * kTileRows, 0.0f);   // re-arm
-            if (two) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) __stcg(col0p + (32 + j) * kTileRows, 0.0f);
-            }
+            float v0[32], v1[32];
+            ld_sum_chunk(acc_tile, c, trow, v0);
+            if (two) ld_sum_chunk(acc_tile, c + 1, trow, v1);
+            zero_sum_chunk(acc_tile, c, trow);
+            if (two) zero_sum_chunk(acc_tile, c + 1, trow);
             transform_chunk(v0, E, E.swap ? col0 + c * 32 : row0 + trow, E.swap);
             stage_out_chunk(E, v0, c - c0, trow, stg_u32);
             if (two) {
@@ -393,7 +457,10 @@ __device__ __forceinline__ void split_finalize(const EpiParams& E, int row0, int
         fence_async_smem();
         named_bar_sync(3, 128);
         if (etid == 0) issue_out_stores(E, row0, col0, c0, cend, stg);
+        S.done();
+        ++groups;
     }
+    return groups;
 }
 
 template <typename T>
@@ -493,16 +560,21 @@ __device__ void eltwise_range(const DevProblem* Pg, int e0, int e1, int tid, int
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const KernelArgs args) {
-    extern __shared__ uint8_t smem_raw[];
+template <int kCtasPerSm>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) coalesced_step_kernel(const KernelArgs args) {
+    using Cfg = SmemCfg<kCtasPerSm>;
+    constexpr int kStages = Cfg::stages;
+    constexpr int kStageOut = Cfg::stage_out;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    if (Cfg::align_pad == 0 && smem != smem_raw) __trap();   // SWIZZLE_128B tiles need 1024-byte alignment
     uint8_t* stg = smem + kStages * kStageBytes;                       // epilogue staging (1024-aligned)
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes + kStageOut);
+    uint64_t* full = reinterpret_cast<uint64_t*>(stg + kStageOut);
     uint64_t* empty = full + kStages;
     uint64_t* tfull = empty + kStages;
-    uint64_t* tempty = tfull + 2;
-    uint64_t* ebar = tempty + 2;                                       // epilogue bulk loads
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 1);
+    constexpr int kAcc = Cfg::acc_bufs;
+    uint64_t* tempty = tfull + kAcc;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAcc);
     int32_t* split_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5;
@@ -517,14 +589,13 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < kAcc; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 4);   // one arrival per epilogue warp
         }
-        mbar_init(ebar, 1);
         mbar_fence_init();
     }
-    if (warp == 1 && has_gemm) tmem_alloc(tmem_slot, kTmemCols);
+    if (warp == 1 && has_gemm) tmem_alloc(tmem_slot, Cfg::tmem_cols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -532,6 +603,10 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
     // Programmatic dependent launch: everything above overlapped the previous step's tail; a
     // dependent step waits here until that grid has completed and flushed its memory.
     if (!args.independent) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // Early trigger: the next step's grid may launch as soon as every CTA of this one is
+    // resident; its CTAs then take SMs as ours retire, so a step's tail overlaps the next
+    // step's start (a dependent next step still waits for our completion and flush).
+    if (args.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
@@ -576,14 +651,13 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
                     const uint64_t b_desc = smem_desc_sw128(tile + kStageA);
 #pragma unroll
                     for (int k = 0; k < kBlockK / 16; ++k)   // 16-element UMMA K steps = +32 B
-                        umma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb > it.kb0 || k > 0) ? 1u : 0u);
+                        if (!(args.dbg & 4)) umma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb > it.kb0 || k > 0) ? 1u : 0u);
                     umma_commit(&empty[stage]);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
                 umma_commit(&tfull[acc]);
                 if (args.trace) args.trace[8 * i + 1] = global_timer_ns();
-                acc ^= 1;
-                if (acc == 0) acc_phase ^= 1;
+                if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
             }
         }
     } else {
@@ -593,7 +667,36 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
         const int trow = lgrp * 32 + lane;       // tile row owned by this thread
         const int etid = ew * 32 + lane;         // 0..127
         int acc = 0;
-        uint32_t acc_phase = 0, ephase = 0;
+        uint32_t acc_phase = 0;
+        Staging S{stg, kStageOut / Cfg::stage_bufs, Cfg::stage_bufs, 0u};
+        uint32_t groups = 0;                     // bulk groups committed by etid 0 (tracked by all)
+        int pend = -1, pend_age = 0;             // split item whose completion is deferred
+        auto complete_pending = [&]() {
+            const WorkItem pt = args.items[pend];
+            int32_t* counter = args.counters + pt.tile_slot;
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");   // this thread's reductions have landed
+            named_bar_sync(1, 128);
+            if (etid == 0) {
+                int32_t prev;
+                asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(counter) : "memory");
+                const int last = prev == pt.nsplit - 1;
+                if (last) {
+                    *counter = 0;   // re-arm for the next launch of this plan
+                    fence_proxy_async_global();   // the other splits' sums, for the bulk loads
+                }
+                *split_flag = last;
+                if (args.trace) args.trace[8 * pend + 5] = global_timer_ns();
+            }
+            named_bar_sync(1, 128);
+            const bool last = *split_flag != 0;
+            named_bar_sync(1, 128);   // split_flag read by all before it can be rewritten
+            if (last) {
+                groups += split_finalize(load_epi(args.probs + pt.problem), pt.row0, pt.col0,
+                                         args.ws + (int64_t)pt.ws_blk * kWsBlock, S, trow, etid);
+                if (args.trace && etid == 0) args.trace[8 * pend + 6] = global_timer_ns();
+            }
+            pend = -1;
+        };
         for (int i = beg; i < end; ++i) {
             const WorkItem it = args.items[i];
             const DevProblem* Pg = args.probs + it.problem;
@@ -606,8 +709,12 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
                 const uint32_t taddr = tmem_base + ((uint32_t)(lgrp * 32) << 16) + (uint32_t)acc * kMaxBN;
                 const int nchunks = E.bn / 32;
                 const bool split = it.nsplit > 1;
-                if (!split && E.tma_out) {
-                    epilogue_staged(E, it.row0, it.col0, stg, trow, etid, taddr, &tempty[acc],
+                if (args.dbg & 2) {   // experiment: no epilogue (bounds the load/MMA side)
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                } else if (!split && E.tma_out && !(args.dbg & 8)) {
+                    groups += epilogue_staged(E, it.row0, it.col0, S, trow, etid, taddr, &tempty[acc],
                                     args.trace ? args.trace + 8 * i : nullptr);
                 } else if (!split) {
                     for (int c = 0; c < nchunks; ++c) {
@@ -619,32 +726,15 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[acc]);
                 } else {
-                    // split-K (planner only splits TMA-store problems): reduce-add this split's
-                    // partial into the tile's fp32 accumulator; the last arrival finalizes.
+                    // split-K (planner only splits TMA-store problems): reduce now, complete later
+                    if (pend >= 0) complete_pending();   // at most one split in flight
                     float* acc_tile = args.ws + (int64_t)it.ws_blk * kWsBlock;
-                    uint64_t* tr = args.trace ? args.trace + 8 * i : nullptr;
-                    split_partial_reduce(E, acc_tile, trow, taddr, &tempty[acc]);
-                    if (tr && etid == 0) tr[4] = global_timer_ns();
-                    named_bar_sync(1, 128);   // all of this CTA's REDs issued
-                    if (etid == 0) {
-                        asm volatile("fence.acq_rel.gpu;" ::: "memory");   // release: REDs before the count
-                        const int prev = atomicAdd(args.counters + it.tile_slot, 1);
-                        const int last = prev == it.nsplit - 1;
-                        if (last) {
-                            asm volatile("fence.acq_rel.gpu;" ::: "memory");   // acquire the others' REDs
-                            args.counters[it.tile_slot] = 0;   // re-arm for the next launch
-                        }
-                        *split_flag = last;
-                    }
-                    named_bar_sync(1, 128);
-                    if (tr && etid == 0) tr[5] = global_timer_ns();
-                    if (*split_flag) {
-                        split_finalize(E, it.row0, it.col0, acc_tile, stg, trow, etid);
-                        if (tr && etid == 0) tr[6] = global_timer_ns();
-                    }
+                    split_reduce(E, acc_tile, trow, taddr, &tempty[acc]);
+                    if (args.trace && etid == 0) args.trace[8 * i + 4] = global_timer_ns();
+                    pend = i;
+                    pend_age = 0;
                 }
-                acc ^= 1;
-                if (acc == 0) acc_phase ^= 1;
+                if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
             } else if (it.type == kItemGemv) {
                 if (Pg->in_dt == GMX_ST_F32)
                     gemv_rows<float>(Pg, it.row0, it.col0, ew);
@@ -660,17 +750,21 @@ __global__ void __launch_bounds__(kThreads, 1) coalesced_step_kernel(const Kerne
                 named_bar_sync(2, 128);
                 if (etid == 0) args.trace[8 * i + 3] = global_timer_ns();
             }
+            if (pend >= 0 && pend != i && ++pend_age >= 1) complete_pending();
         }
-        if (etid == 0) bulk_wait0();   // all TMA stores of this CTA complete
+        if (pend >= 0) complete_pending();
+        // TMA stores must have read their smem before the CTA exits; their global writes
+        // complete with the grid (a dependent launch's griddepcontrol.wait covers them)
+        if (etid == 0) bulk_wait_read0();
     }
 
     tc_fence_before();
     __syncthreads();
     // this CTA's work is done: the next step may start taking SMs
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (!args.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp == 1 && has_gemm) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, kTmemCols);
+        tmem_dealloc(tmem_base, Cfg::tmem_cols);
     }
 }
 
@@ -776,10 +870,13 @@ struct gmx_exec {
     int32_t* counters = nullptr;
     int32_t counters_cap = 0;
     int64_t max_split = 32;
+    int64_t split_pct = 100;     // split a tile into pieces of about this % of the per-CTA share
+    int ctas_per_sm = 2;         // 1 or 2 resident CTAs of the coalesced kernel per SM
     bool cache_plans = true;
     bool attr_set = false;
     bool tracing = false;
     bool pdl = true;
+    bool early_trigger = true;
     bool multi_stream = false;   // launches may come from several streams (realtime runtime)
     int32_t dbg = 0;
     const gmx::Plan* recent[3] = {nullptr, nullptr, nullptr};   // plans of the last launches
@@ -813,7 +910,7 @@ static int ensure_table(gmx_exec* ex, cudaStream_t stream) {
 // last split's finalize ~2.2 us.
 constexpr double kNsPerKB = 20.0;
 constexpr double kTileFixedNs = 600.0;
-constexpr double kSplitNs = 2000.0 + 2200.0;
+constexpr double kSplitNs = 800.0;   // epilogue-side reduce issue; the L2 round trips are deferred
 constexpr double kCudaCoreFixedNs = 400.0;
 
 static double gemm_tile_cost(const DevProblem& P, int kb) {
@@ -848,15 +945,18 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
             total += (double)hp.op_bytes / 1024.0 * kNsPerKB + kCudaCoreFixedNs;
         }
     }
-    const double target = std::max(total / ex->num_sms, 2000.0);
+    const int slots_total = ex->num_sms * ex->ctas_per_sm;   // resident CTAs of one launch
+    // per-CTA share; with 2 CTAs/SM each streams at about half an SM's rate
+    const double target = std::max(total * ex->ctas_per_sm / slots_total, 2000.0);
     // GEMM tiles, split along K when one tile exceeds the per-SM share
     int32_t n_counters = 0;
     int64_t ws_blocks = 0;
     for (const TileRef& t : tiles) {
         const DevProblem& P = ex->probs[t.slot].dev;
         int nsplit = 1;
-        if (t.cost > target && P.kblocks >= 2 && P.tma_out) {
-            nsplit = (int)std::min<int64_t>({(int64_t)std::ceil(t.cost / target), (int64_t)P.kblocks, ex->max_split, 255});
+        const double piece = target * (double)ex->split_pct / 100.0;
+        if (t.cost > piece && P.kblocks >= 2 && P.tma_out) {
+            nsplit = (int)std::min<int64_t>({(int64_t)std::ceil(t.cost / piece), (int64_t)P.kblocks, ex->max_split, 255});
             // splitting only pays when a piece plus the fixup beats the whole tile
             if (gemm_tile_cost(P, (P.kblocks + nsplit - 1) / nsplit) + kSplitNs >= t.cost) nsplit = 1;
         }
@@ -919,7 +1019,7 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
     }
     // LPT: longest item first onto the least-loaded CTA
     std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.cost > b.cost; });
-    const int grid = (int)std::max<size_t>(1, std::min<size_t>((size_t)ex->num_sms, cands.size()));
+    const int grid = (int)std::max<size_t>(1, std::min<size_t>((size_t)slots_total, cands.size()));
     std::vector<std::vector<int32_t>> per_cta(grid);
     std::vector<double> load(grid, 0.0);
     using QE = std::pair<double, int>;
@@ -936,6 +1036,9 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
     plan.cta_off.assign(1, 0);
     std::vector<int32_t> flags(grid, 0);
     for (int c = 0; c < grid; ++c) {
+        // split pieces first: their deferred completion then overlaps the CTA's other items
+        std::stable_partition(per_cta[c].begin(), per_cta[c].end(),
+                              [&](int32_t idx) { return cands[idx].it.nsplit > 1; });
         for (int32_t idx : per_cta[c]) {
             plan.items.push_back(cands[idx].it);
             if (cands[idx].it.type == kItemGemm) flags[c] |= 1;
@@ -975,7 +1078,7 @@ static int upload_plan(gmx_exec* ex, Plan& plan, cudaStream_t stream) {
     plan.d_off = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(plan.d_buf) + items_bytes);
     if (plan.ws_floats > 0 || plan.n_counters > 0) {
         const size_t ws_bytes = (size_t)plan.ws_floats * sizeof(float);
-        const size_t state = ws_bytes + (size_t)std::max(1, plan.n_counters) * sizeof(int32_t);
+        const size_t state = ws_bytes + (size_t)std::max(1, 2 * plan.n_counters) * sizeof(int32_t);
         GMX_CUDA(cudaMallocAsync(&plan.d_state, state, stream));
         GMX_CUDA(cudaMemsetAsync(plan.d_state, 0, state, stream));
         plan.d_ws = reinterpret_cast<float*>(plan.d_state);
@@ -1229,7 +1332,10 @@ int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stre
     plan->stream = stream;
     plan->last_use = ++ex->clock;
     if (!ex->attr_set) {
-        GMX_CUDA(cudaFuncSetAttribute(coalesced_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+        GMX_CUDA(cudaFuncSetAttribute(coalesced_step_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      smem_bytes<1>()));
+        GMX_CUDA(cudaFuncSetAttribute(coalesced_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      smem_bytes<2>()));
         ex->attr_set = true;
     }
     if (ex->tracing && (int64_t)plan->items.size() > ex->trace_cap) {
@@ -1246,18 +1352,22 @@ int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stre
     bool independent = (flags & GMX_LAUNCH_INDEPENDENT) != 0 && !ex->tracing;
     for (const Plan* r : ex->recent) independent &= (r != plan);
     KernelArgs args{ex->d_probs, plan->d_items, plan->d_off, plan->d_off + plan->stats.grid + 1, plan->d_ws,
-                    plan->d_counters, ex->tracing ? ex->trace : nullptr, ex->dbg, independent ? 1 : 0};
+                    plan->d_counters, ex->tracing ? ex->trace : nullptr, ex->dbg, independent ? 1 : 0,
+                    ex->early_trigger ? 1 : 0};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(plan->stats.grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.dynamicSmemBytes = ex->ctas_per_sm == 2 ? smem_bytes<2>() : smem_bytes<1>();
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = ex->pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    GMX_CUDA(cudaLaunchKernelEx(&cfg, coalesced_step_kernel, args));
+    if (ex->ctas_per_sm == 2)
+        GMX_CUDA(cudaLaunchKernelEx(&cfg, coalesced_step_kernel<2>, args));
+    else
+        GMX_CUDA(cudaLaunchKernelEx(&cfg, coalesced_step_kernel<1>, args));
     if (ex->multi_stream) {
         if (!plan->done_ev) GMX_CUDA(cudaEventCreateWithFlags(&plan->done_ev, cudaEventDisableTiming));
         GMX_CUDA(cudaEventRecord(plan->done_ev, stream));
@@ -1291,6 +1401,12 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
     if (n == "max_split") {
         if (value < 1 || value > 255) return fail(GMX_EINVAL, "max_split must be in [1, 255]");
         ex->max_split = value;
+    } else if (n == "ctas_per_sm") {
+        if (value != 1 && value != 2) return fail(GMX_EINVAL, "ctas_per_sm must be 1 or 2");
+        ex->ctas_per_sm = (int)value;
+    } else if (n == "split_pct") {
+        if (value < 10 || value > 400) return fail(GMX_EINVAL, "split_pct must be in [10, 400]");
+        ex->split_pct = value;
     } else if (n == "cache_plans") {
         ex->cache_plans = value != 0;
     } else if (n == "plan_capacity") {
@@ -1298,6 +1414,9 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
         ex->plan_capacity = (size_t)value;
     } else if (n == "multi_stream") {
         ex->multi_stream = value != 0;
+        return GMX_OK;
+    } else if (n == "early_trigger") {
+        ex->early_trigger = value != 0;
         return GMX_OK;
     } else if (n == "pdl") {
         ex->pdl = value != 0;

@@ -93,7 +93,7 @@ def test_c2_coalesced_single_launch(ex):
     ex.launch(slots)
     torch.cuda.synchronize()
     plan = ex.last_plan()
-    assert plan["grid"] <= ex.num_sms and plan["n_items"] >= plan["n_gemm_tiles"]
+    assert plan["grid"] <= 2 * ex.num_sms and plan["n_items"] >= plan["n_gemm_tiles"]
     for o in ops:
         _check(o)
     # repeated launches (cached plan, split-K accumulators/counters re-armed) stay correct;
@@ -185,3 +185,47 @@ def test_scheduler_step_drives_one_launch(ex):
     assert done == set(range(16))
     for o in ops.values():
         _check(o)
+
+
+@pytest.mark.parametrize("ctas_per_sm,split_pct", [(1, 100), (1, 250), (2, 60), (2, 100), (2, 400)])
+def test_c2_kernel_shapes_and_split_plans(ex, ctas_per_sm, split_pct):
+    """Both kernel build shapes (1 or 2 CTAs/SM) and coarse/fine split-K plans give the same
+    (within-tolerance) results, also on repeated launches with the workspace re-armed."""
+    from paper_1901_10008_b200.executor import OperandSet
+    ex.set_option("ctas_per_sm", ctas_per_sm)
+    ex.set_option("split_pct", split_pct)
+    try:
+        ops = [OperandSet("gemm", C2_SHAPES[i % 13], seed=300 + i, bias=(i % 3 == 0),
+                          activation=("relu", "none", "gelu")[i % 3]) for i in range(16)]
+        slots = [o.register(ex) for o in ops]
+        for _ in range(3):
+            ex.launch(slots)
+        torch.cuda.synchronize()
+        assert ex.last_plan()["grid"] <= ctas_per_sm * ex.num_sms
+        for o in ops:
+            _check(o)
+        for s in slots:
+            ex.unregister(s)
+    finally:
+        ex.set_option("ctas_per_sm", 2)
+        ex.set_option("split_pct", 100)
+
+
+def test_independent_back_to_back_launches(ex):
+    """PDL early trigger: independent launches over rotating operand sets overlap on the GPU
+    (the next grid's CTAs take SMs as ours retire); every set's results stay correct."""
+    from paper_1901_10008_b200.executor import OperandSet
+    sets = [[OperandSet("gemm", C2_SHAPES[(i + r) % 13], seed=400 + 16 * r + i) for i in range(16)]
+            for r in range(3)]
+    slots = [[o.register(ex) for o in row] for row in sets]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for k in range(12):
+            ex.launch(slots[k % 3], s, independent=True)
+    s.synchronize()
+    for row in sets:
+        for o in row:
+            _check(o)
+    for row in slots:
+        for sl in row:
+            ex.unregister(sl)
