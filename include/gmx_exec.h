@@ -101,6 +101,23 @@ int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream)
 int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream, int32_t flags);
 /* Stats of the plan used by the last launch. */
 int gmx_exec_last_plan(const gmx_exec* ex, gmx_plan_stats* out);
+
+/* Resident (persistent) mode. begin launches ONE cooperative kernel on `stream` that stays on
+ * the GPU; every gmx_exec_launch_ex until end() appends its step to a queue (pinned host ring,
+ * relayed to a device ring) instead of launching, so consecutive steps stream through the same
+ * smem/TMEM pipelines with no launch gap. Steps run in queue order with bounded skew; a step
+ * without GMX_LAUNCH_INDEPENDENT (or reusing a slot/plan of the last 2 steps) waits for all
+ * earlier steps. end() queues a stop; the kernel exits after the last step, so later work on
+ * `stream` is ordered after every queued step. completed() = longest finished prefix of steps. */
+int gmx_exec_resident_begin(gmx_exec* ex, void* stream);
+/* hold != 0: the kernel relays no step until gmx_exec_resident_release (or end), so a batch
+ * queued meanwhile runs back to back; resident_device_ns then gives the device time from the
+ * release to the last step's completion (%globaltimer), i.e. the kernel alone. */
+int gmx_exec_resident_begin_ex(gmx_exec* ex, void* stream, int32_t hold);
+int gmx_exec_resident_release(gmx_exec* ex);
+int gmx_exec_resident_device_ns(gmx_exec* ex, int64_t* ns);
+int gmx_exec_resident_end(gmx_exec* ex);
+int gmx_exec_resident_completed(gmx_exec* ex, int64_t* steps_done);
 /* A caller-owned stream is about to be destroyed: wait for its work and stop using it for
  * the stream-ordered release of plan memory. */
 int gmx_exec_stream_retired(gmx_exec* ex, void* stream);

@@ -50,7 +50,7 @@ namespace gmx {
 
 enum : int32_t { kItemGemm = 0, kItemGemv = 1, kItemEltwise = 2 };
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;             // 6 role warps + 1 queue-dispatcher warp (resident mode)
 // Two build shapes of the same kernel (selected per executor, option "ctas_per_sm"):
 //   1 CTA/SM : 6-stage ring, 32 KB output staging (one resident CTA streams alone)
 //   2 CTAs/SM: 3-stage ring each, 16 KB staging; two CTAs (of one launch, or of consecutive
@@ -73,7 +73,7 @@ constexpr int kStageBytes = kStageA + kStageB;
 template <int kCtasPerSm>
 constexpr int smem_bytes() {
     using C = SmemCfg<kCtasPerSm>;
-    return C::stages * kStageBytes + C::stage_out + C::align_pad + 256 /*barriers*/;
+    return C::stages * kStageBytes + C::stage_out + C::align_pad + 512 /*barriers + unit queue*/;
 }
 static_assert(2 * (smem_bytes<2>() + 1024) <= 233472, "two CTAs must fit one SM's shared memory");
 constexpr int kWsBlock = 4096;             // split-K workspace allocation unit (floats)
@@ -117,6 +117,44 @@ struct WorkItem {
 };
 static_assert(sizeof(WorkItem) == 32, "WorkItem layout");
 
+// ---- resident mode: one persistent launch consumes a queue of steps ----------------------
+// The host appends StepDescs to a ring in pinned, device-mapped host memory and publishes a
+// count; one dispatcher lane (block 0) copies each new descriptor into a device-memory ring and
+// publishes it there, so the 2 x #SM role leaders poll L2, not PCIe. Steps run back to back
+// through the same smem/TMEM pipelines: the producer streams step k+1's tiles while the
+// epilogue drains step k. Each CTA counts its finish of a step into a monotonic per-slot
+// counter; a step may start only when step k - kWindow has completed everywhere (bounded
+// skew, so split-K state and outputs of a plan reused kWindow+ steps later are free), and a
+// step flagged `wait_all` (dependent members, or slots/plans reused inside the window) waits
+// for every earlier step.
+constexpr int kQueue = 1024;  // ring slots (host and device)
+constexpr int kMaxWindow = 16;   // max steps a CTA may run ahead of the slowest (option, <= this)
+
+struct StepDesc {
+    const DevProblem* probs;
+    const WorkItem* items;
+    const int32_t* cta_off;   // cta_off[grid + 1] (items of CTA c: [cta_off[c], cta_off[c + 1]))
+    float* ws;
+    int32_t* counters;
+    int32_t grid;             // CTAs holding items in this step (<= gridDim.x)
+    int32_t wait_all;         // a member depends on earlier outputs: all earlier steps first
+    int32_t stop;
+    int32_t _pad;
+    int64_t wait_step;        // latest earlier step sharing a plan or slot with this one, or -1
+};
+static_assert(sizeof(StepDesc) == 64, "StepDesc layout");
+
+struct DevQueue {
+    StepDesc ring[kQueue];
+    int64_t published;        // steps available in `ring` (dispatcher -> role leaders)
+    uint64_t t_first;         // %globaltimer when step 0 was relayed (after a held start's release)
+    uint64_t t_last;          // %globaltimer of the latest step completion
+    uint64_t t_relay;         // %globaltimer of the dispatcher's latest relay
+    int64_t _pad[4];
+    uint32_t done[kQueue];    // monotonic count of item lists finished, per slot
+    uint32_t grab[kQueue];    // monotonic list-grab counter, per slot (2 x grid per step)
+};
+
 struct KernelArgs {
     const DevProblem* probs;
     const WorkItem* items;
@@ -128,7 +166,55 @@ struct KernelArgs {
     int32_t dbg;             // experiment flags (reserved)
     int32_t independent;     // 1: no data dependency on the previous launch (skip griddepcontrol.wait)
     int32_t early_trigger;   // 1: let the next launch start as soon as all our CTAs are resident
+    int32_t resident;        // 1: persistent: steps come from the queue below, not the fields above
+    DevQueue* dq;
+    const StepDesc* hring;   // host-mapped ring + published count (resident mode)
+    const int64_t* hpub;
+    int64_t* hdone;          // host-mapped: step seq + 1 written when a slot's step completed
+    int32_t window;          // resident: max steps a CTA may run ahead of the slowest
+    uint64_t* rtrace;        // resident diagnostics: 4 stamps per (step, CTA), or null
+    int32_t rtrace_steps;
 };
+
+// The items/tables one step works on, as seen by one CTA.
+struct StepView {
+    const DevProblem* probs;
+    const WorkItem* items;
+    float* ws;
+    int32_t* counters;
+    int beg, end;
+    bool stop;
+};
+
+__device__ __forceinline__ int64_t ld_acquire_gpu_s64(const int64_t* p) {
+    int64_t v;
+    asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int64_t ld_acquire_sys_s64(const int64_t* p) {
+    int64_t v;
+    asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Spin (with backoff) until the step in `slot` of round `round` (= seq / kQueue) was finished
+// by all `nctas` CTAs. A watchdog turns a protocol bug into a launch error instead of a hang.
+__device__ __forceinline__ void wait_step_done(const DevQueue* q, int64_t seq, uint32_t nctas) {
+    if (seq < 0) return;
+    const uint32_t need = nctas * (uint32_t)(seq / kQueue + 1);
+    const uint32_t* c = &q->done[seq % kQueue];
+    if ((int32_t)(ld_acquire_gpu_u32(c) - need) >= 0) return;
+    const uint64_t t0 = global_timer_ns();
+    while ((int32_t)(ld_acquire_gpu_u32(c) - need) < 0) {
+        __nanosleep(64);
+        if (global_timer_ns() - t0 > 8000000000ull) __trap();
+    }
+}
 
 __device__ __forceinline__ float apply_act(float x, int32_t act) {
     if (act == GMX_ACT_RELU) return fmaxf(x, 0.0f);
@@ -387,6 +473,20 @@ __device__ __forceinline__ uint32_t epilogue_staged(const EpiParams& E, int row0
 // launches on other streams) can deadlock. fp32 add order is arrival order (within tolerance;
 // `max_split=1` is bitwise-stable).
 
+// cp.async.bulk.wait_group takes an immediate: wait until at most n groups are pending.
+__device__ __forceinline__ void bulk_wait_upto(uint32_t n) {
+    switch (n) {
+        case 0: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
+        case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
+        case 3: asm volatile("cp.async.bulk.wait_group 3;" ::: "memory"); break;
+        case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
+        case 5: asm volatile("cp.async.bulk.wait_group 5;" ::: "memory"); break;
+        case 6: asm volatile("cp.async.bulk.wait_group 6;" ::: "memory"); break;
+        default: asm volatile("cp.async.bulk.wait_group 7;" ::: "memory"); break;
+    }
+}
+
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");
@@ -560,29 +660,144 @@ __device__ void eltwise_range(const DevProblem* Pg, int e0, int e1, int tid, int
     }
 }
 
+// Items of list `idx` of step k (non-resident: the launch's own plan, k == 0).
+__device__ __forceinline__ StepView list_view(const KernelArgs& a, int64_t k, int idx) {
+    StepView v{};
+    if (!a.resident) {
+        v.probs = a.probs; v.items = a.items; v.ws = a.ws; v.counters = a.counters;
+        v.beg = a.cta_off[idx];
+        v.end = a.cta_off[idx + 1];
+        return v;
+    }
+    const StepDesc* d = &a.dq->ring[k % kQueue];
+    v.probs = (const DevProblem*)__ldcg((const long long*)&d->probs);
+    v.items = (const WorkItem*)__ldcg((const long long*)&d->items);
+    v.ws = (float*)__ldcg((const long long*)&d->ws);
+    v.counters = (int32_t*)__ldcg((const long long*)&d->counters);
+    const int32_t* off = (const int32_t*)__ldcg((const long long*)&d->cta_off);
+    if (idx < __ldcg(&d->grid)) {
+        v.beg = __ldcg(off + idx);
+        v.end = __ldcg(off + idx + 1);
+    }
+    return v;
+}
+
+// Resident producer: wait until step k is published; returns true for the stop step.
+__device__ __forceinline__ bool step_published(const KernelArgs& a, int64_t k) {
+    const uint64_t t0 = global_timer_ns();
+    while (ld_acquire_gpu_s64(&a.dq->published) <= k) {
+        __nanosleep(128);
+        if (global_timer_ns() - t0 > 60000000000ull) __trap();   // host never published
+    }
+    return __ldcg(&a.dq->ring[k % kQueue].stop) != 0;
+}
+
+// Resident producer: bounded skew + explicit ordering before taking lists of step k.
+__device__ __forceinline__ void step_order(const KernelArgs& a, int64_t k) {
+    const StepDesc* d = &a.dq->ring[k % kQueue];
+    if (__ldcg(&d->wait_all)) {
+        for (int64_t j = k - 1; j >= 0 && j >= k - a.window; --j) wait_step_done(a.dq, j, gridDim.x);
+        fence_proxy_async_global();   // later TMA loads read what those steps wrote
+    } else {
+        // bounded skew, plus the latest step that used the same plan (split-K state) or wrote a
+        // slot this step writes; that step itself waited for any earlier sharer, transitively
+        wait_step_done(a.dq, k - a.window, gridDim.x);
+        wait_step_done(a.dq, (int64_t)__ldcg((const long long*)&d->wait_step), gridDim.x);
+    }
+}
+
+// Work units flow producer -> (MMA, epilogue) through a small smem ring: the producer takes
+// item lists of step k from a per-step counter (any CTA may take any list: the device balances
+// the lists dynamically, like the block scheduler does for separate launches), then issues
+// their loads; the MMA issuer and the epilogue consume the same units in order.
+constexpr int kUnitQ = 8;
+constexpr int32_t kUnitEndStep = -1;   // this CTA took no more lists of step k
+constexpr int32_t kUnitStop = -2;
+struct Unit {
+    int64_t k;
+    int32_t idx;
+    int32_t _pad;
+};
+
+// Dispatcher (resident mode; block 0, warp 6): host ring -> device ring.
+__device__ void dispatch_steps(const KernelArgs& a) {
+    // held start: relay nothing until the host sets the go flag (hpub[1]), so a batch queued
+    // beforehand runs back to back and t_first..t_last times the device alone
+    const uint64_t th = global_timer_ns();
+    while (ld_acquire_sys_s64(a.hpub + 1) == 0) {
+        __nanosleep(512);
+        if (global_timer_ns() - th > 60000000000ull) __trap();
+    }
+    a.dq->t_first = global_timer_ns();
+    // relay in batches: one poll of the host count, then up to kBatch entries whose PCIe loads
+    // are all in flight together (a PCIe round trip costs ~1-2 us; one per step would cap the
+    // step rate)
+    constexpr int kBatch = 8;
+    int64_t k = 0;
+    for (;;) {
+        int64_t avail;
+        const uint64_t t0 = global_timer_ns();
+        uint32_t nap = 64;   // back off while idle: each poll is a PCIe round trip
+        while ((avail = ld_acquire_sys_s64(a.hpub)) <= k) {
+            __nanosleep(nap);
+            nap = nap < 2048 ? 2 * nap : nap;
+            if (global_timer_ns() - t0 > 60000000000ull) __trap();   // host never published
+        }
+        const int n = (int)(avail - k < kBatch ? avail - k : kBatch);
+        uint4 w[kBatch][4];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            if (b < n) {
+                const uint4* src = reinterpret_cast<const uint4*>(&a.hring[(k + b) % kQueue]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)   // system-scope loads of host-written entries (after the acquire)
+                    asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(w[b][q].x), "=r"(w[b][q].y), "=r"(w[b][q].z), "=r"(w[b][q].w)
+                                 : "l"(src + q));
+            }
+        }
+        bool stop = false;
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            if (b < n && !stop) {
+                uint4* dst = reinterpret_cast<uint4*>(&a.dq->ring[(k + b) % kQueue]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) __stcg(dst + q, w[b][q]);
+                stop = reinterpret_cast<const StepDesc*>(w[b])->stop != 0;
+            }
+        }
+        k += n;
+        asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(&a.dq->published), "l"(k) : "memory");
+        a.dq->t_relay = global_timer_ns();
+        if (stop) break;
+    }
+}
+
+// Register cap per shape (the 2-CTA shape keeps two CTAs' registers within one SM's 64K).
 template <int kCtasPerSm>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) coalesced_step_kernel(const KernelArgs args) {
+__global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(const KernelArgs args) {
     using Cfg = SmemCfg<kCtasPerSm>;
     constexpr int kStages = Cfg::stages;
     constexpr int kStageOut = Cfg::stage_out;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    extern __shared__ __align__(16) uint8_t smem_raw[];   // 1024-aligned in practice (no static smem); checked below
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     if (Cfg::align_pad == 0 && smem != smem_raw) __trap();   // SWIZZLE_128B tiles need 1024-byte alignment
     uint8_t* stg = smem + kStages * kStageBytes;                       // epilogue staging (1024-aligned)
-    uint64_t* full = reinterpret_cast<uint64_t*>(stg + kStageOut);
+    Unit* uq = reinterpret_cast<Unit*>(stg + kStageOut);               // resident work-unit ring
+    uint64_t* full = reinterpret_cast<uint64_t*>(uq + kUnitQ);
     uint64_t* empty = full + kStages;
     uint64_t* tfull = empty + kStages;
     constexpr int kAcc = Cfg::acc_bufs;
     uint64_t* tempty = tfull + kAcc;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAcc);
+    uint64_t* ufull = tempty + kAcc;
+    uint64_t* uempty = ufull + kUnitQ;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uempty + kUnitQ);
     int32_t* split_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
-    const int beg = args.cta_off[blockIdx.x];
-    const int end = args.cta_off[blockIdx.x + 1];
-
-    const bool has_gemm = (args.cta_flags[blockIdx.x] & 1) != 0;   // host-computed: CTA owns GEMM tiles
+    // host-computed: CTA owns GEMM tiles (a resident CTA may get them in any step)
+    const bool has_gemm = args.resident || (args.cta_flags[blockIdx.x] & 1) != 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -592,6 +807,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) coalesced_step_kernel(co
         for (int a = 0; a < kAcc; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 4);   // one arrival per epilogue warp
+        }
+        for (int u = 0; u < kUnitQ; ++u) {
+            mbar_init(&ufull[u], 1);
+            mbar_init(&uempty[u], 2);   // MMA issuer + epilogue
         }
         mbar_fence_init();
     }
@@ -608,26 +827,76 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) coalesced_step_kernel(co
     // step's start (a dependent next step still waits for our completion and flush).
     if (args.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-    if (warp == 0) {
-        // ---------------- TMA producer ----------------
+    // Units: non-resident = this CTA's own list of the launch's plan, then stop; resident =
+    // the unit ring filled by the producer.
+    int uslot = 0;
+    uint32_t uphase = 0;
+    auto next_unit = [&](bool first) -> Unit {
+        if (!args.resident) return first ? Unit{0, (int32_t)blockIdx.x, 0} : Unit{0, kUnitStop, 0};
+        mbar_wait(&ufull[uslot], uphase);
+        return uq[uslot];
+    };
+    auto release_unit = [&]() {   // one consumer thread: done reading the current unit
+        if (args.resident) mbar_arrive(&uempty[uslot]);
+    };
+    auto advance_unit = [&]() {
+        if (args.resident && ++uslot == kUnitQ) { uslot = 0; uphase ^= 1; }
+    };
+
+    if (warp == 6) {
+        // ---------------- queue dispatcher (resident mode, block 0) ----------------
+        if (lane == 0 && args.resident && blockIdx.x == 0) dispatch_steps(args);
+    } else if (warp == 0) {
+        // ---------------- TMA producer (resident: also takes the item lists) ----------------
         if (lane == 0 && has_gemm) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int i = beg; i < end; ++i) {
-                const WorkItem it = args.items[i];
-                if (it.type != kItemGemm) continue;
-                const DevProblem* P = args.probs + it.problem;
-                const uint32_t bytes = kStageA + (uint32_t)P->bn * (kBlockK * 2);
-                if (args.trace) args.trace[8 * i + 0] = global_timer_ns();
-                tma_prefetch_desc(&P->tm_rows);   // descriptor fetch overlaps the slot wait
-                tma_prefetch_desc(&P->tm_cols);
-                for (int kb = it.kb0; kb < it.kb1; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* tile = smem + stage * kStageBytes;
-                    mbar_expect_tx(&full[stage], bytes);
-                    tma_load_2d(tile, &P->tm_rows, &full[stage], kb * kBlockK, it.row0);
-                    tma_load_2d(tile + kStageA, &P->tm_cols, &full[stage], kb * kBlockK, it.col0);
-                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+            auto issue_list = [&](const StepView& v, uint64_t* rt) {
+                for (int i = v.beg; i < v.end; ++i) {
+                    const WorkItem it = v.items[i];
+                    if (it.type != kItemGemm) continue;
+                    const DevProblem* P = v.probs + it.problem;
+                    const uint32_t bytes = kStageA + (uint32_t)P->bn * (kBlockK * 2);
+                    if (args.trace) args.trace[8 * i + 0] = global_timer_ns();
+                    tma_prefetch_desc(&P->tm_rows);   // descriptor fetch overlaps the slot wait
+                    tma_prefetch_desc(&P->tm_cols);
+                    for (int kb = it.kb0; kb < it.kb1; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* tile = smem + stage * kStageBytes;
+                        mbar_expect_tx(&full[stage], bytes);
+                        tma_load_2d(tile, &P->tm_rows, &full[stage], kb * kBlockK, it.row0);
+                        tma_load_2d(tile + kStageA, &P->tm_cols, &full[stage], kb * kBlockK, it.col0);
+                        if (++stage == kStages) { stage = 0; phase ^= 1; }
+                    }
+                }
+                if (rt) rt[1] = global_timer_ns();
+            };
+            if (!args.resident) {
+                issue_list(list_view(args, 0, blockIdx.x), nullptr);
+            } else {
+                auto push = [&](int64_t k, int32_t idx) {
+                    mbar_wait(&uempty[uslot], uphase ^ 1);
+                    uq[uslot] = Unit{k, idx, 0};
+                    mbar_arrive(&ufull[uslot]);   // release: the unit is visible to the consumers
+                    advance_unit();
+                };
+                const uint32_t G = gridDim.x;
+                for (int64_t k = 0;; ++k) {
+                    if (step_published(args, k)) { push(k, kUnitStop); break; }
+                    step_order(args, k);
+                    uint64_t* rt = (args.rtrace && k < args.rtrace_steps) ? args.rtrace + (k * G + blockIdx.x) * 8 : nullptr;
+                    if (rt) rt[0] = global_timer_ns();
+                    const uint32_t base = 2u * G * (uint32_t)(k / kQueue);   // every step takes 2 x G grabs
+                    uint32_t* grab = &args.dq->grab[k % kQueue];
+                    uint32_t idx = atomicAdd(grab, 1u) - base;
+                    for (;;) {
+                        if (idx >= G) { push(k, kUnitEndStep); break; }
+                        push(k, (int32_t)idx);
+                        // the next grab's L2 round trip overlaps this list's load issue
+                        const uint32_t nxt = atomicAdd(grab, 1u) - base;
+                        issue_list(list_view(args, k, (int)idx), rt);
+                        idx = nxt;
+                    }
                 }
             }
         }
@@ -636,31 +905,41 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) coalesced_step_kernel(co
         if (lane == 0 && has_gemm) {
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            for (int i = beg; i < end; ++i) {
-                const WorkItem it = args.items[i];
-                if (it.type != kItemGemm) continue;
-                const uint32_t idesc = idesc_bf16_m128((uint32_t)args.probs[it.problem].bn);
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem_base + (uint32_t)acc * kMaxBN;
-                for (int kb = it.kb0; kb < it.kb1; ++kb) {
-                    mbar_wait(&full[stage], phase);
+            for (bool first = true;; first = false) {
+                const Unit u = next_unit(first);
+                release_unit();
+                advance_unit();
+                if (u.idx == kUnitStop) break;
+                if (u.idx < 0) continue;
+                const StepView v = list_view(args, u.k, u.idx);
+                for (int i = v.beg; i < v.end; ++i) {
+                    const WorkItem it = v.items[i];
+                    if (it.type != kItemGemm) continue;
+                    const uint32_t idesc = idesc_bf16_m128((uint32_t)v.probs[it.problem].bn);
+                    mbar_wait(&tempty[acc], acc_phase ^ 1);
                     tc_fence_after();
-                    const uint8_t* tile = smem + stage * kStageBytes;
-                    const uint64_t a_desc = smem_desc_sw128(tile);
-                    const uint64_t b_desc = smem_desc_sw128(tile + kStageA);
+                    const uint32_t d_tmem = tmem_base + (uint32_t)acc * kMaxBN;
+                    for (int kb = it.kb0; kb < it.kb1; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint8_t* tile = smem + stage * kStageBytes;
+                        const uint64_t a_desc = smem_desc_sw128(tile);
+                        const uint64_t b_desc = smem_desc_sw128(tile + kStageA);
 #pragma unroll
-                    for (int k = 0; k < kBlockK / 16; ++k)   // 16-element UMMA K steps = +32 B
-                        if (!(args.dbg & 4)) umma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb > it.kb0 || k > 0) ? 1u : 0u);
-                    umma_commit(&empty[stage]);
-                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                        for (int kk = 0; kk < kBlockK / 16; ++kk)   // 16-element UMMA K steps = +32 B
+                            if (!(args.dbg & 4))
+                                umma_bf16(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc,
+                                          (kb > it.kb0 || kk > 0) ? 1u : 0u);
+                        umma_commit(&empty[stage]);
+                        if (++stage == kStages) { stage = 0; phase ^= 1; }
+                    }
+                    umma_commit(&tfull[acc]);
+                    if (args.trace) args.trace[8 * i + 1] = global_timer_ns();
+                    if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
                 }
-                umma_commit(&tfull[acc]);
-                if (args.trace) args.trace[8 * i + 1] = global_timer_ns();
-                if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
             }
         }
-    } else {
+    } else if (warp >= 2 && warp <= 5) {
         // ---------------- epilogue / CUDA-core items ----------------
         const int ew = warp - 2;                 // 0..3
         const int lgrp = warp & 3;               // TMEM lane quarter this warp may access
@@ -671,9 +950,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) coalesced_step_kernel(co
         Staging S{stg, kStageOut / Cfg::stage_bufs, Cfg::stage_bufs, 0u};
         uint32_t groups = 0;                     // bulk groups committed by etid 0 (tracked by all)
         int pend = -1, pend_age = 0;             // split item whose completion is deferred
+        StepView v{};
         auto complete_pending = [&]() {
-            const WorkItem pt = args.items[pend];
-            int32_t* counter = args.counters + pt.tile_slot;
+            const WorkItem pt = v.items[pend];
+            int32_t* counter = v.counters + pt.tile_slot;
             asm volatile("fence.acq_rel.gpu;" ::: "memory");   // this thread's reductions have landed
             named_bar_sync(1, 128);
             if (etid == 0) {
@@ -691,68 +971,120 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) coalesced_step_kernel(co
             const bool last = *split_flag != 0;
             named_bar_sync(1, 128);   // split_flag read by all before it can be rewritten
             if (last) {
-                groups += split_finalize(load_epi(args.probs + pt.problem), pt.row0, pt.col0,
-                                         args.ws + (int64_t)pt.ws_blk * kWsBlock, S, trow, etid);
+                groups += split_finalize(load_epi(v.probs + pt.problem), pt.row0, pt.col0,
+                                         v.ws + (int64_t)pt.ws_blk * kWsBlock, S, trow, etid);
                 if (args.trace && etid == 0) args.trace[8 * pend + 6] = global_timer_ns();
             }
             pend = -1;
         };
-        for (int i = beg; i < end; ++i) {
-            const WorkItem it = args.items[i];
-            const DevProblem* Pg = args.probs + it.problem;
-            if (args.trace && etid == 0 && it.type != kItemGemm) args.trace[8 * i + 0] = global_timer_ns();
-            if (it.type == kItemGemm) {
-                const EpiParams E = load_epi(Pg);
-                mbar_wait(&tfull[acc], acc_phase);
-                tc_fence_after();
-                if (args.trace && etid == 0) args.trace[8 * i + 2] = global_timer_ns();
-                const uint32_t taddr = tmem_base + ((uint32_t)(lgrp * 32) << 16) + (uint32_t)acc * kMaxBN;
-                const int nchunks = E.bn / 32;
-                const bool split = it.nsplit > 1;
-                if (args.dbg & 2) {   // experiment: no epilogue (bounds the load/MMA side)
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[acc]);
-                } else if (!split && E.tma_out && !(args.dbg & 8)) {
-                    groups += epilogue_staged(E, it.row0, it.col0, S, trow, etid, taddr, &tempty[acc],
-                                    args.trace ? args.trace + 8 * i : nullptr);
-                } else if (!split) {
-                    for (int c = 0; c < nchunks; ++c) {
-                        float v[32];
-                        tmem_ld32(taddr + (uint32_t)(c * 32), v);
-                        store_tile_chunk(E, it.row0, it.col0, trow, c, v);
-                    }
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[acc]);
-                } else {
-                    // split-K (planner only splits TMA-store problems): reduce now, complete later
-                    if (pend >= 0) complete_pending();   // at most one split in flight
-                    float* acc_tile = args.ws + (int64_t)it.ws_blk * kWsBlock;
-                    split_reduce(E, acc_tile, trow, taddr, &tempty[acc]);
-                    if (args.trace && etid == 0) args.trace[8 * i + 4] = global_timer_ns();
-                    pend = i;
-                    pend_age = 0;
+        // Resident accounting: a list counts into its step's done counter once its writes (generic
+        // and TMA stores) are complete. To keep the TMA-store round trip off the critical path it
+        // is deferred until the CTA finished its next list (then only the older list's store
+        // groups are waited for); at the end of a step (no more lists for this CTA) it is flushed,
+        // since a later step may wait for this one.
+        int64_t acct_k = -1;
+        uint32_t acct_groups = 0;
+        auto account = [&](int64_t kk, uint32_t newer_groups) {
+            named_bar_sync(1, 128);   // every epilogue thread's writes happen-before etid 0's release
+            if (etid == 0) {
+                bulk_wait_upto(newer_groups);   // TMA stores of that list have landed
+                fence_proxy_async_global();
+                uint32_t prev;
+                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                             : "=r"(prev) : "l"(&args.dq->done[kk % kQueue]) : "memory");
+                if (prev + 1 == gridDim.x * (uint32_t)(kk / kQueue + 1)) {   // step kk complete
+                    atomicMax(reinterpret_cast<unsigned long long*>(&args.dq->t_last),
+                              (unsigned long long)global_timer_ns());
+                    asm volatile("fence.acq_rel.sys;" ::: "memory");
+                    asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(&args.hdone[kk % kQueue]), "l"(kk + 1)
+                                 : "memory");
                 }
-                if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
-            } else if (it.type == kItemGemv) {
-                if (Pg->in_dt == GMX_ST_F32)
-                    gemv_rows<float>(Pg, it.row0, it.col0, ew);
-                else
-                    gemv_rows<__nv_bfloat16>(Pg, it.row0, it.col0, ew);
-            } else {
-                if (Pg->in_dt == GMX_ST_F32)
-                    eltwise_range<float>(Pg, it.row0, it.col0, etid, 128);
-                else
-                    eltwise_range<__nv_bfloat16>(Pg, it.row0, it.col0, etid, 128);
+                if (args.rtrace && kk < args.rtrace_steps)
+                    args.rtrace[(kk * gridDim.x + blockIdx.x) * 8 + 3] = global_timer_ns();
             }
-            if (args.trace) {
-                named_bar_sync(2, 128);
-                if (etid == 0) args.trace[8 * i + 3] = global_timer_ns();
+        };
+        for (bool first = true;; first = false) {
+            const Unit u = next_unit(first);   // every epilogue thread waits on the unit barrier
+            named_bar_sync(1, 128);            // all have read the unit
+            if (etid == 0) release_unit();
+            advance_unit();
+            if (u.idx < 0) {   // end of a step for this CTA, or stop: flush the pending count
+                if (acct_k >= 0) {
+                    account(acct_k, 0);
+                    acct_k = -1;
+                }
+                if (u.idx == kUnitStop) break;
+                continue;
             }
-            if (pend >= 0 && pend != i && ++pend_age >= 1) complete_pending();
+            v = list_view(args, u.k, u.idx);
+            uint64_t* rt = (args.rtrace && u.k < args.rtrace_steps) ? args.rtrace + (u.k * gridDim.x + blockIdx.x) * 8 : nullptr;
+            if (rt && etid == 0) {
+                rt[2] = global_timer_ns();
+                rt[4] = (uint64_t)(v.end - v.beg);
+            }
+            for (int i = v.beg; i < v.end; ++i) {
+                const WorkItem it = v.items[i];
+                const DevProblem* Pg = v.probs + it.problem;
+                if (args.trace && etid == 0 && it.type != kItemGemm) args.trace[8 * i + 0] = global_timer_ns();
+                if (it.type == kItemGemm) {
+                    const EpiParams E = load_epi(Pg);
+                    mbar_wait(&tfull[acc], acc_phase);
+                    tc_fence_after();
+                    if (args.trace && etid == 0) args.trace[8 * i + 2] = global_timer_ns();
+                    const uint32_t taddr = tmem_base + ((uint32_t)(lgrp * 32) << 16) + (uint32_t)acc * kMaxBN;
+                    const int nchunks = E.bn / 32;
+                    const bool split = it.nsplit > 1;
+                    if (args.dbg & 2) {   // experiment: no epilogue (bounds the load/MMA side)
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                    } else if (!split && E.tma_out && !(args.dbg & 8)) {
+                        groups += epilogue_staged(E, it.row0, it.col0, S, trow, etid, taddr, &tempty[acc],
+                                                  args.trace ? args.trace + 8 * i : nullptr);
+                    } else if (!split) {
+                        for (int c = 0; c < nchunks; ++c) {
+                            float vv[32];
+                            tmem_ld32(taddr + (uint32_t)(c * 32), vv);
+                            store_tile_chunk(E, it.row0, it.col0, trow, c, vv);
+                        }
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                    } else {
+                        // split-K (planner only splits TMA-store problems): reduce now, complete later
+                        if (pend >= 0) complete_pending();   // at most one split in flight
+                        float* acc_tile = v.ws + (int64_t)it.ws_blk * kWsBlock;
+                        split_reduce(E, acc_tile, trow, taddr, &tempty[acc]);
+                        if (args.trace && etid == 0) args.trace[8 * i + 4] = global_timer_ns();
+                        pend = i;
+                        pend_age = 0;
+                    }
+                    if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
+                } else if (it.type == kItemGemv) {
+                    if (Pg->in_dt == GMX_ST_F32)
+                        gemv_rows<float>(Pg, it.row0, it.col0, ew);
+                    else
+                        gemv_rows<__nv_bfloat16>(Pg, it.row0, it.col0, ew);
+                } else {
+                    if (Pg->in_dt == GMX_ST_F32)
+                        eltwise_range<float>(Pg, it.row0, it.col0, etid, 128);
+                    else
+                        eltwise_range<__nv_bfloat16>(Pg, it.row0, it.col0, etid, 128);
+                }
+                if (args.trace) {
+                    named_bar_sync(2, 128);
+                    if (etid == 0) args.trace[8 * i + 3] = global_timer_ns();
+                }
+                if (pend >= 0 && pend != i && ++pend_age >= 1) complete_pending();
+            }
+            if (pend >= 0) complete_pending();
+            if (rt && etid == 0) rt[7] = global_timer_ns();
+            if (args.resident) {
+                if (acct_k >= 0) account(acct_k, groups - acct_groups);   // the previous list
+                acct_k = u.k;
+                acct_groups = groups;
+            }
         }
-        if (pend >= 0) complete_pending();
         // TMA stores must have read their smem before the CTA exits; their global writes
         // complete with the grid (a dependent launch's griddepcontrol.wait covers them)
         if (etid == 0) bulk_wait_read0();
@@ -870,25 +1202,67 @@ struct gmx_exec {
     int32_t* counters = nullptr;
     int32_t counters_cap = 0;
     int64_t max_split = 32;
-    int64_t split_pct = 100;     // split a tile into pieces of about this % of the per-CTA share
-    int ctas_per_sm = 2;         // 1 or 2 resident CTAs of the coalesced kernel per SM
+    int64_t split_pct = 400;     // split a tile into pieces of about this % of the per-CTA share
+    int ctas_per_sm = 1;         // 1, or 2 CTAs of the coalesced kernel per SM (the latter runs as 2 waves)
     bool cache_plans = true;
     bool attr_set = false;
     bool tracing = false;
     bool pdl = true;
     bool early_trigger = true;
     bool multi_stream = false;   // launches may come from several streams (realtime runtime)
+    int occupancy[2] = {0, 0};   // measured resident CTAs/SM of the 1- and 2-CTA kernel shapes
     int32_t dbg = 0;
     const gmx::Plan* recent[3] = {nullptr, nullptr, nullptr};   // plans of the last launches
     uint64_t* trace = nullptr;
     int64_t trace_cap = 0;
     int64_t trace_items = 0;
+    // resident (persistent) mode
+    struct Resident {
+        bool active = false;
+        cudaStream_t stream = nullptr;        // stream of the persistent launch
+        cudaStream_t upload = nullptr;        // non-blocking stream for plan/table uploads
+        gmx::StepDesc* hring = nullptr;       // pinned, device-mapped
+        int64_t* hpub = nullptr;              // pinned, device-mapped: [0] published count
+        int64_t* hdone = nullptr;             // pinned, device-mapped: [kQueue] seq + 1 per slot
+        gmx::StepDesc* hring_d = nullptr;     // device aliases of the three above
+        int64_t* hpub_d = nullptr;
+        int64_t* hdone_d = nullptr;
+        gmx::DevQueue* dq = nullptr;
+        int64_t seq = 0;                      // steps enqueued in this residency
+        int grid = 0;
+        std::vector<std::vector<int32_t>> recent_keys;   // slot sets of the last kWindow steps
+        std::vector<const gmx::Plan*> recent_plans;
+        std::vector<int64_t> recent_seq;
+        std::vector<void*> graveyard;          // device tables retired during residency
+        std::vector<uint8_t> zeros;            // host zeros for copy-engine clears while resident
+        int window = 10;                       // max steps a CTA may run ahead (option "resident_window")
+        int64_t relay_ns = 0;                  // last residency: release -> last relay (diagnostic)
+        int32_t rtrace_steps = 0;              // option "rtrace": stamp this many steps
+        uint64_t* rtrace = nullptr;
+    } res;
 };
 
 namespace gmx {
 
 static int ensure_table(gmx_exec* ex, cudaStream_t stream) {
     if (!ex->table_dirty) return GMX_OK;
+    std::vector<DevProblem> host(ex->probs.size());
+    for (size_t i = 0; i < host.size(); ++i) host[i] = ex->probs[i].dev;
+    if (ex->res.active) {
+        // the persistent kernel may still read the current table through queued steps: write a
+        // fresh copy (upload stream, waited here) and retire the old one until residency ends
+        const size_t cap = std::max<size_t>(64, ex->probs.size());
+        DevProblem* fresh = nullptr;
+        GMX_CUDA(cudaMallocAsync(&fresh, cap * sizeof(DevProblem), ex->res.upload));
+        GMX_CUDA(cudaMemcpyAsync(fresh, host.data(), host.size() * sizeof(DevProblem), cudaMemcpyHostToDevice,
+                                 ex->res.upload));
+        GMX_CUDA(cudaStreamSynchronize(ex->res.upload));
+        if (ex->d_probs) ex->res.graveyard.push_back(ex->d_probs);
+        ex->d_probs = fresh;
+        ex->d_cap = cap;
+        ex->table_dirty = false;
+        return GMX_OK;
+    }
     if (ex->probs.size() > ex->d_cap) {
         size_t cap = std::max<size_t>(64, ex->d_cap);
         while (cap < ex->probs.size()) cap *= 2;
@@ -896,8 +1270,6 @@ static int ensure_table(gmx_exec* ex, cudaStream_t stream) {
         GMX_CUDA(cudaMalloc(&ex->d_probs, cap * sizeof(DevProblem)));
         ex->d_cap = cap;
     }
-    std::vector<DevProblem> host(ex->probs.size());
-    for (size_t i = 0; i < host.size(); ++i) host[i] = ex->probs[i].dev;
     GMX_CUDA(cudaMemcpy(ex->d_probs, host.data(), host.size() * sizeof(DevProblem), cudaMemcpyHostToDevice));
     ex->table_dirty = false;
     (void)stream;
@@ -1065,7 +1437,6 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
 // Split-K state is owned by the plan, so steps of different plans that overlap under PDL never
 // share accumulators; a plan launched again while a recent launch of it may still run waits.
 static int upload_plan(gmx_exec* ex, Plan& plan, cudaStream_t stream) {
-    (void)ex;
     if (plan.uploaded) return GMX_OK;
     const size_t items_bytes = std::max<size_t>(1, plan.items.size()) * sizeof(WorkItem);
     const size_t off_bytes = plan.cta_off.size() * sizeof(int32_t);
@@ -1080,7 +1451,14 @@ static int upload_plan(gmx_exec* ex, Plan& plan, cudaStream_t stream) {
         const size_t ws_bytes = (size_t)plan.ws_floats * sizeof(float);
         const size_t state = ws_bytes + (size_t)std::max(1, 2 * plan.n_counters) * sizeof(int32_t);
         GMX_CUDA(cudaMallocAsync(&plan.d_state, state, stream));
-        GMX_CUDA(cudaMemsetAsync(plan.d_state, 0, state, stream));
+        if (ex->res.active) {
+            // a memset KERNEL could not get an SM while the persistent kernel holds them all:
+            // zero through the copy engine instead
+            ex->res.zeros.resize(std::max(ex->res.zeros.size(), state));
+            GMX_CUDA(cudaMemcpyAsync(plan.d_state, ex->res.zeros.data(), state, cudaMemcpyHostToDevice, stream));
+        } else {
+            GMX_CUDA(cudaMemsetAsync(plan.d_state, 0, state, stream));
+        }
         plan.d_ws = reinterpret_cast<float*>(plan.d_state);
         plan.d_counters = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(plan.d_state) + ws_bytes);
     }
@@ -1116,9 +1494,256 @@ static void evict_plans(gmx_exec* ex) {
 
 }  // namespace gmx
 
+namespace gmx {
+
+static int set_kernel_attrs(gmx_exec* ex) {
+    if (ex->attr_set) return GMX_OK;
+    // maximum shared-memory carveout, so two 2-CTA/SM blocks really fit one SM
+    GMX_CUDA(cudaFuncSetAttribute(coalesced_step_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<1>()));
+    GMX_CUDA(cudaFuncSetAttribute(coalesced_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<2>()));
+    GMX_CUDA(cudaFuncSetAttribute(coalesced_step_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    GMX_CUDA(cudaFuncSetAttribute(coalesced_step_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int occ1 = 0, occ2 = 0;
+    GMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, coalesced_step_kernel<1>, kThreads, smem_bytes<1>()));
+    GMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, coalesced_step_kernel<2>, kThreads, smem_bytes<2>()));
+    ex->occupancy[0] = occ1;
+    ex->occupancy[1] = occ2;
+    // tcgen05.alloc users are placed one CTA per SM by the runtime (occupancy reports 1 for both
+    // shapes), so the 2-CTA shape runs as extra waves, and resident mode uses the 1-CTA shape
+    if (occ1 < 1) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, coalesced_step_kernel<2>);
+        int smem_sm = 0, smem_blk = 0, regs_sm = 0, resv = 0;
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ex->device);
+        cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, ex->device);
+        cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, ex->device);
+        cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, ex->device);
+        return fail(GMX_ECUDA, "occupancy: 1-CTA shape " + std::to_string(occ1) + "/SM, 2-CTA shape " +
+                                   std::to_string(occ2) + "/SM (need 1 and 2); regs " + std::to_string(fa.numRegs) +
+                                   " static smem " + std::to_string(fa.sharedSizeBytes) + " dyn " +
+                                   std::to_string(smem_bytes<2>()) + " smem/SM " + std::to_string(smem_sm) +
+                                   " optin/blk " + std::to_string(smem_blk) + " reserved/blk " + std::to_string(resv) +
+                                   " regs/SM " + std::to_string(regs_sm));
+    }
+    ex->attr_set = true;
+    return GMX_OK;
+}
+
+static bool keys_intersect(const std::vector<int32_t>& a, const std::vector<int32_t>& b) {
+    size_t i = 0, j = 0;
+    while (i < a.size() && j < b.size()) {
+        if (a[i] == b[j]) return true;
+        if (a[i] < b[j]) ++i; else ++j;
+    }
+    return false;
+}
+
+// Spin until host ring slot `slot` is free again (its previous step completed on the device).
+static int wait_slot_free(gmx_exec* ex, int64_t seq) {
+    auto& r = ex->res;
+    if (seq < kQueue) return GMX_OK;
+    const int64_t need = seq - kQueue + 1;
+    volatile int64_t* d = r.hdone + (seq % kQueue);
+    for (uint64_t spins = 0; *d < need; ++spins) {
+        if ((spins & 1023) == 1023) {
+            const cudaError_t e = cudaStreamQuery(r.stream);
+            if (e != cudaErrorNotReady && e != cudaSuccess) return fail(GMX_ECUDA, std::string("resident kernel: ") + cudaGetErrorString(e));
+            if (e == cudaSuccess && *d < need) return fail(GMX_ESTATE, "resident kernel exited early");
+        }
+    }
+    return GMX_OK;
+}
+
+static int publish_step(gmx_exec* ex, const StepDesc& d) {
+    auto& r = ex->res;
+    int rc;
+    if ((rc = wait_slot_free(ex, r.seq))) return rc;
+    StepDesc* slot = r.hring + (r.seq % kQueue);
+    std::memcpy(slot, &d, sizeof d);
+    __atomic_store_n(r.hpub, r.seq + 1, __ATOMIC_RELEASE);   // x86: ordered after the entry
+    ++r.seq;
+    return GMX_OK;
+}
+
+// Resident mode: the step goes to the persistent kernel's queue instead of a launch.
+static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>& key, int32_t flags, bool cached) {
+    auto& r = ex->res;
+    int rc;
+    if (!plan->uploaded) {
+        if ((rc = upload_plan(ex, *plan, r.upload))) return rc;
+        GMX_CUDA(cudaStreamSynchronize(r.upload));
+    }
+    plan->stream = r.stream;   // later frees are ordered after the persistent kernel
+    plan->last_use = ++ex->clock;
+    // wait for every earlier step if a member depends on earlier outputs, or this step reuses
+    // a plan (split-K state) or a slot (outputs) of a step that may still be running
+    const bool wait_all = (flags & GMX_LAUNCH_INDEPENDENT) == 0;
+    int64_t wait_step = -1;   // latest step inside the window sharing the plan or a slot
+    for (size_t i = 0; i < r.recent_keys.size(); ++i)
+        if (r.recent_plans[i] == plan || keys_intersect(r.recent_keys[i], key)) {
+            wait_step = r.recent_seq[i];
+            break;
+        }
+    StepDesc d{};
+    d.probs = ex->d_probs;
+    d.items = plan->d_items;
+    d.cta_off = plan->d_off;
+    d.ws = plan->d_ws;
+    d.counters = plan->d_counters;
+    d.grid = plan->stats.grid;
+    d.wait_all = wait_all ? 1 : 0;
+    d.wait_step = wait_step;
+    if (d.grid > r.grid) return fail(GMX_ESTATE, "plan grid exceeds the resident grid");
+    if ((rc = publish_step(ex, d))) return rc;
+    r.recent_keys.insert(r.recent_keys.begin(), key);
+    r.recent_plans.insert(r.recent_plans.begin(), plan);
+    r.recent_seq.insert(r.recent_seq.begin(), r.seq - 1);
+    if ((int)r.recent_keys.size() > r.window) {
+        r.recent_keys.pop_back();
+        r.recent_plans.pop_back();
+        r.recent_seq.pop_back();
+    }
+    plan->stats.cached = cached;
+    ex->last = plan;
+    return GMX_OK;
+}
+
+}  // namespace gmx
+
 using namespace gmx;
 
 extern "C" {
+
+int gmx_exec_resident_begin(gmx_exec* ex, void* stream_ptr) { return gmx_exec_resident_begin_ex(ex, stream_ptr, 0); }
+
+int gmx_exec_resident_begin_ex(gmx_exec* ex, void* stream_ptr, int32_t hold) {
+    if (!ex) return fail(GMX_EINVAL, "null argument");
+    auto& r = ex->res;
+    if (r.active) return fail(GMX_ESTATE, "already resident");
+    if (ex->tracing) return fail(GMX_ESTATE, "tracing is not supported in resident mode");
+    if (!ex->cache_plans) return fail(GMX_ESTATE, "resident mode needs cache_plans");
+    if (ex->ctas_per_sm != 1) return fail(GMX_ESTATE, "resident mode needs ctas_per_sm = 1 (all CTAs co-resident)");
+    if (!r.hring) {
+        GMX_CUDA(cudaHostAlloc(&r.hring, kQueue * sizeof(StepDesc), cudaHostAllocMapped));
+        GMX_CUDA(cudaHostAlloc(&r.hpub, 64, cudaHostAllocMapped));
+        GMX_CUDA(cudaHostAlloc(&r.hdone, kQueue * sizeof(int64_t), cudaHostAllocMapped));
+        GMX_CUDA(cudaHostGetDevicePointer((void**)&r.hring_d, r.hring, 0));
+        GMX_CUDA(cudaHostGetDevicePointer((void**)&r.hpub_d, r.hpub, 0));
+        GMX_CUDA(cudaHostGetDevicePointer((void**)&r.hdone_d, r.hdone, 0));
+        GMX_CUDA(cudaMalloc(&r.dq, sizeof(DevQueue)));
+        GMX_CUDA(cudaStreamCreateWithFlags(&r.upload, cudaStreamNonBlocking));
+    }
+    cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
+    int rc;
+    if ((rc = ensure_table(ex, stream))) return rc;
+    std::memset(r.hring, 0, kQueue * sizeof(StepDesc));
+    std::memset(r.hdone, 0, kQueue * sizeof(int64_t));
+    __atomic_store_n(r.hpub, (int64_t)0, __ATOMIC_RELEASE);
+    __atomic_store_n(r.hpub + 1, (int64_t)(hold ? 0 : 1), __ATOMIC_RELEASE);   // go flag
+    GMX_CUDA(cudaMemsetAsync(r.dq, 0, sizeof(DevQueue), stream));
+    if ((rc = set_kernel_attrs(ex))) return rc;
+    r.grid = ex->num_sms * ex->ctas_per_sm;
+    r.seq = 0;
+    r.stream = stream;
+    r.recent_keys.clear();
+    r.recent_plans.clear();
+    r.recent_seq.clear();
+    KernelArgs args{};
+    args.dbg = ex->dbg;
+    args.independent = 1;
+    args.early_trigger = 0;
+    args.resident = 1;
+    args.dq = r.dq;
+    args.hring = r.hring_d;
+    args.hpub = r.hpub_d;
+    args.hdone = r.hdone_d;
+    args.window = r.window;
+    if (r.rtrace_steps > 0) {
+        if (!r.rtrace) GMX_CUDA(cudaMalloc(&r.rtrace, (size_t)r.rtrace_steps * r.grid * 8 * sizeof(uint64_t)));
+        GMX_CUDA(cudaMemsetAsync(r.rtrace, 0, (size_t)r.rtrace_steps * r.grid * 8 * sizeof(uint64_t), stream));
+        args.rtrace = r.rtrace;
+        args.rtrace_steps = r.rtrace_steps;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(r.grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = ex->ctas_per_sm == 2 ? smem_bytes<2>() : smem_bytes<1>();
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident, or the launch fails
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (ex->ctas_per_sm == 2)
+        GMX_CUDA(cudaLaunchKernelEx(&cfg, coalesced_step_kernel<2>, args));
+    else
+        GMX_CUDA(cudaLaunchKernelEx(&cfg, coalesced_step_kernel<1>, args));
+    r.active = true;
+    return GMX_OK;
+}
+
+int gmx_exec_resident_release(gmx_exec* ex) {
+    if (!ex) return fail(GMX_EINVAL, "null argument");
+    if (!ex->res.hpub) return fail(GMX_ESTATE, "not resident");
+    __atomic_store_n(ex->res.hpub + 1, (int64_t)1, __ATOMIC_RELEASE);
+    return GMX_OK;
+}
+
+int gmx_exec_resident_device_ns(gmx_exec* ex, int64_t* out) {
+    if (!ex || !out) return fail(GMX_EINVAL, "null argument");
+    if (!ex->res.dq) return fail(GMX_ESTATE, "never resident");
+    uint64_t t[3];
+    GMX_CUDA(cudaMemcpy(t, &ex->res.dq->t_first, sizeof t, cudaMemcpyDeviceToHost));
+    *out = (int64_t)(t[1] - t[0]);
+    ex->res.relay_ns = (int64_t)(t[2] - t[0]);
+    return GMX_OK;
+}
+
+int gmx_exec_resident_read_rtrace(gmx_exec* ex, uint64_t* out, int64_t capacity, int32_t* grid) {
+    if (!ex || !grid) return fail(GMX_EINVAL, "null argument");
+    auto& r = ex->res;
+    *grid = r.grid;
+    const int64_t n = (int64_t)r.rtrace_steps * r.grid * 8;
+    if (!r.rtrace || capacity < n) return fail(GMX_EINVAL, "no rtrace or capacity too small");
+    GMX_CUDA(cudaDeviceSynchronize());
+    GMX_CUDA(cudaMemcpy(out, r.rtrace, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return GMX_OK;
+}
+
+int gmx_exec_resident_relay_ns(gmx_exec* ex, int64_t* out) {
+    if (!ex || !out) return fail(GMX_EINVAL, "null argument");
+    *out = ex->res.relay_ns;
+    return GMX_OK;
+}
+
+int gmx_exec_resident_end(gmx_exec* ex) {
+    if (!ex) return fail(GMX_EINVAL, "null argument");
+    auto& r = ex->res;
+    if (!r.active) return fail(GMX_ESTATE, "not resident");
+    __atomic_store_n(r.hpub + 1, (int64_t)1, __ATOMIC_RELEASE);   // a held start is released
+    StepDesc d{};
+    d.stop = 1;
+    d.wait_step = -1;
+    int rc = publish_step(ex, d);
+    r.active = false;
+    for (void* p : r.graveyard) cudaFreeAsync(p, r.stream);   // after the persistent kernel
+    r.graveyard.clear();
+    return rc;
+}
+
+int gmx_exec_resident_completed(gmx_exec* ex, int64_t* out) {
+    if (!ex || !out) return fail(GMX_EINVAL, "null argument");
+    auto& r = ex->res;
+    // steps complete out of order; report the longest completed prefix
+    int64_t done = 0;
+    const int64_t lo = std::max<int64_t>(0, r.seq - kQueue);
+    done = lo;
+    for (int64_t q = lo; q < r.seq; ++q) {
+        if (((volatile int64_t*)r.hdone)[q % kQueue] >= q + 1) done = q + 1; else break;
+    }
+    *out = done;
+    return GMX_OK;
+}
 
 int gmx_exec_create(int32_t device, gmx_exec** out) {
     if (!out) return fail(GMX_EINVAL, "null argument");
@@ -1146,6 +1771,18 @@ int gmx_exec_create(int32_t device, gmx_exec** out) {
 void gmx_exec_destroy(gmx_exec* ex) {
     if (!ex) return;
     cudaSetDevice(ex->device);
+    if (ex->res.active) {
+        gmx_exec_resident_end(ex);
+        cudaStreamSynchronize(ex->res.stream);
+    }
+    if (ex->res.hring) {
+        cudaDeviceSynchronize();
+        cudaFreeHost(ex->res.hring);
+        cudaFreeHost(ex->res.hpub);
+        cudaFreeHost(ex->res.hdone);
+        cudaFree(ex->res.dq);
+        cudaStreamDestroy(ex->res.upload);
+    }
     ex->plans.clear();
     ex->uncached.reset();
     if (ex->d_probs) cudaFree(ex->d_probs);
@@ -1312,7 +1949,8 @@ int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stre
                 break;
             }
         if (!plan) {
-            if (ex->n_plans >= ex->plan_capacity) evict_plans(ex);
+            // no eviction while resident: queued steps may still reference any cached plan
+            if (ex->n_plans >= ex->plan_capacity && !ex->res.active) evict_plans(ex);
             auto p = std::make_unique<Plan>();
             if ((rc = build_plan(ex, key, *p))) return rc;
             p->key = key;
@@ -1321,23 +1959,19 @@ int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stre
             ++ex->n_plans;
         }
     } else {
+        if (ex->res.active) return fail(GMX_ESTATE, "resident mode needs cache_plans");
         ex->uncached = std::make_unique<Plan>();   // the previous one is freed stream-ordered
         if ((rc = build_plan(ex, key, *ex->uncached))) return rc;
         plan = ex->uncached.get();
     }
+    if (ex->res.active) return enqueue_resident(ex, plan, key, flags, cached);
     // multi-stream: a plan's split-K state and outputs must not be used by two launches at once
     if (ex->multi_stream && plan->done_ev && plan->stream != stream)
         GMX_CUDA(cudaStreamWaitEvent(stream, plan->done_ev, 0));
     if ((rc = upload_plan(ex, *plan, stream))) return rc;
     plan->stream = stream;
     plan->last_use = ++ex->clock;
-    if (!ex->attr_set) {
-        GMX_CUDA(cudaFuncSetAttribute(coalesced_step_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      smem_bytes<1>()));
-        GMX_CUDA(cudaFuncSetAttribute(coalesced_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      smem_bytes<2>()));
-        ex->attr_set = true;
-    }
+    if ((rc = set_kernel_attrs(ex))) return rc;
     if (ex->tracing && (int64_t)plan->items.size() > ex->trace_cap) {
         if (ex->trace) GMX_CUDA(cudaFree(ex->trace));
         ex->trace_cap = std::max<int64_t>(1024, (int64_t)plan->items.size());
@@ -1398,14 +2032,24 @@ int gmx_exec_clear_plans(gmx_exec* ex) {
 int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
     if (!ex || !name) return fail(GMX_EINVAL, "null argument");
     const std::string n(name);
+    if (ex->res.active) return fail(GMX_ESTATE, "options cannot change while resident");
     if (n == "max_split") {
         if (value < 1 || value > 255) return fail(GMX_EINVAL, "max_split must be in [1, 255]");
         ex->max_split = value;
+    } else if (n == "rtrace") {
+        if (value < 0 || value > 100000) return fail(GMX_EINVAL, "rtrace must be in [0, 100000]");
+        if (ex->res.rtrace) { cudaFree(ex->res.rtrace); ex->res.rtrace = nullptr; }
+        ex->res.rtrace_steps = (int32_t)value;
+        return GMX_OK;
+    } else if (n == "resident_window") {
+        if (value < 1 || value > kMaxWindow) return fail(GMX_EINVAL, "resident_window must be in [1, 16]");
+        ex->res.window = (int)value;
+        return GMX_OK;
     } else if (n == "ctas_per_sm") {
         if (value != 1 && value != 2) return fail(GMX_EINVAL, "ctas_per_sm must be 1 or 2");
         ex->ctas_per_sm = (int)value;
     } else if (n == "split_pct") {
-        if (value < 10 || value > 400) return fail(GMX_EINVAL, "split_pct must be in [10, 400]");
+        if (value < 10 || value > 2000) return fail(GMX_EINVAL, "split_pct must be in [10, 2000]");
         ex->split_pct = value;
     } else if (n == "cache_plans") {
         ex->cache_plans = value != 0;

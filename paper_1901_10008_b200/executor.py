@@ -55,6 +55,14 @@ EXEC_SIGNATURES = {
     "gmx_exec_last_plan": (C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
     "gmx_exec_clear_plans": (C.c_int, [C.c_void_p]),
     "gmx_exec_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
+    "gmx_exec_resident_begin": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gmx_exec_resident_end": (C.c_int, [C.c_void_p]),
+    "gmx_exec_resident_begin_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "gmx_exec_resident_release": (C.c_int, [C.c_void_p]),
+    "gmx_exec_resident_relay_ns": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "gmx_exec_resident_read_rtrace": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int32)]),
+    "gmx_exec_resident_device_ns": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "gmx_exec_resident_completed": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "gmx_exec_read_trace": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
                                       C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32),
                                       C.POINTER(C.c_int32)]),
@@ -211,6 +219,48 @@ class Executor:
         st = PlanStats()
         _check(self._lib.gmx_exec_last_plan(self._h, C.byref(st)))
         return {name: getattr(st, name) for name, _ in PlanStats._fields_ if name != "_pad"}
+
+    # ---- resident (persistent) mode --------------------------------------------------
+
+    def resident_begin(self, stream=None, hold=False):
+        """Launch the persistent coalesced kernel on `stream`; until resident_end(), every
+        launch() appends its step to the kernel's queue instead of launching (include/gmx_exec.h).
+        hold=True: nothing runs until resident_release() (device-only timing of a queued batch)."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(self._lib.gmx_exec_resident_begin_ex(self._h, C.c_void_p(s.cuda_stream), 1 if hold else 0))
+
+    def resident_release(self):
+        _check(self._lib.gmx_exec_resident_release(self._h))
+
+    def resident_device_ns(self) -> int:
+        """Device time (ns, %globaltimer) from the (released) start to the last step's completion."""
+        n = C.c_int64()
+        _check(self._lib.gmx_exec_resident_device_ns(self._h, C.byref(n)))
+        return n.value
+
+    def resident_end(self):
+        """Queue the stop step; work later on the resident stream is ordered after all steps."""
+        _check(self._lib.gmx_exec_resident_end(self._h))
+
+    def resident_completed(self) -> int:
+        """Number of queued steps (from the start of residency) that have fully completed."""
+        n = C.c_int64()
+        _check(self._lib.gmx_exec_resident_completed(self._h, C.byref(n)))
+        return n.value
+
+    def resident(self, stream=None):
+        """Context manager: `with ex.resident(stream): ...launches...`."""
+        ex = self
+
+        class _Ctx:
+            def __enter__(self):
+                ex.resident_begin(stream)
+                return ex
+
+            def __exit__(self, *exc):
+                ex.resident_end()
+                return False
+        return _Ctx()
 
     def set_option(self, name: str, value: int):
         _check(self._lib.gmx_exec_set_option(self._h, name.encode(), int(value)))

@@ -207,8 +207,8 @@ def test_c2_kernel_shapes_and_split_plans(ex, ctas_per_sm, split_pct):
         for s in slots:
             ex.unregister(s)
     finally:
-        ex.set_option("ctas_per_sm", 2)
-        ex.set_option("split_pct", 100)
+        ex.set_option("ctas_per_sm", 1)
+        ex.set_option("split_pct", 400)
 
 
 def test_independent_back_to_back_launches(ex):
@@ -223,6 +223,61 @@ def test_independent_back_to_back_launches(ex):
         for k in range(12):
             ex.launch(slots[k % 3], s, independent=True)
     s.synchronize()
+    for row in sets:
+        for o in row:
+            _check(o)
+    for row in slots:
+        for sl in row:
+            ex.unregister(sl)
+
+
+def test_resident_queue_matches_launches(ex):
+    """Resident mode: one persistent launch consumes a queue of steps (independent rotating
+    operand sets, a dependent step, a re-used plan inside the window); all results correct."""
+    from paper_1901_10008_b200.executor import OperandSet
+    sets = [[OperandSet("gemm", C2_SHAPES[(i + r) % 13], seed=500 + 16 * r + i,
+                        bias=(i % 2 == 0), activation="relu" if i % 3 == 0 else "none") for i in range(16)]
+            for r in range(3)]
+    sets.append([OperandSet("gemv", (1000, 2048), dtype="fp32", seed=600),
+                 OperandSet("elementwise", (50176,), seed=601, activation="gelu"),
+                 OperandSet("gemm", (512, 49, 4608), seed=602)])
+    slots = [[o.register(ex) for o in row] for row in sets]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for row in slots:   # warm the plans (built + uploaded outside residency as well)
+            ex.launch(row, s)
+        s.synchronize()
+        for row in sets:
+            for o in row:
+                o.c.zero_()
+        with ex.resident(s):
+            for k in range(40):
+                ex.launch(slots[k % 4], s, independent=(k % 5 != 0))
+            ex.launch(slots[0], s, independent=True)   # plan reuse inside the window
+            ex.launch(slots[0], s, independent=True)
+        s.synchronize()
+    assert ex.resident_completed() == 42
+    for row in sets:
+        for o in row:
+            _check(o)
+    for row in slots:
+        for sl in row:
+            ex.unregister(sl)
+
+
+def test_resident_many_steps_ring_wrap(ex):
+    """More steps than the 64-entry queue ring: slots are recycled only after completion."""
+    from paper_1901_10008_b200.executor import OperandSet
+    sets = [[OperandSet("gemm", C2_SHAPES[(3 * r + i) % 13], seed=700 + 4 * r + i) for i in range(4)]
+            for r in range(5)]
+    slots = [[o.register(ex) for o in row] for row in sets]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with ex.resident(s):
+            for k in range(300):
+                ex.launch(slots[k % 5], s, independent=True)
+        s.synchronize()
+    assert ex.resident_completed() == 300
     for row in sets:
         for o in row:
             _check(o)

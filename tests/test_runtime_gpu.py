@@ -20,7 +20,7 @@ from oracle import sim  # noqa: E402
 from .conftest import load_golden  # noqa: E402
 
 
-def _run_workload(workload, library, profile_name="b200", params=None, check_numerics=True):
+def _run_workload(workload, library, profile_name="b200", params=None, check_numerics=True, resident=False):
     import paper_1901_10008_b200 as gm
     from paper_1901_10008_b200.executor import Executor, OperandSet
     from paper_1901_10008_b200.runtime import Runtime
@@ -42,7 +42,15 @@ def _run_workload(workload, library, profile_name="b200", params=None, check_num
                                       tuple(gm.KernelSpec(k.kernel_id, k.stream_id, k.op_kind, k.dims, k.dtype,
                                                           k.deps, k.arrival, k.deadline) for k in r.kernels),
                                       r.arrival, gm.LatencyConstraint.batch()), slots)
-    stats = rt.run()
+    if resident:   # every scheduler step goes to ONE persistent launch's queue
+        s = torch.cuda.current_stream()
+        ex.resident_begin(s)
+        try:
+            stats = rt.run(stream=s)
+        finally:
+            ex.resident_end()
+    else:
+        stats = rt.run()
     torch.cuda.synchronize()
     got = dict(rt.drain_completions())
     # oracle: completion time per request from the restated reference engine
@@ -64,23 +72,25 @@ def _run_workload(workload, library, profile_name="b200", params=None, check_num
     return stats
 
 
-def test_runtime_c2_matches_oracle_engine():
+@pytest.mark.parametrize("resident", [False, True])
+def test_runtime_c2_matches_oracle_engine(resident):
     traces = load_golden("traces.json")
     wl = traces["workloads"]["c2_resnet50_16"]
     wl = dict(wl, streams=[dict(s, model_name="resnet50_like_fp16") for s in wl["streams"]])
     lib = dict(load_golden("models.json"))
     lib["resnet50_like_fp16"] = [dict(p, dtype="fp16") for p in lib["resnet50_like"]]
-    stats = _run_workload(wl, lib)
+    stats = _run_workload(wl, lib, resident=resident)
     assert stats["completed_requests"] == 16 and stats["launches"] >= 1
 
 
-def test_runtime_mixed_chains_match_oracle_engine():
+@pytest.mark.parametrize("resident", [False, True])
+def test_runtime_mixed_chains_match_oracle_engine(resident):
     lib = dict(load_golden("models.json"))
     wl = {"duration_ns": 2_000_000, "streams": [
         {"stream_id": f"m{i}", "model_name": m, "slo_ns": 10_000_000,
          "arrival": {"kind": "fixed", "schedule": [0, 150_000 * (i + 1)]}}
         for i, m in enumerate(["mixed_fp16", "tiny_chain", "resnet50_fc", "eltwise_fp32", "mixed_fp16"])]}
-    stats = _run_workload(wl, lib, params={"stagger_horizon": 50_000})
+    stats = _run_workload(wl, lib, params={"stagger_horizon": 50_000}, resident=resident)
     assert stats["completed_requests"] == 10
 
 

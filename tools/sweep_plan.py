@@ -10,7 +10,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-from bench import C2Bench, algorithmic_bytes, time_launch_only  # noqa: E402
+from bench import C2Bench, algorithmic_bytes, time_launch_only, time_resident  # noqa: E402
 
 grid = {}
 for arg in sys.argv[1:]:
@@ -21,16 +21,23 @@ if not grid:
 b = C2Bench(replicas=8)
 nbytes = algorithmic_bytes(b.shapes)
 merge = grid.pop("merge", [1])
+resident = grid.pop("resident", [0])
 base_slots = [list(s) for s in b.slots]
-for mg, combo in itertools.product(merge, itertools.product(*grid.values())):
+for rs, mg, combo in itertools.product(resident, merge, itertools.product(*grid.values())):
     opts = dict(zip(grid.keys(), combo))
     for k, v in opts.items():
         b.ex.set_option(k, v)
     # merge=M: one launch covers M replicas' steps (per-step cost = time / M)
     b.slots = [sum((base_slots[(j + q) % len(base_slots)] for q in range(mg)), []) for j in range(len(base_slots))]
-    t, plan = time_launch_only(b, 200)
+    t, plan = time_resident(b, 400) if rs else time_launch_only(b, 200)
     t /= mg
     opts["merge"] = mg
+    opts["resident"] = rs
+    if rs:
+        import ctypes as C
+        r = C.c_int64()
+        b.ex._lib.gmx_exec_resident_relay_ns(b.ex._h, C.byref(r))
+        opts["relay_us_per_step"] = round(r.value / 400 / 1e3, 3)
     print(json.dumps({"opts": opts, "kernel_us": round(t * 1e6, 3), "GBps": round(nbytes / t / 1e9, 1),
                       "n_items": plan["n_items"], "n_split_items": plan["n_split_items"],
                       "max_cta_cost": plan["max_cta_cost"], "mean_cta_cost": round(plan["mean_cta_cost"], 1)}),
