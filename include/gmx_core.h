@@ -218,6 +218,10 @@ int gmx_sched_add_request(gmx_sched* s, int64_t request_id, int32_t stream, int6
 int gmx_sched_step(gmx_sched* s, int64_t now, gmx_step_view* out);
 /* scheduler.py:210-235 complete; GMX_ENOTFOUND for an unknown dispatch id */
 int gmx_sched_complete(gmx_sched* s, int64_t dispatch_id, int64_t now, gmx_complete_view* out);
+/* Serving loops: drop finished requests from the scheduler's tables once they outnumber the
+ * live ones (decisions are unchanged; finished kernels can no longer be queried by id and kernel
+ * ids must not be reused). Off by default: the reference keeps everything (scheduler.py:150-163). */
+int gmx_sched_set_retire(gmx_sched* s, int32_t on);
 /* scheduler.py:256-278 evict_straggler */
 int gmx_sched_evict_stream(gmx_sched* s, int32_t stream, int64_t now, gmx_evict_view* out);
 /* scheduler.py:195-206 */

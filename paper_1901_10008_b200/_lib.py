@@ -109,6 +109,7 @@ CORE_SIGNATURES = {
                                         P(i32), P(i64), P(i32)]),
     "gmx_sched_step": (C.c_int, [C.c_void_p, i64, P(StepView)]),
     "gmx_sched_complete": (C.c_int, [C.c_void_p, i64, i64, P(CompleteView)]),
+    "gmx_sched_set_retire": (C.c_int, [C.c_void_p, i32]),
     "gmx_sched_evict_stream": (C.c_int, [C.c_void_p, i32, i64, P(EvictView)]),
     "gmx_sched_predicted_remaining": (C.c_int, [C.c_void_p, i64, P(i64)]),
     "gmx_sched_kernel_slack": (C.c_int, [C.c_void_p, i64, i64, P(i64)]),

@@ -76,6 +76,11 @@ class IdMap {
     }
 
     size_t size() const { return size_; }
+    void clear() {
+        slots_.assign(64, Slot{0, 0, 0});
+        mask_ = 63;
+        size_ = 0;
+    }
 
    private:
     struct Slot {           // key, value and occupancy in one 16-byte entry (one cache line probe)
@@ -119,6 +124,34 @@ class SigSet {
         slots_[i] = e;
         ++count_;
         return true;
+    }
+
+    size_t size() const { return count_; }
+
+    // Keep only the signatures for which keep(ids, n) is true (rebuilds the table).
+    template <typename F>
+    void retain(F keep) {
+        std::vector<uint64_t> h2;
+        std::vector<int64_t> off2, arena2;
+        for (int32_t e = 0; e < (int32_t)hashes_.size(); ++e) {
+            const int64_t* p = arena_.data() + offsets_[e];
+            if (!keep(p + 1, (int32_t)p[0])) continue;
+            h2.push_back(hashes_[e]);
+            off2.push_back((int64_t)arena2.size());
+            arena2.insert(arena2.end(), p, p + 1 + p[0]);
+        }
+        hashes_.swap(h2);
+        offsets_.swap(off2);
+        arena_.swap(arena2);
+        count_ = hashes_.size();
+        size_t cap = 256;
+        while (cap < 2 * (count_ + 1)) cap *= 2;
+        slots_.assign(cap, -1);
+        for (int32_t e = 0; e < (int32_t)hashes_.size(); ++e) {
+            size_t i = hashes_[e] & (slots_.size() - 1);
+            while (slots_[i] >= 0) i = (i + 1) & (slots_.size() - 1);
+            slots_[i] = e;
+        }
     }
 
    private:

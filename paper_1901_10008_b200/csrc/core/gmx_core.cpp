@@ -420,6 +420,10 @@ struct gmx_sched {
     std::string last_ctx;
     int32_t rr_last = -1;
     gmx::SigSet withheld_sigs;
+    // retire mode (serving loops): finished requests are dropped from the tables once they
+    // outnumber the live ones, so a long-running scheduler's state stays small and cache-resident
+    bool retire = false;
+    int64_t n_finished = 0;
 
     // view storage
     std::vector<gmx_dispatch_rec> v_disp;
@@ -846,6 +850,53 @@ static void unlock_dependents(S* s, int64_t done_id, const RequestRec& r, std::v
     }
 }
 
+// Retire mode: drop finished requests (and their kernels, dependency lists, id-map entries and
+// the withheld signatures that can no longer recur), renumbering kernel/request slots in
+// ready, in-flight dispatches and the id map. Decisions only ever read live state (ready,
+// blocked and in-flight kernels of unfinished requests), so they are unchanged; what changes is
+// that finished kernels can no longer be queried by id and kernel ids must not be reused.
+static void compact(S* s) {
+    std::vector<int32_t> kmap(s->kernels.size(), -1);
+    std::vector<KernelRec> nk;
+    std::vector<RequestRec> nr;
+    std::vector<int64_t> nd;
+    nk.reserve(s->kernels.size() / 2 + 16);
+    for (const RequestRec& r0 : s->requests) {
+        if (r0.finished) continue;
+        RequestRec r = r0;
+        r.first = (int32_t)nk.size();
+        const int32_t rslot = (int32_t)nr.size();
+        for (int32_t slot = r0.first; slot < r0.first + r0.count; ++slot) {
+            KernelRec k = s->kernels[slot];
+            kmap[slot] = (int32_t)nk.size();
+            k.req = rslot;
+            const int32_t off = (int32_t)nd.size();
+            nd.insert(nd.end(), s->dep_arena.begin() + k.dep_off, s->dep_arena.begin() + k.dep_off + k.dep_n);
+            k.dep_off = off;
+            nk.push_back(k);
+        }
+        nr.push_back(r);
+    }
+    for (int32_t& slot : s->ready) slot = kmap[slot];
+    for (DispatchRec& d : s->pool)
+        if (d.live)
+            for (int32_t& slot : d.kernels) slot = kmap[slot];
+    s->kernel_slot.clear();
+    for (int32_t i = 0; i < (int32_t)nk.size(); ++i) s->kernel_slot.put(nk[i].id, i);
+    s->kernels.swap(nk);
+    s->requests.swap(nr);
+    s->dep_arena.swap(nd);
+    // a withheld member set can only recur while all its kernels are still waiting
+    s->withheld_sigs.retain([s](const int64_t* ids, int32_t n) {
+        for (int32_t i = 0; i < n; ++i) {
+            const int32_t slot = s->kernel_slot.find(ids[i]);
+            if (slot < 0 || s->kernels[slot].done) return false;
+        }
+        return true;
+    });
+    ++s->ready_version;   // the clustering cache holds kernel slots
+}
+
 }  // namespace gmx
 
 // ======================================================================= ABI
@@ -1158,6 +1209,7 @@ int gmx_sched_complete(gmx_sched* s, int64_t did, int64_t now, gmx_complete_view
         if (first && r.remaining > 0) --r.remaining;
         if (r.remaining == 0 && !r.finished) {
             r.finished = true;
+            ++s->n_finished;
             s->v_ids_b.push_back(r.id);
         }
         unlock_dependents(s, k.id, r, s->v_ids_c);
@@ -1170,6 +1222,16 @@ int gmx_sched_complete(gmx_sched* s, int64_t did, int64_t now, gmx_complete_view
     out->n_unlocked = (int32_t)s->v_ids_c.size();
     out->unlocked_kernel_ids = s->v_ids_c.data();
     release_dispatch(s, pi);
+    if (s->retire && s->n_finished >= 256 && 2 * s->n_finished >= (int64_t)s->requests.size()) {
+        compact(s);
+        s->n_finished = 0;
+    }
+    return GMX_OK;
+}
+
+int gmx_sched_set_retire(gmx_sched* s, int32_t on) {
+    if (!s) return fail(GMX_EINVAL, "null argument");
+    s->retire = on != 0;
     return GMX_OK;
 }
 

@@ -78,6 +78,7 @@ struct gmx_runtime {
     };
     std::deque<InFlight> inflight;
     std::vector<cudaStream_t> streams;   // realtime: launches round-robin over these
+    int64_t prof_ns[4] = {0, 0, 0, 0};   // host time in add_request / step / complete / launch
     size_t next_stream = 0;
     std::vector<cudaEvent_t> event_pool;
     std::vector<gmx_replay_rec> log;
@@ -155,6 +156,12 @@ int gmx_runtime_set_origin(gmx_runtime* rt, int64_t ns) {
     return GMX_OK;
 }
 
+int gmx_runtime_host_profile(const gmx_runtime* rt, int64_t* out4) {
+    if (!rt || !out4) return fail(GMX_EINVAL, "null argument");
+    for (int i = 0; i < 4; ++i) out4[i] = rt->prof_ns[i];
+    return GMX_OK;
+}
+
 int64_t gmx_runtime_clock_ns(const gmx_runtime* rt) {
     if (!rt || !rt->origin_set) return 0;
     return steady_ns() - rt->origin_ns;
@@ -222,9 +229,11 @@ static int on_arrival(gmx_runtime* rt, int64_t rid) {
     rt->pred.resize((size_t)std::max(1, p.n));
     const int32_t dep_base = rt->off_arena[p.d_off + p.n + 1];
     int32_t accepted = 0;
+    const int64_t t_add = steady_ns();
     int rc = gmx_sched_add_request(rt->sched, rid, p.stream, p.arrival, rt->k_arena.data() + p.k_off, p.n,
                                    rt->dep_arena.data() + dep_base, rt->off_arena.data() + p.d_off,
                                    rt->pred.data(), &accepted);
+    rt->prof_ns[0] += steady_ns() - t_add;
     if (rc) return fail(rc, std::string("add_request: ") + gmx_last_error());
     if (!accepted) release_request(rt, rid);
     return GMX_OK;
@@ -234,7 +243,9 @@ static int on_arrival(gmx_runtime* rt, int64_t rid) {
 // dispatch ids of the launch are returned in `ids` (completion is observed, not scheduled).
 static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool realtime, std::vector<int64_t>* ids) {
     gmx_step_view v;
+    const int64_t t_step = steady_ns();
     int rc = gmx_sched_step(rt->sched, now, &v);
+    rt->prof_ns[1] += steady_ns() - t_step;
     if (rc) return fail(rc, std::string("step: ") + gmx_last_error());
     ++rt->st.steps;
     rt->st.withheld += v.n_withheld;
@@ -273,8 +284,10 @@ static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool real
             rt->st.useful_flops += r.useful_flops;
             rt->st.kernels += r.n_kernels;
         }
+        const int64_t t_l = steady_ns();
         rc = gmx_exec_launch_ex(rt->ex, rt->launch_slots.data(), (int32_t)rt->launch_slots.size(), stream,
                                 independent ? GMX_LAUNCH_INDEPENDENT : 0);
+        rt->prof_ns[3] += steady_ns() - t_l;
         if (rc) return fail(rc, std::string("launch: ") + gmx_exec_last_error());
         ++rt->st.launches;
         rt->st.dispatches += v.n_dispatches;
@@ -368,7 +381,9 @@ int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* stream, gmx_runtime_st
             rt->heap.pop();
             if (e.kind == kComplete) {
                 gmx_complete_view cv;
+                const int64_t t_c = steady_ns();
                 int rc = gmx_sched_complete(rt->sched, e.id, now, &cv);
+                rt->prof_ns[2] += steady_ns() - t_c;
                 if (rc) return fail(rc, std::string("complete: ") + gmx_last_error());
                 on_finished(rt, cv, now);
             } else if (e.kind == kArrival) {

@@ -50,6 +50,7 @@ RT_SIGNATURES = {
     "gmx_runtime_set_origin": (C.c_int, [C.c_void_p, C.c_int64]),
     "gmx_runtime_set_streams": (C.c_int, [C.c_void_p, C.c_int32]),
     "gmx_runtime_clock_ns": (C.c_int64, [C.c_void_p]),
+    "gmx_runtime_host_profile": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "gmx_runtime_replay_log": (C.c_int, [C.c_void_p, C.POINTER(ReplayRec), C.c_int64,
                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_int64,
                                          C.POINTER(C.c_int64)]),
@@ -82,7 +83,8 @@ class Runtime:
     gpumux.engine.run); mode="realtime": wall clock, completions observed from CUDA events,
     every step logged for replay parity (`replay_log`)."""
 
-    def __init__(self, executor, profile, policy, tuning_table=None, jitter_state=0, mode="lockstep"):
+    def __init__(self, executor, profile, policy, tuning_table=None, jitter_state=0, mode="lockstep",
+                 retire=True):
         self.ex = executor
         core = _lib.core()
         p = policy.params
@@ -99,6 +101,9 @@ class Runtime:
                                          float(model["footprint_slope"]), int(jitter_state),
                                          C.byref(h)))
         self._sched = h
+        # the serving loop never queries finished requests: let the core retire them so its
+        # tables stay small over long runs (decisions are unchanged)
+        _lib.check(core.gmx_sched_set_retire(h, 1 if retire else 0))
         rt = C.c_void_p()
         _check(_rt_lib().gmx_runtime_create(h, executor._h, MODES[mode], C.byref(rt)))
         self.mode = mode
@@ -152,6 +157,12 @@ class Runtime:
         _check(_rt_lib().gmx_runtime_run(self._rt, int(until), C.c_void_p(s.cuda_stream),
                                          C.byref(self._stats)))
         return {n: getattr(self._stats, n) for n, _ in RuntimeStats._fields_}
+
+    def host_profile(self) -> dict:
+        """Cumulative host ns in the decision core (add/step/complete) and the launch path."""
+        arr = (C.c_int64 * 4)()
+        _check(_rt_lib().gmx_runtime_host_profile(self._rt, arr))
+        return dict(zip(("add_request", "step", "complete", "launch"), list(arr)))
 
     def set_streams(self, n: int):
         """Realtime mode: launch over n runtime-owned CUDA streams (small steps co-run)."""

@@ -17,6 +17,7 @@ int main(int argc, char** argv) {
     gmx_policy_params pp = {0.25, 0.5, 2.0, 32, 8, 0.15, 10000, 0.0};
     gmx_sched* s;
     if (gmx_sched_create(&p, GMX_POLICY_OOO, &pp, NULL, 0.6, 0.4, 0, &s)) return 1;
+    if (argc > 3) gmx_sched_set_retire(s, atoi(argv[3]));
     int32_t codes[1024];
     char name[32];
     for (int i = 0; i < tenants; ++i) { snprintf(name, sizeof name, "t%03d", i); gmx_sched_intern_stream(s, name, &codes[i]); }
