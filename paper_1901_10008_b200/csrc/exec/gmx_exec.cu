@@ -1202,7 +1202,7 @@ struct gmx_exec {
     int32_t* counters = nullptr;
     int32_t counters_cap = 0;
     int64_t max_split = 32;
-    int64_t split_pct = 400;     // split a tile into pieces of about this % of the per-CTA share
+    int64_t split_pct = 250;     // split a tile into pieces of about this % of the per-CTA share
     int ctas_per_sm = 1;         // 1, or 2 CTAs of the coalesced kernel per SM (the latter runs as 2 waves)
     bool cache_plans = true;
     bool attr_set = false;
