@@ -581,10 +581,13 @@ __device__ __forceinline__ float dot_v4(uint4 w, uint4 x, __nv_bfloat16) {
            bf_lo(w.z) * bf_lo(x.z) + bf_hi(w.z) * bf_hi(x.z) + bf_lo(w.w) * bf_lo(x.w) + bf_hi(w.w) * bf_hi(x.w);
 }
 
-// y[r] for r in [r0, r1): each epilogue warp owns every 4th row; 16-byte streaming loads of W
-// with 4 outstanding per lane, x re-read through L1.
+// y[r] for r in [r0, r1): each epilogue warp owns every 4th row and works on kRowsPerWarp of
+// its rows at once, so every lane keeps kRowsPerWarp x 4 sixteen-byte non-allocating loads of W
+// in flight (8 KB per warp, 32 KB per SM): a batch-1 GEMV is a pure HBM stream and only enough
+// bytes in flight reach the bandwidth. x is re-read through L1.
 template <typename T>
 __device__ void gemv_rows(const DevProblem* Pg, int r0, int r1, int ew) {
+    constexpr int kRowsPerWarp = 4;
     const T* __restrict__ W = reinterpret_cast<const T*>(Pg->in0);
     const T* __restrict__ x = reinterpret_cast<const T*>(Pg->in1);
     const int n = Pg->cols;
@@ -596,31 +599,60 @@ __device__ void gemv_rows(const DevProblem* Pg, int r0, int r1, int ew) {
     const int lane = lane_id();
     const bool vec_ok = (n % kVec == 0) && (ld % kVec == 0) &&
                         ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(x)) & 15) == 0;
-    for (int r = r0 + ew; r < r1; r += 4) {
-        const T* w = W + (int64_t)r * ld;
-        float acc = 0.0f;
+    const uint4* xv = reinterpret_cast<const uint4*>(x);
+    for (int rb = r0 + ew; rb < r1; rb += 4 * kRowsPerWarp) {
+        float acc[kRowsPerWarp];
+        const T* w[kRowsPerWarp];
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+            acc[q] = 0.0f;
+            const int r = min(rb + 4 * q, r1 - 1);   // rows past the end recompute the last one
+            w[q] = W + (int64_t)r * ld;
+        }
         if (vec_ok) {
             const int nv = n / kVec;
             int j = lane;
             for (; j + 96 < nv; j += 128) {
-                const uint4 w0 = ld_stream_v4(w + (int64_t)j * kVec);
-                const uint4 w1 = ld_stream_v4(w + (int64_t)(j + 32) * kVec);
-                const uint4 w2 = ld_stream_v4(w + (int64_t)(j + 64) * kVec);
-                const uint4 w3 = ld_stream_v4(w + (int64_t)(j + 96) * kVec);
-                const uint4* xv = reinterpret_cast<const uint4*>(x);
-                acc += dot_v4(w0, __ldg(xv + j), T()) + dot_v4(w1, __ldg(xv + j + 32), T()) +
-                       dot_v4(w2, __ldg(xv + j + 64), T()) + dot_v4(w3, __ldg(xv + j + 96), T());
+                uint4 wv[kRowsPerWarp][4];
+#pragma unroll
+                for (int q = 0; q < kRowsPerWarp; ++q)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) wv[q][u] = ld_stream_v4(w[q] + (int64_t)(j + 32 * u) * kVec);
+                uint4 xx[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) xx[u] = __ldg(xv + j + 32 * u);
+#pragma unroll
+                for (int q = 0; q < kRowsPerWarp; ++q)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[q] += dot_v4(wv[q][u], xx[u], T());
             }
-            for (; j < nv; j += 32)
-                acc += dot_v4(ld_stream_v4(w + (int64_t)j * kVec), __ldg(reinterpret_cast<const uint4*>(x) + j), T());
+            for (; j < nv; j += 32) {
+                const uint4 xx = __ldg(xv + j);
+#pragma unroll
+                for (int q = 0; q < kRowsPerWarp; ++q)
+                    acc[q] += dot_v4(ld_stream_v4(w[q] + (int64_t)j * kVec), xx, T());
+            }
         } else {
-            for (int j = lane; j < n; j += 32) acc += load_f<T>(w + j) * load_f<T>(x + j);
+            for (int jj = lane; jj < n; jj += 32) {
+                const float xs = load_f<T>(x + jj);
+#pragma unroll
+                for (int q = 0; q < kRowsPerWarp; ++q) acc[q] += load_f<T>(w[q] + jj) * xs;
+            }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+        }
         if (lane == 0) {
-            const float b = bias ? __ldg(bias + r) : 0.0f;
-            store_one(out, r, out_dt, apply_act(acc + b, act));
+#pragma unroll
+            for (int q = 0; q < kRowsPerWarp; ++q) {
+                const int r = rb + 4 * q;
+                if (r < r1) {
+                    const float b = bias ? __ldg(bias + r) : 0.0f;
+                    store_one(out, r, out_dt, apply_act(acc[q] + b, act));
+                }
+            }
         }
     }
 }
@@ -1363,8 +1395,9 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
         if (P.kind == kItemGemv) {
             const double row_bytes = (double)P.cols * (P.in_dt == GMX_ST_F32 ? 4 : 2);
             const double item_bytes = std::max(32768.0, (target * 0.5 - kCudaCoreFixedNs) / kNsPerKB * 1024.0);
-            int rows_per = (int)std::max(4.0, std::floor(item_bytes / row_bytes));
-            rows_per = std::max(4, (rows_per / 4) * 4);
+            // multiples of 16 rows: 4 epilogue warps x 4 rows in flight each (gemv_rows)
+            int rows_per = (int)std::max(16.0, std::floor(item_bytes / row_bytes));
+            rows_per = std::max(16, (rows_per / 16) * 16);
             for (int r0 = 0; r0 < P.rows; r0 += rows_per) {
                 WorkItem it{};
                 it.problem = s;
