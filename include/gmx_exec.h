@@ -99,6 +99,13 @@ int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream)
  * previous step's CTAs retire (the executor still waits when split-K state could alias). */
 #define GMX_LAUNCH_INDEPENDENT 1
 int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream, int32_t flags);
+/* As launch_ex, plus the slots whose OUTPUTS this step's members read (their producers): in
+ * resident mode the step then waits only for the steps that last wrote those slots (and for
+ * earlier users of its plan/slots), so independent chains overlap; any dependency makes a
+ * per-step launch dependent. *step_seq (may be NULL) = the step's queue position in resident
+ * mode, else -1. */
+int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const int32_t* dep_slots, int32_t ndep,
+                         void* stream, int32_t flags, int64_t* step_seq);
 /* Stats of the plan used by the last launch. */
 int gmx_exec_last_plan(const gmx_exec* ex, gmx_plan_stats* out);
 
@@ -118,6 +125,9 @@ int gmx_exec_resident_release(gmx_exec* ex);
 int gmx_exec_resident_device_ns(gmx_exec* ex, int64_t* ns);
 int gmx_exec_resident_end(gmx_exec* ex);
 int gmx_exec_resident_completed(gmx_exec* ex, int64_t* steps_done);
+int gmx_exec_resident_active(const gmx_exec* ex);
+/* 1 once resident step `seq` (from gmx_exec_launch_deps) completed on the device, else 0. */
+int gmx_exec_resident_step_done(gmx_exec* ex, int64_t seq);
 /* A caller-owned stream is about to be destroyed: wait for its work and stop using it for
  * the stream-ordered release of plan memory. */
 int gmx_exec_stream_retired(gmx_exec* ex, void* stream);

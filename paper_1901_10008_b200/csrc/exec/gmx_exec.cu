@@ -137,12 +137,15 @@ struct StepDesc {
     float* ws;
     int32_t* counters;
     int32_t grid;             // CTAs holding items in this step (<= gridDim.x)
-    int32_t wait_all;         // a member depends on earlier outputs: all earlier steps first
+    int32_t wait_all;         // a member depends on earlier outputs of unknown steps: all first
     int32_t stop;
-    int32_t _pad;
-    int64_t wait_step;        // latest earlier step sharing a plan or slot with this one, or -1
+    int32_t nwait;            // entries of wait_steps in use
+    int64_t wait_steps[4];    // earlier steps that must be complete first: producers of this
+                              // step's inputs, users of its plan (split-K state) or slots (outputs)
+    int64_t _pad[5];
 };
-static_assert(sizeof(StepDesc) == 64, "StepDesc layout");
+static_assert(sizeof(StepDesc) == 128, "StepDesc layout");
+constexpr int kStepVec = (int)(sizeof(StepDesc) / 16);
 
 struct DevQueue {
     StepDesc ring[kQueue];
@@ -731,10 +734,13 @@ __device__ __forceinline__ void step_order(const KernelArgs& a, int64_t k) {
         for (int64_t j = k - 1; j >= 0 && j >= k - a.window; --j) wait_step_done(a.dq, j, gridDim.x);
         fence_proxy_async_global();   // later TMA loads read what those steps wrote
     } else {
-        // bounded skew, plus the latest step that used the same plan (split-K state) or wrote a
-        // slot this step writes; that step itself waited for any earlier sharer, transitively
+        // bounded skew, plus the listed steps: producers of this step's inputs and the latest
+        // earlier users of its plan or slots (those waited for any earlier sharer, transitively)
         wait_step_done(a.dq, k - a.window, gridDim.x);
-        wait_step_done(a.dq, (int64_t)__ldcg((const long long*)&d->wait_step), gridDim.x);
+        const int nw = __ldcg(&d->nwait);
+        for (int q = 0; q < nw; ++q)
+            wait_step_done(a.dq, (int64_t)__ldcg((const long long*)&d->wait_steps[q]), gridDim.x);
+        if (nw > 0) fence_proxy_async_global();   // later TMA loads may read what they wrote
     }
 }
 
@@ -764,7 +770,7 @@ __device__ void dispatch_steps(const KernelArgs& a) {
     // relay in batches: one poll of the host count, then up to kBatch entries whose PCIe loads
     // are all in flight together (a PCIe round trip costs ~1-2 us; one per step would cap the
     // step rate)
-    constexpr int kBatch = 8;
+    constexpr int kBatch = 4;
     int64_t k = 0;
     for (;;) {
         int64_t avail;
@@ -776,13 +782,13 @@ __device__ void dispatch_steps(const KernelArgs& a) {
             if (global_timer_ns() - t0 > 60000000000ull) __trap();   // host never published
         }
         const int n = (int)(avail - k < kBatch ? avail - k : kBatch);
-        uint4 w[kBatch][4];
+        uint4 w[kBatch][kStepVec];
 #pragma unroll
         for (int b = 0; b < kBatch; ++b) {
             if (b < n) {
                 const uint4* src = reinterpret_cast<const uint4*>(&a.hring[(k + b) % kQueue]);
 #pragma unroll
-                for (int q = 0; q < 4; ++q)   // system-scope loads of host-written entries (after the acquire)
+                for (int q = 0; q < kStepVec; ++q)   // system-scope loads of host-written entries (after the acquire)
                     asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                                  : "=r"(w[b][q].x), "=r"(w[b][q].y), "=r"(w[b][q].z), "=r"(w[b][q].w)
                                  : "l"(src + q));
@@ -794,7 +800,7 @@ __device__ void dispatch_steps(const KernelArgs& a) {
             if (b < n && !stop) {
                 uint4* dst = reinterpret_cast<uint4*>(&a.dq->ring[(k + b) % kQueue]);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) __stcg(dst + q, w[b][q]);
+                for (int q = 0; q < kStepVec; ++q) __stcg(dst + q, w[b][q]);
                 stop = reinterpret_cast<const StepDesc*>(w[b])->stop != 0;
             }
         }
@@ -1265,6 +1271,7 @@ struct gmx_exec {
         std::vector<std::vector<int32_t>> recent_keys;   // slot sets of the last kWindow steps
         std::vector<const gmx::Plan*> recent_plans;
         std::vector<int64_t> recent_seq;
+        std::vector<int64_t> last_write;       // per slot: last step (seq) that wrote its output
         std::vector<void*> graveyard;          // device tables retired during residency
         std::vector<uint8_t> zeros;            // host zeros for copy-engine clears while resident
         int window = 10;                       // max steps a CTA may run ahead (option "resident_window")
@@ -1599,7 +1606,8 @@ static int publish_step(gmx_exec* ex, const StepDesc& d) {
 }
 
 // Resident mode: the step goes to the persistent kernel's queue instead of a launch.
-static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>& key, int32_t flags, bool cached) {
+static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>& key, const int32_t* dep_slots,
+                            int32_t ndep, int32_t flags, bool cached, int64_t* seq_out) {
     auto& r = ex->res;
     int rc;
     if (!plan->uploaded) {
@@ -1608,13 +1616,30 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
     }
     plan->stream = r.stream;   // later frees are ordered after the persistent kernel
     plan->last_use = ++ex->clock;
-    // wait for every earlier step if a member depends on earlier outputs, or this step reuses
-    // a plan (split-K state) or a slot (outputs) of a step that may still be running
-    const bool wait_all = (flags & GMX_LAUNCH_INDEPENDENT) == 0;
-    int64_t wait_step = -1;   // latest step inside the window sharing the plan or a slot
+    // Ordering. Steps <= seq - window are complete before this one starts anyway. Inside the
+    // window wait for: the producers of the inputs (dep_slots: the last step that wrote each),
+    // and the latest step sharing this plan (split-K state) or a slot (outputs). Without
+    // dependency information a non-independent step waits for every earlier step.
+    const int64_t seq = r.seq;
+    const int64_t oldest = seq - r.window + 1;
+    bool wait_all = (flags & GMX_LAUNCH_INDEPENDENT) == 0 && ndep == 0;
+    int64_t waits[4];
+    int nw = 0;
+    auto need = [&](int64_t j) {
+        if (wait_all || j < oldest || j >= seq) return;
+        for (int q = 0; q < nw; ++q)
+            if (waits[q] == j) return;
+        if (nw == 4) { wait_all = true; return; }
+        waits[nw++] = j;
+    };
+    if (r.last_write.size() < ex->probs.size()) r.last_write.resize(ex->probs.size(), -1);
+    for (int32_t i = 0; i < ndep; ++i) {
+        const int32_t sl = dep_slots[i];
+        if (sl >= 0 && sl < (int32_t)r.last_write.size()) need(r.last_write[sl]);
+    }
     for (size_t i = 0; i < r.recent_keys.size(); ++i)
         if (r.recent_plans[i] == plan || keys_intersect(r.recent_keys[i], key)) {
-            wait_step = r.recent_seq[i];
+            need(r.recent_seq[i]);
             break;
         }
     StepDesc d{};
@@ -1625,12 +1650,14 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
     d.counters = plan->d_counters;
     d.grid = plan->stats.grid;
     d.wait_all = wait_all ? 1 : 0;
-    d.wait_step = wait_step;
+    d.nwait = wait_all ? 0 : nw;
+    for (int q = 0; q < nw; ++q) d.wait_steps[q] = waits[q];
     if (d.grid > r.grid) return fail(GMX_ESTATE, "plan grid exceeds the resident grid");
     if ((rc = publish_step(ex, d))) return rc;
+    for (int32_t sl : key) r.last_write[sl] = seq;
     r.recent_keys.insert(r.recent_keys.begin(), key);
     r.recent_plans.insert(r.recent_plans.begin(), plan);
-    r.recent_seq.insert(r.recent_seq.begin(), r.seq - 1);
+    r.recent_seq.insert(r.recent_seq.begin(), seq);
     if ((int)r.recent_keys.size() > r.window) {
         r.recent_keys.pop_back();
         r.recent_plans.pop_back();
@@ -1638,6 +1665,7 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
     }
     plan->stats.cached = cached;
     ex->last = plan;
+    if (seq_out) *seq_out = seq;
     return GMX_OK;
 }
 
@@ -1681,6 +1709,7 @@ int gmx_exec_resident_begin_ex(gmx_exec* ex, void* stream_ptr, int32_t hold) {
     r.recent_keys.clear();
     r.recent_plans.clear();
     r.recent_seq.clear();
+    r.last_write.assign(ex->probs.size(), -1);
     KernelArgs args{};
     args.dbg = ex->dbg;
     args.independent = 1;
@@ -1743,6 +1772,16 @@ int gmx_exec_resident_read_rtrace(gmx_exec* ex, uint64_t* out, int64_t capacity,
     return GMX_OK;
 }
 
+int gmx_exec_resident_active(const gmx_exec* ex) { return ex && ex->res.active ? 1 : 0; }
+
+int gmx_exec_resident_step_done(gmx_exec* ex, int64_t seq) {
+    if (!ex || seq < 0) return 0;
+    auto& r = ex->res;
+    if (!r.hdone) return 0;
+    if (seq < r.seq - kQueue) return 1;   // its ring slot was recycled, so it completed
+    return ((volatile int64_t*)r.hdone)[seq % kQueue] >= seq + 1 ? 1 : 0;
+}
+
 int gmx_exec_resident_relay_ns(gmx_exec* ex, int64_t* out) {
     if (!ex || !out) return fail(GMX_EINVAL, "null argument");
     *out = ex->res.relay_ns;
@@ -1756,7 +1795,7 @@ int gmx_exec_resident_end(gmx_exec* ex) {
     __atomic_store_n(r.hpub + 1, (int64_t)1, __ATOMIC_RELEASE);   // a held start is released
     StepDesc d{};
     d.stop = 1;
-    d.wait_step = -1;
+    d.nwait = 0;
     int rc = publish_step(ex, d);
     r.active = false;
     for (void* p : r.graveyard) cudaFreeAsync(p, r.stream);   // after the persistent kernel
@@ -1958,8 +1997,15 @@ int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream_
 }
 
 int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream_ptr, int32_t flags) {
-    if (!ex || (n > 0 && !slots)) return fail(GMX_EINVAL, "null argument");
+    return gmx_exec_launch_deps(ex, slots, n, nullptr, 0, stream_ptr, flags, nullptr);
+}
+
+int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const int32_t* dep_slots, int32_t ndep,
+                         void* stream_ptr, int32_t flags, int64_t* step_seq) {
+    if (!ex || (n > 0 && !slots) || (ndep > 0 && !dep_slots)) return fail(GMX_EINVAL, "null argument");
+    if (step_seq) *step_seq = -1;
     if (n == 0) return GMX_OK;
+    if (ndep > 0) flags &= ~GMX_LAUNCH_INDEPENDENT;   // reads earlier outputs
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
     std::vector<int32_t>& key = ex->key_scratch;
     key.assign(slots, slots + n);
@@ -1997,7 +2043,7 @@ int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stre
         if ((rc = build_plan(ex, key, *ex->uncached))) return rc;
         plan = ex->uncached.get();
     }
-    if (ex->res.active) return enqueue_resident(ex, plan, key, flags, cached);
+    if (ex->res.active) return enqueue_resident(ex, plan, key, dep_slots, ndep, flags, cached, step_seq);
     // multi-stream: a plan's split-K state and outputs must not be used by two launches at once
     if (ex->multi_stream && plan->done_ev && plan->stream != stream)
         GMX_CUDA(cudaStreamWaitEvent(stream, plan->done_ev, 0));

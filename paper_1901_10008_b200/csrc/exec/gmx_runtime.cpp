@@ -60,6 +60,9 @@ struct gmx_runtime {
     std::vector<int32_t> pool_free;
     gmx::IdMap req_index;                 // request id -> pool index (until the request finishes)
     gmx::IdMap slot_of;                   // kernel id -> executor slot (until dispatched)
+    gmx::IdMap depslots_of;               // kernel id -> offset in depslot_arena (kernels with deps)
+    std::vector<int32_t> depslot_arena;   // [count, producer slot...] per kernel with deps
+    std::vector<int32_t> launch_deps;     // producer slots of one launch
     std::vector<gmx_kernel_desc> k_arena; // compacted when the pool drains
     std::vector<int64_t> dep_arena;
     std::vector<int32_t> off_arena;
@@ -73,12 +76,14 @@ struct gmx_runtime {
     bool origin_set = false;
     int64_t origin_ns = 0;
     struct InFlight {
-        cudaEvent_t ev;
+        cudaEvent_t ev;                  // launch per step: event after the launch
         std::vector<int64_t> dispatch_ids;
+        int64_t seq;                     // resident executor: step queue position (ev unused)
     };
     std::deque<InFlight> inflight;
     std::vector<cudaStream_t> streams;   // realtime: launches round-robin over these
     int64_t prof_ns[4] = {0, 0, 0, 0};   // host time in add_request / step / complete / launch
+    int64_t last_seq = -1;               // resident executor: queue position of the last step
     size_t next_stream = 0;
     std::vector<cudaEvent_t> event_pool;
     std::vector<gmx_replay_rec> log;
@@ -104,6 +109,8 @@ static void release_request(gmx_runtime* rt, int64_t rid) {
         rt->k_arena.clear();
         rt->dep_arena.clear();
         rt->off_arena.clear();
+        rt->depslot_arena.clear();
+        rt->depslots_of.clear();
     }
 }
 
@@ -200,6 +207,21 @@ int gmx_runtime_submit(gmx_runtime* rt, int64_t rid, int32_t stream, int64_t arr
     // earlier launch wrote, so their launch must not overlap it)
     for (int32_t i = 0; i < n; ++i)
         rt->slot_of.put(ks[i].kernel_id, slots[i] | ((n > 0 && dep_off[i + 1] > dep_off[i]) ? kHasDeps : 0));
+    // producers' executor slots per dependent kernel (deps name kernels of the same request,
+    // kernels.py:95-124), so a launch can tell the executor exactly which outputs it reads
+    for (int32_t i = 0; i < n; ++i) {
+        if (dep_off[i + 1] <= dep_off[i]) continue;
+        const int32_t off = (int32_t)rt->depslot_arena.size();
+        rt->depslot_arena.push_back(0);
+        for (int32_t j = dep_off[i]; j < dep_off[i + 1]; ++j)
+            for (int32_t q = 0; q < n; ++q)
+                if (ks[q].kernel_id == dep_ids[j]) {
+                    rt->depslot_arena.push_back(slots[q]);
+                    ++rt->depslot_arena[off];
+                    break;
+                }
+        rt->depslots_of.put(ks[i].kernel_id, off);
+    }
     rt->req_index.put(rid, pi);
     ++rt->live_requests;
     rt->heap.push({arrival, kArrival, rid});
@@ -266,6 +288,7 @@ static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool real
     }
     if (v.n_dispatches > 0) {
         rt->launch_slots.clear();
+        rt->launch_deps.clear();
         bool independent = true;
         for (int32_t d = 0; d < v.n_dispatches; ++d) {
             const gmx_dispatch_rec& r = v.dispatches[d];
@@ -276,6 +299,15 @@ static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool real
                 independent &= (slot & kHasDeps) == 0;
                 rt->launch_slots.push_back(slot & ~kHasDeps);
                 rt->slot_of.erase(kid);
+                if (slot & kHasDeps) {
+                    const int32_t off = rt->depslots_of.find(kid);
+                    if (off >= 0) {
+                        const int32_t cnt = rt->depslot_arena[off];
+                        rt->launch_deps.insert(rt->launch_deps.end(), rt->depslot_arena.begin() + off + 1,
+                                               rt->depslot_arena.begin() + off + 1 + cnt);
+                        rt->depslots_of.erase(kid);
+                    }
+                }
             }
             if (realtime)
                 ids->push_back(r.dispatch_id);
@@ -285,8 +317,13 @@ static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool real
             rt->st.kernels += r.n_kernels;
         }
         const int64_t t_l = steady_ns();
-        rc = gmx_exec_launch_ex(rt->ex, rt->launch_slots.data(), (int32_t)rt->launch_slots.size(), stream,
-                                independent ? GMX_LAUNCH_INDEPENDENT : 0);
+        // dependencies go to the executor as the producers' slots: a per-step launch becomes
+        // dependent, a resident step waits only for the steps that wrote those slots
+        int64_t seq = -1;
+        rc = gmx_exec_launch_deps(rt->ex, rt->launch_slots.data(), (int32_t)rt->launch_slots.size(),
+                                  rt->launch_deps.data(), (int32_t)rt->launch_deps.size(), stream,
+                                  independent ? GMX_LAUNCH_INDEPENDENT : 0, &seq);
+        rt->last_seq = seq;
         rt->prof_ns[3] += steady_ns() - t_l;
         if (rc) return fail(rc, std::string("launch: ") + gmx_exec_last_error());
         ++rt->st.launches;
@@ -312,12 +349,19 @@ static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtim
         // COMPLETE: any launch whose event has completed (launches on several streams may
         // retire out of order; each launch's dispatches complete in dispatch-id order)
         for (size_t i = 0; i < rt->inflight.size();) {
-            const cudaError_t q = cudaEventQuery(rt->inflight[i].ev);
-            if (q == cudaErrorNotReady) {
-                ++i;
-                continue;
+            if (rt->inflight[i].seq >= 0) {   // resident: the executor's host-mapped completion flags
+                if (!gmx_exec_resident_step_done(rt->ex, rt->inflight[i].seq)) {
+                    ++i;
+                    continue;
+                }
+            } else {
+                const cudaError_t q = cudaEventQuery(rt->inflight[i].ev);
+                if (q == cudaErrorNotReady) {
+                    ++i;
+                    continue;
+                }
+                if (q != cudaSuccess) return fail(GMX_ECUDA, std::string("launch failed: ") + cudaGetErrorString(q));
             }
-            if (q != cudaSuccess) return fail(GMX_ECUDA, std::string("launch failed: ") + cudaGetErrorString(q));
             for (int64_t did : rt->inflight[i].dispatch_ids) {
                 gmx_complete_view cv;
                 int rc = gmx_sched_complete(rt->sched, did, now, &cv);
@@ -325,7 +369,7 @@ static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtim
                 log_rec(rt, 0, now, did);
                 on_finished(rt, cv, now);
             }
-            rt->event_pool.push_back(rt->inflight[i].ev);
+            if (rt->inflight[i].seq < 0) rt->event_pool.push_back(rt->inflight[i].ev);
             rt->inflight.erase(rt->inflight.begin() + (long)i);
             any = true;
         }
@@ -349,7 +393,9 @@ static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtim
             }
             int rc = step_and_launch(rt, now, launch_stream, true, &ids);
             if (rc) return rc;
-            if (!ids.empty()) {
+            if (!ids.empty() && rt->last_seq >= 0) {   // resident executor: no events needed
+                rt->inflight.push_back({nullptr, ids, rt->last_seq});
+            } else if (!ids.empty()) {
                 cudaEvent_t ev;
                 if (!rt->event_pool.empty()) {
                     ev = rt->event_pool.back();
@@ -358,7 +404,7 @@ static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtim
                     return fail(GMX_ECUDA, "cudaEventCreate failed");
                 }
                 if (cudaEventRecord(ev, cs) != cudaSuccess) return fail(GMX_ECUDA, "cudaEventRecord failed");
-                rt->inflight.push_back({ev, ids});
+                rt->inflight.push_back({ev, ids, -1});
                 if (!rt->streams.empty()) rt->next_stream = (rt->next_stream + 1) % rt->streams.size();
             }
             continue;

@@ -56,6 +56,10 @@ EXEC_SIGNATURES = {
     "gmx_exec_clear_plans": (C.c_int, [C.c_void_p]),
     "gmx_exec_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
     "gmx_exec_resident_begin": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gmx_exec_launch_deps": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32),
+                                       C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int64)]),
+    "gmx_exec_resident_active": (C.c_int, [C.c_void_p]),
+    "gmx_exec_resident_step_done": (C.c_int, [C.c_void_p, C.c_int64]),
     "gmx_exec_resident_end": (C.c_int, [C.c_void_p]),
     "gmx_exec_resident_begin_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "gmx_exec_resident_release": (C.c_int, [C.c_void_p]),
@@ -200,16 +204,26 @@ class Executor:
 
     # ---- execution ----------------------------------------------------------------------
 
-    def launch(self, slots, stream=None, independent=False):
+    def launch(self, slots, stream=None, independent=False, dep_slots=None):
         """One coalesced launch over the given registered slots (async on `stream`).
 
         independent=True promises no member reads what the previous launch on the stream
-        writes, letting this step overlap the previous step's tail (PDL)."""
+        writes, letting this step overlap the previous step's tail (PDL). dep_slots: slots whose
+        outputs the members read (their producers); in resident mode the step then waits only
+        for the steps that wrote them. Returns the resident queue position (or -1)."""
         slots = list(slots)
         arr = (C.c_int32 * max(1, len(slots)))(*slots)
+        deps = list(dep_slots or [])
+        darr = (C.c_int32 * max(1, len(deps)))(*deps)
+        seq = C.c_int64(-1)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        _check(self._lib.gmx_exec_launch_ex(self._h, arr, len(slots), C.c_void_p(s.cuda_stream),
-                                            1 if independent else 0))
+        _check(self._lib.gmx_exec_launch_deps(self._h, arr, len(slots), darr, len(deps),
+                                              C.c_void_p(s.cuda_stream), 1 if independent else 0,
+                                              C.byref(seq)))
+        return seq.value
+
+    def resident_step_done(self, seq: int) -> bool:
+        return bool(self._lib.gmx_exec_resident_step_done(self._h, int(seq)))
 
     def launch_dispatches(self, dispatches, stream=None):
         """Execute every member of every dispatch of one scheduler step in ONE launch."""

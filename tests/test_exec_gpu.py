@@ -284,3 +284,36 @@ def test_resident_many_steps_ring_wrap(ex):
     for row in slots:
         for sl in row:
             ex.unregister(sl)
+
+
+def test_resident_dependency_slots_order_producer_consumer(ex):
+    """A consumer step that declares its producer's slot sees the producer's output even when
+    other independent steps are queued between them (resident fine-grained waits)."""
+    from paper_1901_10008_b200.executor import OperandSet
+    prod = OperandSet("gemm", (256, 64, 512), seed=900)
+    # consumer reads the producer's output C (m=256 x n=64, bf16) as its B^T operand (k=256? no:
+    # B^T is [n][k]): use an elementwise member over the producer's output buffer instead
+    pslot = prod.register(ex)
+    assert prod.c.is_contiguous()
+    cons = OperandSet.from_tensors("elementwise", (prod.c.numel(),), prod.c.reshape(-1), None,
+                                   torch.empty_like(prod.c).reshape(-1), activation="relu")
+    cslot = cons.register(ex)
+    others = [[OperandSet("gemm", C2_SHAPES[(i + r) % 13], seed=950 + 16 * r + i) for i in range(8)] for r in range(3)]
+    oslots = [[o.register(ex) for o in row] for row in others]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ex.launch([pslot], s)
+        ex.launch(oslots[0], s, independent=True)
+        ex.launch([cslot], s)
+        s.synchronize()
+        cons.c.zero_()
+        with ex.resident(s):
+            for k in range(6):
+                ex.launch([pslot], s, independent=True)
+                ex.launch(oslots[k % 3], s, independent=True)
+                ex.launch([cslot], s, dep_slots=[pslot])
+        s.synchronize()
+    ref = torch.relu(prod.c.float())
+    assert torch.equal(cons.c.reshape(prod.c.shape).float(), ref.to(prod.c.dtype).float())
+    for o in [pslot, cslot] + [x for row in oslots for x in row]:
+        ex.unregister(o)

@@ -94,7 +94,8 @@ def test_runtime_mixed_chains_match_oracle_engine(resident):
     assert stats["completed_requests"] == 10
 
 
-def test_realtime_mode_replays_through_the_reference_scheduler():
+@pytest.mark.parametrize("resident", [False, True])
+def test_realtime_mode_replays_through_the_reference_scheduler(resident):
     """Wall-clock mode: arrivals at real times, completions from CUDA events. Replaying the
     logged (time, event) sequence through the oracle scheduler (pinned to gpumux) must
     reproduce every step's decisions: dispatch ids + members, withheld groups, wakeups."""
@@ -118,7 +119,16 @@ def test_realtime_mode_replays_through_the_reference_scheduler():
                                                           k.deps, k.arrival, k.deadline) for k in r.kernels),
                                       r.arrival, gm.LatencyConstraint(10_000_000)), slots)
     rt.set_origin_now()
-    stats = rt.run(until=2_000_000_000)
+    if resident:   # completions observed from the resident executor's host-mapped flags
+        s = torch.cuda.current_stream()
+        ex.resident_begin(s)
+        try:
+            stats = rt.run(until=2_000_000_000, stream=s)
+        finally:
+            ex.resident_end()
+        torch.cuda.synchronize()
+    else:
+        stats = rt.run(until=2_000_000_000)
     assert stats["completed_requests"] == len(reqs)
     log = rt.replay_log()
     by_rid = {r.request_id: r for r in reqs}

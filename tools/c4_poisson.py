@@ -39,7 +39,8 @@ def setup(tenants, models):
     return ex, slots
 
 
-def run(ex, slots, rate, tenants, duration_ns, models, lead_ns=20_000_000, streams=8, stagger_ns=10_000, seed=0):
+def run(ex, slots, rate, tenants, duration_ns, models, lead_ns=20_000_000, streams=8, stagger_ns=10_000, seed=0,
+        resident=False):
     lib = gm.kernels.load_model_library()
     wl = {"duration_ns": duration_ns,
           "streams": [{"stream_id": f"p{i:02d}", "model_name": models[i % len(models)], "slo_ns": SLO_NS,
@@ -56,7 +57,16 @@ def run(ex, slots, rate, tenants, duration_ns, models, lead_ns=20_000_000, strea
         rt.submit(gm.InferenceRequest(r.request_id, r.stream_id, ks, r.arrival + lead_ns,
                                       gm.LatencyConstraint(SLO_NS)), slots[r.stream_id])
     rt.set_origin_now()
-    stats = rt.run(until=duration_ns + lead_ns + 2_000_000_000)
+    if resident:   # steps go to one persistent launch; completions from its host-mapped flags
+        s = torch.cuda.current_stream()
+        ex.resident_begin(s)
+        try:
+            stats = rt.run(until=duration_ns + lead_ns + 2_000_000_000, stream=s)
+        finally:
+            ex.resident_end()
+        torch.cuda.synchronize()
+    else:
+        stats = rt.run(until=duration_ns + lead_ns + 2_000_000_000)
     done = dict(rt.drain_completions(1 << 20))
     arrival = {r.request_id: r.arrival + lead_ns for r in reqs}
     lat = sorted(done[rid] - arrival[rid] for rid in done)
@@ -67,7 +77,8 @@ def run(ex, slots, rate, tenants, duration_ns, models, lead_ns=20_000_000, strea
         return lat[max(1, -(-int(p * n * 1000) // 1000)) - 1] if n else None
 
     return {"config": "c4", "rate_per_stream": rate, "tenants": tenants, "duration_s": duration_ns / 1e9,
-            "cuda_streams": streams, "stagger_horizon_ns": stagger_ns,
+            "executor": "resident" if resident else "launch per step",
+            "cuda_streams": None if resident else streams, "stagger_horizon_ns": stagger_ns,
             "requests": len(reqs), "completed": n,
             "slo_attainment": sum(1 for x in lat if x <= SLO_NS) / max(1, len(reqs)),
             "p50_ms": pct(0.5) / 1e6 if n else None, "p99_ms": pct(0.99) / 1e6 if n else None,
@@ -86,16 +97,17 @@ def main():
     ap.add_argument("--models", default=",".join(MODELS))
     ap.add_argument("--streams", default="8")
     ap.add_argument("--stagger-ns", default="10000")
+    ap.add_argument("--resident", action="store_true", help="run the steps through the resident executor")
     args = ap.parse_args()
     models = args.models.split(",")
     ex, slots = setup(args.tenants, models)
     # warm-up pass: CUDA/driver lazy init, TMA descriptors, plan cache for the recurring step shapes
-    run(ex, slots, 20.0, args.tenants, 50_000_000, models, seed=99)
+    run(ex, slots, 20.0, args.tenants, 50_000_000, models, seed=99, resident=args.resident)
     for stagger in (int(x) for x in args.stagger_ns.split(",")):
         for ns in (int(x) for x in args.streams.split(",")):
             for rate in (float(x) for x in args.rates.split(",")):
                 print(json.dumps(run(ex, slots, rate, args.tenants, int(args.duration_ms * 1e6), models,
-                                     streams=ns, stagger_ns=stagger)), flush=True)
+                                     streams=ns, stagger_ns=stagger, resident=args.resident)), flush=True)
 
 
 if __name__ == "__main__":
