@@ -74,6 +74,7 @@ int gmx_runtime_set_streams(gmx_runtime* rt, int32_t n);
 /* Cumulative host nanoseconds spent in the decision core (add_request, step, complete) and in
  * the executor's launch/enqueue path, for host-cost accounting of the serving loop. */
 int gmx_runtime_host_profile(const gmx_runtime* rt, int64_t* ns4);
+int gmx_runtime_set_profiling(gmx_runtime* rt, int32_t on);   /* off by default */
 int64_t gmx_runtime_clock_ns(const gmx_runtime* rt);
 /* Replay log (realtime mode). Records, in order:
  *   kind 0: complete(dispatch_id=a) at time t      kind 1: add_request(request_id=a) at t

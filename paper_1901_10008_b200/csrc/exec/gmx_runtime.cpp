@@ -56,6 +56,10 @@ struct gmx_runtime {
     gmx_exec* ex;
     int32_t mode;
     std::priority_queue<Event, std::vector<Event>, std::greater<Event>> heap;
+    // Arrivals submitted in (time, id) order — the common case, requests are queued ahead —
+    // wait in a FIFO instead of the heap, which then only holds completions and wakeups; an
+    // out-of-order arrival goes to the heap. The event order is unchanged (merge of the two).
+    std::deque<Event> arrivals;
     std::vector<Pending> pool;
     std::vector<int32_t> pool_free;
     gmx::IdMap req_index;                 // request id -> pool index (until the request finishes)
@@ -83,6 +87,7 @@ struct gmx_runtime {
     std::deque<InFlight> inflight;
     std::vector<cudaStream_t> streams;   // realtime: launches round-robin over these
     int64_t prof_ns[4] = {0, 0, 0, 0};   // host time in add_request / step / complete / launch
+    bool prof_on = false;                // gmx_runtime_set_profiling (clock reads cost ~1 us/round)
     int64_t last_seq = -1;               // resident executor: queue position of the last step
     size_t next_stream = 0;
     std::vector<cudaEvent_t> event_pool;
@@ -163,6 +168,12 @@ int gmx_runtime_set_origin(gmx_runtime* rt, int64_t ns) {
     return GMX_OK;
 }
 
+int gmx_runtime_set_profiling(gmx_runtime* rt, int32_t on) {
+    if (!rt) return fail(GMX_EINVAL, "null argument");
+    rt->prof_on = on != 0;
+    return GMX_OK;
+}
+
 int gmx_runtime_host_profile(const gmx_runtime* rt, int64_t* out4) {
     if (!rt || !out4) return fail(GMX_EINVAL, "null argument");
     for (int i = 0; i < 4; ++i) out4[i] = rt->prof_ns[i];
@@ -224,7 +235,11 @@ int gmx_runtime_submit(gmx_runtime* rt, int64_t rid, int32_t stream, int64_t arr
     }
     rt->req_index.put(rid, pi);
     ++rt->live_requests;
-    rt->heap.push({arrival, kArrival, rid});
+    const Event ev{arrival, kArrival, rid};
+    if (rt->arrivals.empty() || !(rt->arrivals.back() > ev))
+        rt->arrivals.push_back(ev);
+    else
+        rt->heap.push(ev);
     return GMX_OK;
 }
 
@@ -251,11 +266,11 @@ static int on_arrival(gmx_runtime* rt, int64_t rid) {
     rt->pred.resize((size_t)std::max(1, p.n));
     const int32_t dep_base = rt->off_arena[p.d_off + p.n + 1];
     int32_t accepted = 0;
-    const int64_t t_add = steady_ns();
+    const int64_t t_add = rt->prof_on ? steady_ns() : 0;
     int rc = gmx_sched_add_request(rt->sched, rid, p.stream, p.arrival, rt->k_arena.data() + p.k_off, p.n,
                                    rt->dep_arena.data() + dep_base, rt->off_arena.data() + p.d_off,
                                    rt->pred.data(), &accepted);
-    rt->prof_ns[0] += steady_ns() - t_add;
+    if (rt->prof_on) rt->prof_ns[0] += steady_ns() - t_add;
     if (rc) return fail(rc, std::string("add_request: ") + gmx_last_error());
     if (!accepted) release_request(rt, rid);
     return GMX_OK;
@@ -265,9 +280,9 @@ static int on_arrival(gmx_runtime* rt, int64_t rid) {
 // dispatch ids of the launch are returned in `ids` (completion is observed, not scheduled).
 static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool realtime, std::vector<int64_t>* ids) {
     gmx_step_view v;
-    const int64_t t_step = steady_ns();
+    const int64_t t_step = rt->prof_on ? steady_ns() : 0;
     int rc = gmx_sched_step(rt->sched, now, &v);
-    rt->prof_ns[1] += steady_ns() - t_step;
+    if (rt->prof_on) rt->prof_ns[1] += steady_ns() - t_step;
     if (rc) return fail(rc, std::string("step: ") + gmx_last_error());
     ++rt->st.steps;
     rt->st.withheld += v.n_withheld;
@@ -316,7 +331,7 @@ static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool real
             rt->st.useful_flops += r.useful_flops;
             rt->st.kernels += r.n_kernels;
         }
-        const int64_t t_l = steady_ns();
+        const int64_t t_l = rt->prof_on ? steady_ns() : 0;
         // dependencies go to the executor as the producers' slots: a per-step launch becomes
         // dependent, a resident step waits only for the steps that wrote those slots
         int64_t seq = -1;
@@ -324,7 +339,7 @@ static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool real
                                   rt->launch_deps.data(), (int32_t)rt->launch_deps.size(), stream,
                                   independent ? GMX_LAUNCH_INDEPENDENT : 0, &seq);
         rt->last_seq = seq;
-        rt->prof_ns[3] += steady_ns() - t_l;
+        if (rt->prof_on) rt->prof_ns[3] += steady_ns() - t_l;
         if (rc) return fail(rc, std::string("launch: ") + gmx_exec_last_error());
         ++rt->st.launches;
         rt->st.dispatches += v.n_dispatches;
@@ -332,6 +347,24 @@ static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool real
     if (v.has_wakeup) rt->heap.push({v.wakeup, kWakeup, ++rt->wake_seq});
     rt->st.now = now;
     return GMX_OK;
+}
+
+// Earliest pending event (heap and arrival FIFO merged); nullptr when none.
+static const Event* peek_event(const gmx_runtime* rt) {
+    const Event* h = rt->heap.empty() ? nullptr : &rt->heap.top();
+    const Event* a = rt->arrivals.empty() ? nullptr : &rt->arrivals.front();
+    if (!h) return a;
+    if (!a) return h;
+    return (*h > *a) ? a : h;
+}
+static Event pop_event(gmx_runtime* rt) {
+    const Event* e = peek_event(rt);
+    const Event out = *e;
+    if (!rt->arrivals.empty() && e == &rt->arrivals.front())
+        rt->arrivals.pop_front();
+    else
+        rt->heap.pop();
+    return out;
 }
 
 // Wall-clock loop: returns when every submitted request has finished and nothing is in flight,
@@ -374,9 +407,8 @@ static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtim
             any = true;
         }
         // ARRIVAL then WAKEUP events that are due (heap order: time, kind, id)
-        while (!rt->heap.empty() && rt->heap.top().time <= now) {
-            const Event e = rt->heap.top();
-            rt->heap.pop();
+        while (peek_event(rt) && peek_event(rt)->time <= now) {
+            const Event e = pop_event(rt);
             if (e.kind == kArrival) {
                 log_rec(rt, 1, now, e.id);
                 int rc = on_arrival(rt, e.id);
@@ -409,7 +441,7 @@ static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtim
             }
             continue;
         }
-        if (rt->heap.empty() && rt->inflight.empty()) break;   // drained
+        if (!peek_event(rt) && rt->inflight.empty()) break;   // drained
         if (now > until) break;
     }
     rt->st.now = steady_ns() - rt->origin_ns;
@@ -420,16 +452,15 @@ static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtim
 int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* stream, gmx_runtime_stats* out) {
     if (!rt) return fail(GMX_EINVAL, "null argument");
     if (rt->mode == GMX_RT_REALTIME) return run_realtime(rt, until, stream, out);
-    while (!rt->heap.empty() && rt->heap.top().time <= until) {
-        const int64_t now = rt->heap.top().time;
-        while (!rt->heap.empty() && rt->heap.top().time == now) {
-            const Event e = rt->heap.top();
-            rt->heap.pop();
+    while (peek_event(rt) && peek_event(rt)->time <= until) {
+        const int64_t now = peek_event(rt)->time;
+        while (peek_event(rt) && peek_event(rt)->time == now) {
+            const Event e = pop_event(rt);
             if (e.kind == kComplete) {
                 gmx_complete_view cv;
-                const int64_t t_c = steady_ns();
+                const int64_t t_c = rt->prof_on ? steady_ns() : 0;
                 int rc = gmx_sched_complete(rt->sched, e.id, now, &cv);
-                rt->prof_ns[2] += steady_ns() - t_c;
+                if (rt->prof_on) rt->prof_ns[2] += steady_ns() - t_c;
                 if (rc) return fail(rc, std::string("complete: ") + gmx_last_error());
                 on_finished(rt, cv, now);
             } else if (e.kind == kArrival) {

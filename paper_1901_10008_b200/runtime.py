@@ -51,6 +51,7 @@ RT_SIGNATURES = {
     "gmx_runtime_set_streams": (C.c_int, [C.c_void_p, C.c_int32]),
     "gmx_runtime_clock_ns": (C.c_int64, [C.c_void_p]),
     "gmx_runtime_host_profile": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "gmx_runtime_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
     "gmx_runtime_replay_log": (C.c_int, [C.c_void_p, C.POINTER(ReplayRec), C.c_int64,
                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_int64,
                                          C.POINTER(C.c_int64)]),
@@ -157,6 +158,10 @@ class Runtime:
         _check(_rt_lib().gmx_runtime_run(self._rt, int(until), C.c_void_p(s.cuda_stream),
                                          C.byref(self._stats)))
         return {n: getattr(self._stats, n) for n, _ in RuntimeStats._fields_}
+
+    def set_profiling(self, on: bool):
+        """Accumulate host ns per phase (host_profile); costs ~1 us per C2 round when on."""
+        _check(_rt_lib().gmx_runtime_set_profiling(self._rt, 1 if on else 0))
 
     def host_profile(self) -> dict:
         """Cumulative host ns in the decision core (add/step/complete) and the launch path."""

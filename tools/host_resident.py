@@ -9,6 +9,7 @@ import torch  # noqa: E402
 from bench import C2Bench  # noqa: E402
 
 b = C2Bench(replicas=8)
+b.rt.set_profiling(True)
 K = 400
 r0 = 0
 for mode in ("launch", "resident", "launch", "resident"):
