@@ -158,7 +158,7 @@ class ClockSampler:
 # ---------------------------------------------------------------- our arm
 
 class C2Bench:
-    def __init__(self, replicas, profile_name="b200"):
+    def __init__(self, replicas, profile_name="b200", tuning=None):
         import torch
 
         import paper_1901_10008_b200 as gm
@@ -197,10 +197,20 @@ class C2Bench:
                 c = self.c_arena[r][self.c_offsets[i]:self.c_offsets[i] + m * ldn].view(m, ldn)[:, :n]
                 row.append(OperandSet.from_tensors("gemm", (m, n, k), src.a, bt, c))
             self.ops.append(row)
-        self.slots = [[o.register(self.ex) for o in row] for row in self.ops]
+        # optional measured TuningTable (tools/autotune.py): decisions use it and each member's
+        # executor tile is the one measured best at its co-tenancy in the round
+        self.table = None
+        tiles = [0] * len(self.shapes)
+        if tuning:
+            from paper_1901_10008_b200.autotune import tile_n_for
+            from paper_1901_10008_b200.tuning import ClusterKey, TuningTable
+            self.table = TuningTable.load(tuning)
+            for i, dims in enumerate(self.shapes):
+                tiles[i] = tile_n_for(self.table, ClusterKey("gemm", "fp16", dims), self.shapes.count(dims))
+        self.slots = [[o.register(self.ex, tile_n=tiles[i]) for i, o in enumerate(row)] for row in self.ops]
         self.profile = gm.load_profile(profile_name)
         self.policy = gm.SchedulerPolicy("ooo")
-        self.rt = Runtime(self.ex, self.profile, self.policy)
+        self.rt = Runtime(self.ex, self.profile, self.policy, tuning_table=self.table)
         self.codes = [self.rt.stream_code(f"t{i:02d}") for i in range(N_TENANTS)]
         self.next_round = 0
         self.stream = torch.cuda.current_stream()
@@ -501,7 +511,7 @@ def read_traffic():
 def run_ours(args, world, rank):
     import torch
     torch.backends.cuda.matmul.allow_tf32 = False
-    bench = C2Bench(args.replicas)
+    bench = C2Bench(args.replicas, tuning=args.tuning)
     shapes = bench.shapes
     flops_round = useful_flops(shapes)
     # warmup (plans cached, TMA descriptors hot, clocks up; the resident executor's queue,
@@ -588,6 +598,7 @@ def run_ours(args, world, rank):
         "config": {"workload": "C2: 16 tenant streams x 1 batch-1 request/round, "
                                "resnet50_like[i%13] im2col GEMMs, bf16, SLO 10ms",
                    "policy": "ooo (native core, bit-exact vs gpumux)", "decision_profile": "b200",
+                   "tuning_table": args.tuning or "none (reference default tiles)",
                    "step": "one scheduling round in lockstep virtual time; each scheduler step "
                            "with dispatches = one coalesced step of the resident sm_100a kernel",
                    "l2": f"inputs rotate over {args.replicas} operand replicas "
@@ -664,6 +675,8 @@ def main():
     ap.add_argument("--replicas", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--quick", action="store_true", help="skip comparators and CPU baseline")
+    ap.add_argument("--tuning", default=None,
+                    help="measured TuningTable JSON (tools/autotune.py) for decisions and tiles")
     ap.add_argument("--launch-per-step", action="store_true",
                     help="one kernel launch per scheduler step instead of the resident executor")
     args = ap.parse_args()

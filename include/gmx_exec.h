@@ -61,6 +61,9 @@ typedef struct gmx_problem_desc {
     void* c;               /* output */
     int64_t ldc;
     const float* bias;     /* optional, length m (gemm/gemv); NULL for none */
+    int32_t tile_n;        /* gemm: UMMA N of the output tiles, 64 or 128; 0 = automatic (a
+                            * measured TuningTable's tile_n, see autotune.py) */
+    int32_t _reserved;
 } gmx_problem_desc;
 
 typedef struct gmx_plan_stats {

@@ -1908,6 +1908,10 @@ int gmx_exec_register(gmx_exec* ex, const gmx_problem_desc* d, int32_t* out_slot
         P.cols = (int32_t)(swap ? d->m : d->n);
         P.K = (int32_t)d->k;
         P.bn = choose_bn(P.cols);
+        if (d->tile_n != 0) {   // tuned tile (autotune.py); multiples of 64 keep output boxes per tile
+            if (d->tile_n != 64 && d->tile_n != 128) return fail(GMX_EINVAL, "tile_n must be 0, 64 or 128");
+            P.bn = d->tile_n;
+        }
         P.kblocks = (int32_t)((d->k + kBlockK - 1) / kBlockK);
         const void* rows_ptr = swap ? d->b : d->a;
         const void* cols_ptr = swap ? d->a : d->b;

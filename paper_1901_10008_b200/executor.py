@@ -32,7 +32,8 @@ class ProblemDesc(C.Structure):
     _fields_ = [("op", C.c_int32), ("in_dtype", C.c_int32), ("out_dtype", C.c_int32),
                 ("activation", C.c_int32), ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64),
                 ("a", C.c_void_p), ("lda", C.c_int64), ("b", C.c_void_p), ("ldb", C.c_int64),
-                ("c", C.c_void_p), ("ldc", C.c_int64), ("bias", C.c_void_p)]
+                ("c", C.c_void_p), ("ldc", C.c_int64), ("bias", C.c_void_p),
+                ("tile_n", C.c_int32), ("_reserved", C.c_int32)]
 
 
 class PlanStats(C.Structure):
@@ -139,8 +140,9 @@ class Executor:
         self._keep[slot.value] = keep
         return slot.value
 
-    def register_gemm(self, a, bt, c, bias=None, activation="none", k=None):
-        """C[m,n] = act(A[m,k] . Bt[n,k]^T + bias[m]); A/Bt bf16 with row stride % 8 == 0."""
+    def register_gemm(self, a, bt, c, bias=None, activation="none", k=None, tile_n=0):
+        """C[m,n] = act(A[m,k] . Bt[n,k]^T + bias[m]); A/Bt bf16 with row stride % 8 == 0.
+        tile_n: UMMA N of the output tiles (64/128; 0 = automatic, or a measured TuningTable's)."""
         self._check_tensor(a, "A", (torch.bfloat16,))
         self._check_tensor(bt, "Bt", (torch.bfloat16,))
         self._check_tensor(c, "C", (torch.bfloat16, torch.float32))
@@ -153,7 +155,7 @@ class Executor:
         d = ProblemDesc(op=_lib.OP_CODE["gemm"], in_dtype=0, out_dtype=ST[c.dtype],
                         activation=ACT[activation], m=m, n=n, k=k, a=a.data_ptr(), lda=a.stride(0),
                         b=bt.data_ptr(), ldb=bt.stride(0), c=c.data_ptr(), ldc=c.stride(0),
-                        bias=self._bias_ptr(bias, m))
+                        bias=self._bias_ptr(bias, m), tile_n=int(tile_n))
         return self._register(d, (a, bt, c, bias))
 
     def register_gemv(self, w, x, y, bias=None, activation="none"):
@@ -387,10 +389,10 @@ class OperandSet:
         self.a, self.b, self.c, self.bias = a, b, c, bias
         return self
 
-    def register(self, ex: Executor) -> int:
+    def register(self, ex: Executor, tile_n=0) -> int:
         if self.op_kind == "gemm":
             return ex.register_gemm(self.a, self.b, self.c, self.bias, self.activation,
-                                    k=self.dims[2])
+                                    k=self.dims[2], tile_n=tile_n)
         if self.op_kind == "gemv":
             return ex.register_gemv(self.a, self.b, self.c, self.bias, self.activation)
         return ex.register_elementwise(self.a, self.c, self.activation)
