@@ -222,6 +222,13 @@ int gmx_sched_complete(gmx_sched* s, int64_t dispatch_id, int64_t now, gmx_compl
  * live ones (decisions are unchanged; finished kernels can no longer be queried by id and kernel
  * ids must not be reused). Off by default: the reference keeps everything (scheduler.py:150-163). */
 int gmx_sched_set_retire(gmx_sched* s, int32_t on);
+/* complete() with the observed duration in the straggler window (ratio = measured / predicted)
+ * instead of the dispatch's modeled one; measured_ns < 0 is plain complete(). */
+int gmx_sched_complete_measured(gmx_sched* s, int64_t dispatch_id, int64_t now, int64_t measured_ns,
+                                gmx_complete_view* out);
+/* scheduler.py:237-254 find_stragglers(): stream codes in stream-id order; *n = how many (only the
+ * first `cap` are written). The engine evicts each with gmx_sched_evict_stream. */
+int gmx_sched_find_stragglers(gmx_sched* s, int32_t* streams, int32_t cap, int32_t* n);
 /* scheduler.py:256-278 evict_straggler */
 int gmx_sched_evict_stream(gmx_sched* s, int32_t stream, int64_t now, gmx_evict_view* out);
 /* scheduler.py:195-206 */

@@ -47,9 +47,12 @@ typedef struct gmx_runtime_stats {
     int64_t completed_requests;
     int64_t useful_flops;        /* padding excluded (engine.py:425) */
     int64_t slo_misses;          /* completions after the request deadline */
+    int64_t evicted_requests;    /* requests evicted: straggler streams (engine.py:345-351) + arrivals on them */
+    int64_t cancelled_dispatches;
 } gmx_runtime_stats;
 
-/* Borrows `sched` and `ex` (caller keeps them alive). */
+/* Borrows `sched` and `ex` (caller keeps them alive). ex == NULL (lockstep only): a
+ * decisions-only engine — same event loop, nothing launched (host-cost and parity runs). */
 int gmx_runtime_create(gmx_sched* sched, gmx_exec* ex, int32_t mode, gmx_runtime** out);
 void gmx_runtime_destroy(gmx_runtime* rt);
 /* Queue one request's ARRIVAL (engine.py:316-318) and bind each kernel id to
@@ -75,6 +78,10 @@ int gmx_runtime_set_streams(gmx_runtime* rt, int32_t n);
  * the executor's launch/enqueue path, for host-cost accounting of the serving loop. */
 int gmx_runtime_host_profile(const gmx_runtime* rt, int64_t* ns4);
 int gmx_runtime_set_profiling(gmx_runtime* rt, int32_t on);   /* off by default */
+/* Wall-clock mode: feed the straggler windows with OBSERVED dispatch durations (completion seen
+ * minus launch time) instead of the modeled ones — meaningful once the decision profile / a
+ * measured TuningTable predicts real step times. Off by default. */
+int gmx_runtime_set_measured_stragglers(gmx_runtime* rt, int32_t on);
 int64_t gmx_runtime_clock_ns(const gmx_runtime* rt);
 /* Replay log (realtime mode). Records, in order:
  *   kind 0: complete(dispatch_id=a) at time t      kind 1: add_request(request_id=a) at t

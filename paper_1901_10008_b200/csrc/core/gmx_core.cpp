@@ -16,6 +16,7 @@
 #include "pyexact.hpp"
 
 #include <algorithm>
+#include <deque>
 #include <cstring>
 #include <map>
 #include <new>
@@ -424,6 +425,10 @@ struct gmx_sched {
     // outnumber the live ones, so a long-running scheduler's state stays small and cache-resident
     bool retire = false;
     int64_t n_finished = 0;
+    // straggler detection (scheduler.py:212-222, 237-254): per-stream sliding windows of
+    // observed / predicted dispatch durations; has_win mirrors dict membership
+    std::vector<std::deque<double>> ratio_win;
+    std::vector<char> has_win;
 
     // view storage
     std::vector<gmx_dispatch_rec> v_disp;
@@ -1191,12 +1196,32 @@ int gmx_sched_step(gmx_sched* s, int64_t now, gmx_step_view* out) {
 }
 
 int gmx_sched_complete(gmx_sched* s, int64_t did, int64_t now, gmx_complete_view* out) {
+    return gmx_sched_complete_measured(s, did, now, -1, out);
+}
+
+int gmx_sched_complete_measured(gmx_sched* s, int64_t did, int64_t now, int64_t measured_ns,
+                                gmx_complete_view* out) {
     (void)now;
     if (!s || !out) return fail(GMX_EINVAL, "null argument");
     const int32_t pi = s->inflight_slot.find(did);
     if (pi < 0) return fail(GMX_ENOTFOUND, "unknown dispatch id");
     DispatchRec& d = s->pool[pi];
     s->free_sms += d.rec.sm_allocation;
+    {   // scheduler.py:212, 219-222: ratio = duration / max(predicted, 1), one window per stream
+        const int64_t dur = measured_ns >= 0 ? measured_ns : d.rec.duration;
+        const double ratio = true_div((u128)(dur < 0 ? 0 : dur), (u128)std::max<int64_t>(d.rec.predicted_duration, 1));
+        const size_t win = (size_t)std::max<int64_t>(1, s->params.eviction_window);
+        if (s->ratio_win.size() < s->stream_names.size()) {
+            s->ratio_win.resize(s->stream_names.size());
+            s->has_win.resize(s->stream_names.size(), 0);
+        }
+        for (int32_t st : d.streams) {
+            auto& w = s->ratio_win[st];
+            s->has_win[st] = 1;
+            w.push_back(ratio);
+            if (w.size() > win) w.pop_front();   // deque(maxlen=eviction_window)
+        }
+    }
     s->v_ids_a.clear();  // kernel ids
     s->v_ids_b.clear();  // finished requests
     s->v_ids_c.clear();  // unlocked kernels
@@ -1226,6 +1251,32 @@ int gmx_sched_complete(gmx_sched* s, int64_t did, int64_t now, gmx_complete_view
         compact(s);
         s->n_finished = 0;
     }
+    return GMX_OK;
+}
+
+int gmx_sched_find_stragglers(gmx_sched* s, int32_t* out_streams, int32_t cap, int32_t* n_out) {
+    if (!s || !n_out) return fail(GMX_EINVAL, "null argument");
+    // scheduler.py:237-254: streams with a window, in sorted stream-id order, not evicted, whose
+    // nearest-rank p99 ratio exceeds the threshold (None while the window is short)
+    std::vector<int32_t> order;
+    for (int32_t st = 0; st < (int32_t)s->has_win.size(); ++st)
+        if (s->has_win[st]) order.push_back(st);
+    std::sort(order.begin(), order.end(), [s](int32_t a, int32_t b) { return s->stream_less(a, b); });
+    int32_t n = 0;
+    std::vector<double> sorted;
+    for (int32_t st : order) {
+        if (s->evicted_stream[st]) continue;
+        const auto& w = s->ratio_win[st];
+        if ((int64_t)w.size() < s->params.eviction_min_samples || w.empty()) continue;
+        sorted.assign(w.begin(), w.end());
+        std::sort(sorted.begin(), sorted.end());
+        const int64_t rank = std::max<int64_t>(1, py_ceil(0.99 * (double)sorted.size()));
+        if (sorted[rank - 1] > s->params.straggler_threshold) {
+            if (n < cap && out_streams) out_streams[n] = st;
+            ++n;
+        }
+    }
+    *n_out = n;
     return GMX_OK;
 }
 

@@ -83,12 +83,16 @@ struct gmx_runtime {
         cudaEvent_t ev;                  // launch per step: event after the launch
         std::vector<int64_t> dispatch_ids;
         int64_t seq;                     // resident executor: step queue position (ev unused)
+        int64_t start;                   // runtime clock at launch (measured durations)
     };
     std::deque<InFlight> inflight;
     std::vector<cudaStream_t> streams;   // realtime: launches round-robin over these
     int64_t prof_ns[4] = {0, 0, 0, 0};   // host time in add_request / step / complete / launch
     bool prof_on = false;                // gmx_runtime_set_profiling (clock reads cost ~1 us/round)
+    bool measured_ratios = false;        // realtime: straggler windows get observed durations
     int64_t last_seq = -1;               // resident executor: queue position of the last step
+    gmx::IdMap cancelled;                // dispatch ids cancelled by straggler eviction
+    std::vector<int32_t> straggler_buf;
     size_t next_stream = 0;
     std::vector<cudaEvent_t> event_pool;
     std::vector<gmx_replay_rec> log;
@@ -124,8 +128,9 @@ extern "C" {
 const char* gmx_runtime_last_error(void) { return g_err.c_str(); }
 
 int gmx_runtime_create(gmx_sched* sched, gmx_exec* ex, int32_t mode, gmx_runtime** out) {
-    if (!sched || !ex || !out) return fail(GMX_EINVAL, "null argument");
+    if (!sched || !out) return fail(GMX_EINVAL, "null argument");
     if (mode != GMX_RT_LOCKSTEP && mode != GMX_RT_REALTIME) return fail(GMX_EINVAL, "unsupported runtime mode");
+    if (!ex && mode == GMX_RT_REALTIME) return fail(GMX_EINVAL, "wall-clock mode needs an executor");
     auto* rt = new gmx_runtime();
     rt->sched = sched;
     rt->ex = ex;
@@ -165,6 +170,12 @@ int gmx_runtime_set_origin(gmx_runtime* rt, int64_t ns) {
     if (!rt) return fail(GMX_EINVAL, "null argument");
     rt->origin_ns = ns;
     rt->origin_set = true;
+    return GMX_OK;
+}
+
+int gmx_runtime_set_measured_stragglers(gmx_runtime* rt, int32_t on) {
+    if (!rt) return fail(GMX_EINVAL, "null argument");
+    rt->measured_ratios = on != 0;
     return GMX_OK;
 }
 
@@ -243,6 +254,32 @@ int gmx_runtime_submit(gmx_runtime* rt, int64_t rid, int32_t stream, int64_t arr
     return GMX_OK;
 }
 
+// engine.py:345-351: after the events at `now` are drained and before the step, every stream
+// whose straggler ratio exceeds the threshold is evicted; its cancelled dispatches' completion
+// events are ignored and its requests leave (evicted, not completed).
+static int evict_stragglers(gmx_runtime* rt, int64_t now) {
+    int32_t n = 0;
+    int rc = gmx_sched_find_stragglers(rt->sched, nullptr, 0, &n);
+    if (rc || n == 0) return rc ? fail(rc, std::string("stragglers: ") + gmx_last_error()) : GMX_OK;
+    rt->straggler_buf.resize((size_t)n);
+    if ((rc = gmx_sched_find_stragglers(rt->sched, rt->straggler_buf.data(), n, &n)))
+        return fail(rc, std::string("stragglers: ") + gmx_last_error());
+    for (int32_t st : rt->straggler_buf) {
+        gmx_evict_view ev;
+        if ((rc = gmx_sched_evict_stream(rt->sched, st, now, &ev))) return fail(rc, std::string("evict: ") + gmx_last_error());
+        for (int32_t i = 0; i < ev.n_cancelled; ++i) {
+            rt->cancelled.put(ev.cancelled_dispatch_ids[i], 1);
+            ++rt->st.cancelled_dispatches;
+        }
+        for (int32_t i = 0; i < ev.n_evicted; ++i) {
+            ++rt->st.evicted_requests;
+            release_request(rt, ev.evicted_request_ids[i]);
+        }
+        log_rec(rt, 6, now, st);
+    }
+    return GMX_OK;
+}
+
 static int on_finished(gmx_runtime* rt, const gmx_complete_view& cv, int64_t now) {
     for (int32_t i = 0; i < cv.n_finished; ++i) {
         const int64_t r = cv.finished_request_ids[i];
@@ -272,7 +309,10 @@ static int on_arrival(gmx_runtime* rt, int64_t rid) {
                                    rt->pred.data(), &accepted);
     if (rt->prof_on) rt->prof_ns[0] += steady_ns() - t_add;
     if (rc) return fail(rc, std::string("add_request: ") + gmx_last_error());
-    if (!accepted) release_request(rt, rid);
+    if (!accepted) {   // stream already evicted (engine.py:338-342, "stream-evicted")
+        ++rt->st.evicted_requests;
+        release_request(rt, rid);
+    }
     return GMX_OK;
 }
 
@@ -310,7 +350,7 @@ static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool real
             for (int32_t j = 0; j < r.n_kernels; ++j) {
                 const int64_t kid = v.dispatch_kernel_ids[r.kernel_offset + j];
                 const int32_t slot = rt->slot_of.find(kid);
-                if (slot < 0) return fail(GMX_ESTATE, "dispatched kernel has no operands bound");
+                if (slot < 0 && rt->ex) return fail(GMX_ESTATE, "dispatched kernel has no operands bound");
                 independent &= (slot & kHasDeps) == 0;
                 rt->launch_slots.push_back(slot & ~kHasDeps);
                 rt->slot_of.erase(kid);
@@ -335,9 +375,10 @@ static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool real
         // dependencies go to the executor as the producers' slots: a per-step launch becomes
         // dependent, a resident step waits only for the steps that wrote those slots
         int64_t seq = -1;
-        rc = gmx_exec_launch_deps(rt->ex, rt->launch_slots.data(), (int32_t)rt->launch_slots.size(),
-                                  rt->launch_deps.data(), (int32_t)rt->launch_deps.size(), stream,
-                                  independent ? GMX_LAUNCH_INDEPENDENT : 0, &seq);
+        rc = rt->ex ? gmx_exec_launch_deps(rt->ex, rt->launch_slots.data(), (int32_t)rt->launch_slots.size(),
+                                           rt->launch_deps.data(), (int32_t)rt->launch_deps.size(), stream,
+                                           independent ? GMX_LAUNCH_INDEPENDENT : 0, &seq)
+                    : GMX_OK;   // decisions-only runtime (no executor): nothing to launch
         rt->last_seq = seq;
         if (rt->prof_on) rt->prof_ns[3] += steady_ns() - t_l;
         if (rc) return fail(rc, std::string("launch: ") + gmx_exec_last_error());
@@ -396,8 +437,14 @@ static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtim
                 if (q != cudaSuccess) return fail(GMX_ECUDA, std::string("launch failed: ") + cudaGetErrorString(q));
             }
             for (int64_t did : rt->inflight[i].dispatch_ids) {
+                if (rt->cancelled.find(did) >= 0) {
+                    rt->cancelled.erase(did);
+                    continue;
+                }
                 gmx_complete_view cv;
-                int rc = gmx_sched_complete(rt->sched, did, now, &cv);
+                int rc = rt->measured_ratios
+                             ? gmx_sched_complete_measured(rt->sched, did, now, now - rt->inflight[i].start, &cv)
+                             : gmx_sched_complete(rt->sched, did, now, &cv);
                 if (rc) return fail(rc, std::string("complete: ") + gmx_last_error());
                 log_rec(rt, 0, now, did);
                 on_finished(rt, cv, now);
@@ -417,6 +464,8 @@ static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtim
             any = true;
         }
         if (any) {
+            int rc0 = evict_stragglers(rt, now);
+            if (rc0) return rc0;
             ids.clear();
             void* launch_stream = stream;
             if (!rt->streams.empty()) {
@@ -426,7 +475,7 @@ static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtim
             int rc = step_and_launch(rt, now, launch_stream, true, &ids);
             if (rc) return rc;
             if (!ids.empty() && rt->last_seq >= 0) {   // resident executor: no events needed
-                rt->inflight.push_back({nullptr, ids, rt->last_seq});
+                rt->inflight.push_back({nullptr, ids, rt->last_seq, now});
             } else if (!ids.empty()) {
                 cudaEvent_t ev;
                 if (!rt->event_pool.empty()) {
@@ -436,7 +485,7 @@ static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtim
                     return fail(GMX_ECUDA, "cudaEventCreate failed");
                 }
                 if (cudaEventRecord(ev, cs) != cudaSuccess) return fail(GMX_ECUDA, "cudaEventRecord failed");
-                rt->inflight.push_back({ev, ids, -1});
+                rt->inflight.push_back({ev, ids, -1, now});
                 if (!rt->streams.empty()) rt->next_stream = (rt->next_stream + 1) % rt->streams.size();
             }
             continue;
@@ -457,6 +506,10 @@ int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* stream, gmx_runtime_st
         while (peek_event(rt) && peek_event(rt)->time == now) {
             const Event e = pop_event(rt);
             if (e.kind == kComplete) {
+                if (rt->cancelled.find(e.id) >= 0) {   // engine.py:326-327
+                    rt->cancelled.erase(e.id);
+                    continue;
+                }
                 gmx_complete_view cv;
                 const int64_t t_c = rt->prof_on ? steady_ns() : 0;
                 int rc = gmx_sched_complete(rt->sched, e.id, now, &cv);
@@ -468,7 +521,9 @@ int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* stream, gmx_runtime_st
                 if (rc) return rc;
             }
         }
-        int rc = step_and_launch(rt, now, stream, false, nullptr);
+        int rc = evict_stragglers(rt, now);
+        if (rc) return rc;
+        rc = step_and_launch(rt, now, stream, false, nullptr);
         if (rc) return rc;
     }
     if (out) *out = rt->st;

@@ -33,7 +33,7 @@ class ReplayRec(C.Structure):
 class RuntimeStats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("now", "steps", "launches", "dispatches", "kernels",
                                          "withheld", "completed_requests", "useful_flops",
-                                         "slo_misses")]
+                                         "slo_misses", "evicted_requests", "cancelled_dispatches")]
 
 
 RT_SIGNATURES = {
@@ -52,6 +52,7 @@ RT_SIGNATURES = {
     "gmx_runtime_clock_ns": (C.c_int64, [C.c_void_p]),
     "gmx_runtime_host_profile": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "gmx_runtime_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
+    "gmx_runtime_set_measured_stragglers": (C.c_int, [C.c_void_p, C.c_int32]),
     "gmx_runtime_replay_log": (C.c_int, [C.c_void_p, C.POINTER(ReplayRec), C.c_int64,
                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_int64,
                                          C.POINTER(C.c_int64)]),
@@ -106,7 +107,9 @@ class Runtime:
         # tables stay small over long runs (decisions are unchanged)
         _lib.check(core.gmx_sched_set_retire(h, 1 if retire else 0))
         rt = C.c_void_p()
-        _check(_rt_lib().gmx_runtime_create(h, executor._h, MODES[mode], C.byref(rt)))
+        # executor None: decisions-only engine (lockstep; nothing is launched)
+        _check(_rt_lib().gmx_runtime_create(h, executor._h if executor is not None else None,
+                                            MODES[mode], C.byref(rt)))
         self.mode = mode
         self._rt = rt
         self._codes = {}
@@ -154,10 +157,17 @@ class Runtime:
                                             int(deadline), descs, int(n), dep_arr, off, slots))
 
     def run(self, until=(1 << 62), stream=None) -> dict:
-        s = stream if stream is not None else torch.cuda.current_stream(self.ex.device)
-        _check(_rt_lib().gmx_runtime_run(self._rt, int(until), C.c_void_p(s.cuda_stream),
-                                         C.byref(self._stats)))
+        if self.ex is None:   # decisions-only engine
+            handle = None
+        else:
+            s = stream if stream is not None else torch.cuda.current_stream(self.ex.device)
+            handle = s.cuda_stream
+        _check(_rt_lib().gmx_runtime_run(self._rt, int(until), C.c_void_p(handle), C.byref(self._stats)))
         return {n: getattr(self._stats, n) for n, _ in RuntimeStats._fields_}
+
+    def set_measured_stragglers(self, on: bool):
+        """Wall-clock mode: straggler windows get observed durations."""
+        _check(_rt_lib().gmx_runtime_set_measured_stragglers(self._rt, 1 if on else 0))
 
     def set_profiling(self, on: bool):
         """Accumulate host ns per phase (host_profile); costs ~1 us per C2 round when on."""
