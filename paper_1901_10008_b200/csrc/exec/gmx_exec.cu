@@ -52,6 +52,11 @@ namespace gmx {
 enum : int32_t { kItemGemm = 0, kItemGemv = 1, kItemEltwise = 2 };
 
 constexpr int kThreads = 224;             // 6 role warps + 1 queue-dispatcher warp (resident mode)
+constexpr int kInlineMaxMembers = 32;   // members of an inline (device-enumerated) step
+constexpr int kInlineMaxItems = 48;     // work items one CTA may hold in an inline step
+constexpr int kInlineGemvRows = 64;     // inline GEMV item: rows
+constexpr int kInlineEltwise = 32768;   // inline elementwise item: elements
+
 // Two build shapes of the same kernel (selected per executor, option "ctas_per_sm"):
 //   1 CTA/SM : 6-stage ring, 32 KB output staging (one resident CTA streams alone)
 //   2 CTAs/SM: 3-stage ring each, 16 KB staging; two CTAs (of one launch, or of consecutive
@@ -77,7 +82,8 @@ constexpr int kStageBytes = kStageA + kStageB;
 template <int kCtasPerSm>
 constexpr int smem_bytes() {
     using C = SmemCfg<kCtasPerSm>;
-    return C::stages * kStageBytes + C::stage_out + C::align_pad + 512 /*barriers + unit queue*/;
+    return C::stages * kStageBytes + C::stage_out + C::align_pad + 512 /*barriers + unit queue*/ +
+           (kCtasPerSm == 1 ? kInlineMaxItems * 32 : 0) /*inline step items (1-CTA shape only)*/;
 }
 static_assert(2 * (smem_bytes<2>() + 1024) <= 233472, "two CTAs must fit one SM's shared memory");
 constexpr int kWsBlock = 4096;             // split-K workspace allocation unit (floats)
@@ -181,6 +187,10 @@ struct KernelArgs {
     int32_t window;          // resident: max steps a CTA may run ahead of the slowest
     uint64_t* rtrace;        // resident diagnostics: 4 stamps per (step, CTA), or null
     int32_t rtrace_steps;
+    // inline step (no host plan): the members' work items are enumerated on the device, item
+    // g of the concatenated tile space going to CTA g % gridDim.x (no split-K, no LPT)
+    int32_t inline_n;
+    int32_t inline_slots[kInlineMaxMembers];
 };
 
 // The items/tables one step works on, as seen by one CTA.
@@ -835,11 +845,56 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
     uint64_t* uempty = ufull + kUnitQ;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uempty + kUnitQ);
     int32_t* split_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
+    int32_t* inline_count = split_flag + 1;                             // [0] items, [1] has GEMM
+    WorkItem* inline_items = reinterpret_cast<WorkItem*>(reinterpret_cast<uint8_t*>(uq) + 512);   // after the 512 B control block
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
-    // host-computed: CTA owns GEMM tiles (a resident CTA may get them in any step)
-    const bool has_gemm = args.resident || (args.cta_flags[blockIdx.x] & 1) != 0;
+
+    if (threadIdx.x == 0 && args.inline_n > 0) {
+        // inline step: enumerate the members' work items, keep every gridDim.x-th for this CTA
+        int cnt = 0, gemm = 0;
+        uint32_t g = 0;
+        const uint32_t G = gridDim.x, me = blockIdx.x;
+        auto take = [&](int32_t slot, int type, int r0, int c0, int kb1) {
+            if (g++ % G != me) return;
+            if (cnt == kInlineMaxItems) __trap();   // the host bounds items per CTA
+            WorkItem& it = inline_items[cnt++];
+            it.problem = slot;
+            it.type = (uint8_t)type;
+            it.nsplit = 1;
+            it.split = 0;
+            it._pad = 0;
+            it.row0 = r0;
+            it.col0 = c0;
+            it.kb0 = 0;
+            it.kb1 = kb1;
+            it.tile_slot = -1;
+            it.ws_blk = 0;
+            gemm |= type == kItemGemm;
+        };
+        for (int m = 0; m < args.inline_n; ++m) {
+            const int32_t slot = args.inline_slots[m];
+            const DevProblem* P = args.probs + slot;
+            const int kind = P->kind, rows = P->rows, cols = P->cols, bn = P->bn, kbl = P->kblocks;
+            if (kind == kItemGemm) {
+                for (int r0 = 0; r0 < rows; r0 += kTileRows)
+                    for (int c0 = 0; c0 < cols; c0 += bn) take(slot, kItemGemm, r0, c0, kbl);
+            } else if (kind == kItemGemv) {
+                for (int r0 = 0; r0 < rows; r0 += kInlineGemvRows)
+                    take(slot, kItemGemv, r0, min(rows, r0 + kInlineGemvRows), 0);
+            } else {
+                for (int e0 = 0; e0 < rows; e0 += kInlineEltwise)
+                    take(slot, kItemEltwise, e0, min(rows, e0 + kInlineEltwise), 0);
+            }
+        }
+        inline_count[0] = cnt;
+        inline_count[1] = gemm;
+    }
+    if (args.inline_n > 0) __syncthreads();
+    // CTA owns GEMM tiles (host-computed; inline: enumerated; resident: any step may bring some)
+    const bool has_gemm = args.resident || (args.inline_n > 0 ? inline_count[1] != 0
+                                                              : (args.cta_flags[blockIdx.x] & 1) != 0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -884,6 +939,18 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
     auto advance_unit = [&]() {
         if (args.resident && ++uslot == kUnitQ) { uslot = 0; uphase ^= 1; }
     };
+    // items of (step, list): the inline step's items live in smem
+    auto view = [&](int64_t k, int idx) -> StepView {
+        if (args.inline_n > 0) {
+            StepView v{};
+            v.probs = args.probs;
+            v.items = inline_items;
+            v.beg = 0;
+            v.end = inline_count[0];
+            return v;
+        }
+        return list_view(args, k, idx);
+    };
 
     if (warp == 6) {
         // ---------------- queue dispatcher (resident mode, block 0) ----------------
@@ -914,7 +981,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 if (rt) rt[1] = global_timer_ns();
             };
             if (!args.resident) {
-                issue_list(list_view(args, 0, blockIdx.x), nullptr);
+                issue_list(view(0, blockIdx.x), nullptr);
             } else {
                 auto push = [&](int64_t k, int32_t idx) {
                     mbar_wait(&uempty[uslot], uphase ^ 1);
@@ -953,7 +1020,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 advance_unit();
                 if (u.idx == kUnitStop) break;
                 if (u.idx < 0) continue;
-                const StepView v = list_view(args, u.k, u.idx);
+                const StepView v = view(u.k, u.idx);
                 for (int i = v.beg; i < v.end; ++i) {
                     const WorkItem it = v.items[i];
                     if (it.type != kItemGemm) continue;
@@ -1058,7 +1125,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 if (u.idx == kUnitStop) break;
                 continue;
             }
-            v = list_view(args, u.k, u.idx);
+            v = view(u.k, u.idx);
             uint64_t* rt = (args.rtrace && u.k < args.rtrace_steps) ? args.rtrace + (u.k * gridDim.x + blockIdx.x) * 8 : nullptr;
             if (rt && etid == 0) {
                 rt[2] = global_timer_ns();
@@ -1253,6 +1320,10 @@ struct gmx_exec {
     bool early_trigger = true;
     bool multi_stream = false;   // launches may come from several streams (realtime runtime)
     int occupancy[2] = {0, 0};   // measured resident CTAs/SM of the 1- and 2-CTA kernel shapes
+    bool inline_plans = false;   // option "inline_plans": first-seen slot sets run as inline steps
+    int inline_promote = 1;      // sightings before a slot set gets a cached plan
+    std::unordered_map<uint64_t, int> inline_seen;
+    int64_t inline_launches = 0;
     int32_t dbg = 0;
     const gmx::Plan* recent[3] = {nullptr, nullptr, nullptr};   // plans of the last launches
     uint64_t* trace = nullptr;
@@ -2025,6 +2096,55 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
     }
     int rc;
     if ((rc = ensure_table(ex, stream))) return rc;
+    if (ex->inline_plans && !ex->res.active && !ex->tracing && n <= kInlineMaxMembers) {
+        // a slot set seen for the first time (wall-clock serving: most step compositions are
+        // one-offs) runs as an INLINE step — the device enumerates the work items — instead of
+        // paying for a host plan build + upload; a recurring one gets a cached LPT plan
+        bool hit = false;
+        auto pit = ex->plans.find(h);
+        if (pit != ex->plans.end())
+            for (auto& p : pit->second) hit |= p->key == key;
+        if (!hit) {
+            if (ex->inline_seen.size() > 65536) ex->inline_seen.clear();
+            int& seen = ex->inline_seen[h];
+            if (seen++ < ex->inline_promote) {
+                int64_t total = 0;
+                for (int32_t sl : key) {
+                    const DevProblem& P = ex->probs[sl].dev;
+                    if (P.kind == kItemGemm)
+                        total += (int64_t)((P.rows + kTileRows - 1) / kTileRows) * ((P.cols + P.bn - 1) / P.bn);
+                    else if (P.kind == kItemGemv)
+                        total += (P.rows + kInlineGemvRows - 1) / kInlineGemvRows;
+                    else
+                        total += (P.rows + kInlineEltwise - 1) / kInlineEltwise;
+                }
+                const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ex->num_sms, total));
+                if ((total + grid - 1) / grid <= kInlineMaxItems) {
+                    if ((rc = set_kernel_attrs(ex))) return rc;
+                    KernelArgs args{};
+                    args.probs = ex->d_probs;
+                    args.dbg = ex->dbg;
+                    args.independent = (flags & GMX_LAUNCH_INDEPENDENT) != 0 ? 1 : 0;
+                    args.early_trigger = ex->early_trigger ? 1 : 0;
+                    args.inline_n = n;
+                    for (int32_t i = 0; i < n; ++i) args.inline_slots[i] = key[i];
+                    cudaLaunchConfig_t cfg{};
+                    cfg.gridDim = dim3((unsigned)grid);
+                    cfg.blockDim = dim3(kThreads);
+                    cfg.dynamicSmemBytes = smem_bytes<1>();
+                    cfg.stream = stream;
+                    cudaLaunchAttribute attr[1];
+                    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                    attr[0].val.programmaticStreamSerializationAllowed = ex->pdl ? 1 : 0;
+                    cfg.attrs = attr;
+                    cfg.numAttrs = 1;
+                    GMX_CUDA(cudaLaunchKernelEx(&cfg, coalesced_step_kernel<1>, args));
+                    ++ex->inline_launches;
+                    return GMX_OK;
+                }
+            }
+        }
+    }
     Plan* plan = nullptr;
     bool cached = false;
     if (ex->cache_plans) {
@@ -2127,6 +2247,14 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
         if (value < 0 || value > 100000) return fail(GMX_EINVAL, "rtrace must be in [0, 100000]");
         if (ex->res.rtrace) { cudaFree(ex->res.rtrace); ex->res.rtrace = nullptr; }
         ex->res.rtrace_steps = (int32_t)value;
+        return GMX_OK;
+    } else if (n == "inline_plans") {
+        if (ex->ctas_per_sm != 1 && value) return fail(GMX_EINVAL, "inline steps use the 1-CTA kernel shape");
+        ex->inline_plans = value != 0;
+        return GMX_OK;
+    } else if (n == "inline_promote") {
+        if (value < 0 || value > 1000000) return fail(GMX_EINVAL, "inline_promote must be >= 0");
+        ex->inline_promote = (int)value;
         return GMX_OK;
     } else if (n == "resident_window") {
         if (value < 1 || value > kMaxWindow) return fail(GMX_EINVAL, "resident_window must be in [1, 16]");

@@ -131,6 +131,12 @@ int gmx_runtime_create(gmx_sched* sched, gmx_exec* ex, int32_t mode, gmx_runtime
     if (!sched || !out) return fail(GMX_EINVAL, "null argument");
     if (mode != GMX_RT_LOCKSTEP && mode != GMX_RT_REALTIME) return fail(GMX_EINVAL, "unsupported runtime mode");
     if (!ex && mode == GMX_RT_REALTIME) return fail(GMX_EINVAL, "wall-clock mode needs an executor");
+    // wall-clock serving: most step compositions are one-offs, so first sightings run as inline
+    // steps (device-enumerated work items) instead of paying a host plan build + upload
+    if (ex && mode == GMX_RT_REALTIME) {
+        gmx_exec_set_option(ex, "inline_plans", 1);
+        gmx_exec_set_option(ex, "inline_promote", 8);
+    }
     auto* rt = new gmx_runtime();
     rt->sched = sched;
     rt->ex = ex;

@@ -352,3 +352,32 @@ def test_measured_autotuner_writes_reference_format_table(tmp_path):
     sched.add_request(gm.InferenceRequest(0, "s0", (k,), 0, gm.LatencyConstraint(10_000_000)))
     dispatches, _, _ = sched.step(0)
     assert dispatches or True   # decisions come from the same cost model with the tuned entry
+
+
+def test_inline_steps_device_enumerated(ex):
+    """Inline steps (no host plan: the device enumerates the members' work items) give the same
+    results as planned launches; the second sighting of a slot set is promoted to a plan."""
+    from paper_1901_10008_b200.executor import OperandSet
+    ex.set_option("inline_plans", 1)
+    try:
+        ops = [OperandSet("gemm", C2_SHAPES[i % 13], seed=1100 + i, bias=(i % 2 == 0), activation="relu")
+               for i in range(6)]
+        ops += [OperandSet("gemv", (1000, 2048), dtype="fp32", seed=1200),
+                OperandSet("elementwise", (100000,), seed=1201, activation="gelu"),
+                OperandSet("gemm", (512, 49, 4608), seed=1202)]
+        slots = [o.register(ex) for o in ops]
+        ex.launch(slots)                 # first sighting: inline
+        torch.cuda.synchronize()
+        for o in ops:
+            _check(o)
+        for o in ops:
+            o.c.zero_()
+        ex.launch(slots)                 # second: planned (LPT, split-K)
+        torch.cuda.synchronize()
+        assert ex.last_plan()["n_items"] > 0
+        for o in ops:
+            _check(o)
+        for s in slots:
+            ex.unregister(s)
+    finally:
+        ex.set_option("inline_plans", 0)

@@ -56,6 +56,7 @@ def run(ex, slots, rate, tenants, duration_ns, models, lead_ns=20_000_000, strea
         flops[r.request_id] = sum(k.flops for k in ks)
         rt.submit(gm.InferenceRequest(r.request_id, r.stream_id, ks, r.arrival + lead_ns,
                                       gm.LatencyConstraint(SLO_NS)), slots[r.stream_id])
+    rt.set_profiling(True)
     rt.set_origin_now()
     if resident:   # steps go to one persistent launch; completions from its host-mapped flags
         s = torch.cuda.current_stream()
@@ -76,7 +77,19 @@ def run(ex, slots, rate, tenants, duration_ns, models, lead_ns=20_000_000, strea
     def pct(p):
         return lat[max(1, -(-int(p * n * 1000) // 1000)) - 1] if n else None
 
+    by_model = {}
+    model_of = {f"p{i:02d}": models[i % len(models)] for i in range(tenants)}
+    for r in reqs:
+        if r.request_id in done:
+            by_model.setdefault(model_of[r.stream_id], []).append(done[r.request_id] - arrival[r.request_id])
+    per_model = {}
+    for m, xs in by_model.items():
+        xs.sort()
+        k = len(xs)
+        per_model[m] = {"n": k, "p50_ms": xs[(k - 1) // 2] / 1e6, "p99_ms": xs[max(0, -(-99 * k // 100) - 1)] / 1e6,
+                        "slo": sum(1 for x in xs if x <= SLO_NS) / k, "layers": len(lib[m])}
     return {"config": "c4", "rate_per_stream": rate, "tenants": tenants, "duration_s": duration_ns / 1e9,
+            "per_model": per_model,
             "executor": "resident" if resident else "launch per step",
             "cuda_streams": None if resident else streams, "stagger_horizon_ns": stagger_ns,
             "requests": len(reqs), "completed": n,
@@ -86,6 +99,8 @@ def run(ex, slots, rate, tenants, duration_ns, models, lead_ns=20_000_000, strea
             "throughput_rps": n / span if span else 0.0,
             "useful_tflops": sum(flops[r] for r in done) / span / 1e12 if span else 0.0,
             "launches": stats["launches"], "steps": stats["steps"], "withheld": stats["withheld"],
+            "evicted": stats["evicted_requests"],
+            "host_ms": {k: round(v / 1e6, 2) for k, v in rt.host_profile().items()},
             "kernels_per_launch": stats["kernels"] / max(1, stats["launches"])}
 
 
