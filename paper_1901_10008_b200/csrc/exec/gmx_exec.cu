@@ -36,6 +36,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstddef>
 #include <cstdlib>
 #include <map>
 #include <memory>
@@ -82,8 +83,7 @@ constexpr int kStageBytes = kStageA + kStageB;
 template <int kCtasPerSm>
 constexpr int smem_bytes() {
     using C = SmemCfg<kCtasPerSm>;
-    return C::stages * kStageBytes + C::stage_out + C::align_pad + 512 /*barriers + unit queue*/ +
-           (kCtasPerSm == 1 ? kInlineMaxItems * 32 : 0) /*inline step items (1-CTA shape only)*/;
+    return C::stages * kStageBytes + C::stage_out + C::align_pad + 512 /*barriers + unit queue*/;
 }
 static_assert(2 * (smem_bytes<2>() + 1024) <= 233472, "two CTAs must fit one SM's shared memory");
 constexpr int kWsBlock = 4096;             // split-K workspace allocation unit (floats)
@@ -152,9 +152,13 @@ struct StepDesc {
     int32_t nwait;            // entries of wait_steps in use
     int64_t wait_steps[4];    // earlier steps that must be complete first: producers of this
                               // step's inputs, users of its plan (split-K state) or slots (outputs)
-    int64_t _pad[5];
+    int32_t inline_n;         // > 0: inline step (no plan): items enumerated from these slots
+    int32_t inline_slots[kInlineMaxMembers];
+    int32_t _pad[9];
 };
-static_assert(sizeof(StepDesc) == 128, "StepDesc layout");
+static_assert(sizeof(StepDesc) == 256, "StepDesc layout");
+static_assert(offsetof(StepDesc, inline_n) < 96 && offsetof(StepDesc, inline_slots) == 92,
+              "the dispatcher relays a 96-byte head that includes inline_n");
 constexpr int kStepVec = (int)(sizeof(StepDesc) / 16);
 
 struct DevQueue {
@@ -201,7 +205,94 @@ struct StepView {
     int32_t* counters;
     int beg, end;
     bool stop;
+    // inline step: list `idx` holds the members' virtual items g with g % G == idx
+    int inl_n;
+    const int32_t* inl_slots;
+    int idx;
+    uint32_t G;
 };
+
+// Walks one list's work items: a planned list's array, or an inline step's virtual items
+// (each member's 128 x BN tiles / 64-row GEMV blocks / 32K-element chunks, concatenated).
+// Apply f(item, index) to every work item of a list; the planned-array and inline paths are
+// separate instantiations of f, so a planned list pays nothing for the inline enumeration.
+struct ItemCursor;
+__device__ __forceinline__ ItemCursor item_begin(const StepView& v);
+__device__ __forceinline__ bool next_item(const StepView& v, ItemCursor& c, WorkItem& it);
+template <typename F>
+__device__ __forceinline__ void for_each_item(const StepView& v, F&& f);
+
+struct ItemCursor {
+    int i;        // planned: next index
+    int m, u;     // inline: member, unit within member
+    uint32_t g;   // inline: global virtual item index
+};
+__device__ __forceinline__ ItemCursor item_begin(const StepView& v) { return ItemCursor{v.beg, 0, 0, 0u}; }
+__device__ __forceinline__ bool next_item(const StepView& v, ItemCursor& c, WorkItem& it) {
+    if (v.inl_n == 0) {
+        if (c.i >= v.end) return false;
+        it = v.items[c.i++];
+        return true;
+    }
+    while (c.m < v.inl_n) {
+        const int32_t slot = v.inl_slots[c.m];
+        const DevProblem* P = v.probs + slot;
+        const int kind = P->kind, rows = P->rows;
+        int units, per_row = 1;
+        if (kind == kItemGemm) {
+            per_row = (P->cols + P->bn - 1) / P->bn;
+            units = ((rows + kTileRows - 1) / kTileRows) * per_row;
+        } else if (kind == kItemGemv) {
+            units = (rows + kInlineGemvRows - 1) / kInlineGemvRows;
+        } else {
+            units = (rows + kInlineEltwise - 1) / kInlineEltwise;
+        }
+        while (c.u < units) {
+            const uint32_t gg = c.g++;
+            const int u = c.u++;
+            if (gg % v.G != (uint32_t)v.idx) continue;
+            it.problem = slot;
+            it.type = (uint8_t)kind;
+            it.nsplit = 1;
+            it.split = 0;
+            it._pad = 0;
+            it.kb0 = 0;
+            it.tile_slot = -1;
+            it.ws_blk = 0;
+            if (kind == kItemGemm) {
+                it.row0 = (u / per_row) * kTileRows;
+                it.col0 = (u % per_row) * P->bn;
+                it.kb1 = P->kblocks;
+            } else if (kind == kItemGemv) {
+                it.row0 = u * kInlineGemvRows;
+                it.col0 = min(rows, it.row0 + kInlineGemvRows);
+                it.kb1 = 0;
+            } else {
+                it.row0 = u * kInlineEltwise;
+                it.col0 = min(rows, it.row0 + kInlineEltwise);
+                it.kb1 = 0;
+            }
+            return true;
+        }
+        ++c.m;
+        c.u = 0;
+    }
+    return false;
+}
+
+template <typename F>
+__device__ __forceinline__ void for_each_item(const StepView& v, F&& f) {
+    if (v.inl_n == 0) {
+        for (int i = v.beg; i < v.end; ++i) {
+            const WorkItem it = v.items[i];
+            f(it, i);
+        }
+    } else {
+        ItemCursor c = item_begin(v);
+        WorkItem it;
+        while (next_item(v, c, it)) f(it, -1);
+    }
+}
 
 __device__ __forceinline__ int64_t ld_acquire_gpu_s64(const int64_t* p) {
     int64_t v;
@@ -714,11 +805,27 @@ __device__ __forceinline__ StepView list_view(const KernelArgs& a, int64_t k, in
     StepView v{};
     if (!a.resident) {
         v.probs = a.probs; v.items = a.items; v.ws = a.ws; v.counters = a.counters;
+        if (a.inline_n > 0) {   // inline launch: the slots are kernel parameters
+            v.inl_n = a.inline_n;
+            v.inl_slots = a.inline_slots;
+            v.idx = idx;
+            v.G = gridDim.x;
+            return v;
+        }
         v.beg = a.cta_off[idx];
         v.end = a.cta_off[idx + 1];
         return v;
     }
     const StepDesc* d = &a.dq->ring[k % kQueue];
+    const int inl = __ldcg(&d->inline_n);
+    if (inl > 0) {   // inline resident step: slots in the device ring entry
+        v.probs = (const DevProblem*)__ldcg((const long long*)&d->probs);
+        v.inl_n = inl;
+        v.inl_slots = d->inline_slots;
+        v.idx = idx;
+        v.G = gridDim.x;
+        return v;
+    }
     v.probs = (const DevProblem*)__ldcg((const long long*)&d->probs);
     v.items = (const WorkItem*)__ldcg((const long long*)&d->items);
     v.ws = (float*)__ldcg((const long long*)&d->ws);
@@ -796,13 +903,17 @@ __device__ void dispatch_steps(const KernelArgs& a) {
             if (global_timer_ns() - t0 > 60000000000ull) __trap();   // host never published
         }
         const int n = (int)(avail - k < kBatch ? avail - k : kBatch);
-        uint4 w[kBatch][kStepVec];
+        // the fixed head of each entry (6 x 16 B: pointers, grid, flags, waits, inline_n and the
+        // first inline slot) for the whole batch in flight together; the rest of an inline
+        // step's slot list only when it has more than one member
+        constexpr int kHead = 6;
+        uint4 w[kBatch][kHead];
 #pragma unroll
         for (int b = 0; b < kBatch; ++b) {
             if (b < n) {
                 const uint4* src = reinterpret_cast<const uint4*>(&a.hring[(k + b) % kQueue]);
 #pragma unroll
-                for (int q = 0; q < kStepVec; ++q)   // system-scope loads of host-written entries (after the acquire)
+                for (int q = 0; q < kHead; ++q)   // system-scope loads of host-written entries (after the acquire)
                     asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                                  : "=r"(w[b][q].x), "=r"(w[b][q].y), "=r"(w[b][q].z), "=r"(w[b][q].w)
                                  : "l"(src + q));
@@ -812,10 +923,24 @@ __device__ void dispatch_steps(const KernelArgs& a) {
 #pragma unroll
         for (int b = 0; b < kBatch; ++b) {
             if (b < n && !stop) {
-                uint4* dst = reinterpret_cast<uint4*>(&a.dq->ring[(k + b) % kQueue]);
+                const int slot = (int)((k + b) % kQueue);
+                uint4* dst = reinterpret_cast<uint4*>(&a.dq->ring[slot]);
 #pragma unroll
-                for (int q = 0; q < kStepVec; ++q) __stcg(dst + q, w[b][q]);
-                stop = reinterpret_cast<const StepDesc*>(w[b])->stop != 0;
+                for (int q = 0; q < kHead; ++q) __stcg(dst + q, w[b][q]);
+                const StepDesc* head = reinterpret_cast<const StepDesc*>(w[b]);
+                const int inl = head->inline_n;
+                if (inl > 1) {
+                    const uint4* src = reinterpret_cast<const uint4*>(&a.hring[slot]);
+                    const int nq = (int)((offsetof(StepDesc, inline_slots) + 4 * inl + 15) / 16);
+                    for (int q = kHead; q < nq; ++q) {
+                        uint4 x;
+                        asm volatile("ld.relaxed.sys.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                                     : "l"(src + q));
+                        __stcg(dst + q, x);
+                    }
+                }
+                stop = head->stop != 0;
             }
         }
         k += n;
@@ -827,7 +952,7 @@ __device__ void dispatch_steps(const KernelArgs& a) {
 
 // Register cap per shape (the 2-CTA shape keeps two CTAs' registers within one SM's 64K).
 template <int kCtasPerSm>
-__global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(const KernelArgs args) {
+__global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(const __grid_constant__ KernelArgs args) {
     using Cfg = SmemCfg<kCtasPerSm>;
     constexpr int kStages = Cfg::stages;
     constexpr int kStageOut = Cfg::stage_out;
@@ -845,56 +970,12 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
     uint64_t* uempty = ufull + kUnitQ;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uempty + kUnitQ);
     int32_t* split_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
-    int32_t* inline_count = split_flag + 1;                             // [0] items, [1] has GEMM
-    WorkItem* inline_items = reinterpret_cast<WorkItem*>(reinterpret_cast<uint8_t*>(uq) + 512);   // after the 512 B control block
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
 
-    if (threadIdx.x == 0 && args.inline_n > 0) {
-        // inline step: enumerate the members' work items, keep every gridDim.x-th for this CTA
-        int cnt = 0, gemm = 0;
-        uint32_t g = 0;
-        const uint32_t G = gridDim.x, me = blockIdx.x;
-        auto take = [&](int32_t slot, int type, int r0, int c0, int kb1) {
-            if (g++ % G != me) return;
-            if (cnt == kInlineMaxItems) __trap();   // the host bounds items per CTA
-            WorkItem& it = inline_items[cnt++];
-            it.problem = slot;
-            it.type = (uint8_t)type;
-            it.nsplit = 1;
-            it.split = 0;
-            it._pad = 0;
-            it.row0 = r0;
-            it.col0 = c0;
-            it.kb0 = 0;
-            it.kb1 = kb1;
-            it.tile_slot = -1;
-            it.ws_blk = 0;
-            gemm |= type == kItemGemm;
-        };
-        for (int m = 0; m < args.inline_n; ++m) {
-            const int32_t slot = args.inline_slots[m];
-            const DevProblem* P = args.probs + slot;
-            const int kind = P->kind, rows = P->rows, cols = P->cols, bn = P->bn, kbl = P->kblocks;
-            if (kind == kItemGemm) {
-                for (int r0 = 0; r0 < rows; r0 += kTileRows)
-                    for (int c0 = 0; c0 < cols; c0 += bn) take(slot, kItemGemm, r0, c0, kbl);
-            } else if (kind == kItemGemv) {
-                for (int r0 = 0; r0 < rows; r0 += kInlineGemvRows)
-                    take(slot, kItemGemv, r0, min(rows, r0 + kInlineGemvRows), 0);
-            } else {
-                for (int e0 = 0; e0 < rows; e0 += kInlineEltwise)
-                    take(slot, kItemEltwise, e0, min(rows, e0 + kInlineEltwise), 0);
-            }
-        }
-        inline_count[0] = cnt;
-        inline_count[1] = gemm;
-    }
-    if (args.inline_n > 0) __syncthreads();
-    // CTA owns GEMM tiles (host-computed; inline: enumerated; resident: any step may bring some)
-    const bool has_gemm = args.resident || (args.inline_n > 0 ? inline_count[1] != 0
-                                                              : (args.cta_flags[blockIdx.x] & 1) != 0);
+    // CTA owns GEMM tiles (host-computed; resident / inline steps: any list may bring some)
+    const bool has_gemm = args.resident || args.inline_n > 0 || (args.cta_flags[blockIdx.x] & 1) != 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -939,18 +1020,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
     auto advance_unit = [&]() {
         if (args.resident && ++uslot == kUnitQ) { uslot = 0; uphase ^= 1; }
     };
-    // items of (step, list): the inline step's items live in smem
-    auto view = [&](int64_t k, int idx) -> StepView {
-        if (args.inline_n > 0) {
-            StepView v{};
-            v.probs = args.probs;
-            v.items = inline_items;
-            v.beg = 0;
-            v.end = inline_count[0];
-            return v;
-        }
-        return list_view(args, k, idx);
-    };
+    auto view = [&](int64_t k, int idx) -> StepView { return list_view(args, k, idx); };
 
     if (warp == 6) {
         // ---------------- queue dispatcher (resident mode, block 0) ----------------
@@ -961,9 +1031,8 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             int stage = 0;
             uint32_t phase = 0;
             auto issue_list = [&](const StepView& v, uint64_t* rt) {
-                for (int i = v.beg; i < v.end; ++i) {
-                    const WorkItem it = v.items[i];
-                    if (it.type != kItemGemm) continue;
+                for_each_item(v, [&](const WorkItem& it, int i) {
+                    if (it.type != kItemGemm) return;
                     const DevProblem* P = v.probs + it.problem;
                     const uint32_t bytes = kStageA + (uint32_t)P->bn * (kBlockK * 2);
                     if (args.trace) args.trace[8 * i + 0] = global_timer_ns();
@@ -977,7 +1046,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                         tma_load_2d(tile + kStageA, &P->tm_cols, &full[stage], kb * kBlockK, it.col0);
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
-                }
+                });
                 if (rt) rt[1] = global_timer_ns();
             };
             if (!args.resident) {
@@ -1021,9 +1090,8 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 if (u.idx == kUnitStop) break;
                 if (u.idx < 0) continue;
                 const StepView v = view(u.k, u.idx);
-                for (int i = v.beg; i < v.end; ++i) {
-                    const WorkItem it = v.items[i];
-                    if (it.type != kItemGemm) continue;
+                for_each_item(v, [&](const WorkItem& it, int i) {
+                    if (it.type != kItemGemm) return;
                     const uint32_t idesc = idesc_bf16_m128((uint32_t)v.probs[it.problem].bn);
                     mbar_wait(&tempty[acc], acc_phase ^ 1);
                     tc_fence_after();
@@ -1045,7 +1113,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     umma_commit(&tfull[acc]);
                     if (args.trace) args.trace[8 * i + 1] = global_timer_ns();
                     if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
-                }
+                });
             }
         }
     } else if (warp >= 2 && warp <= 5) {
@@ -1131,8 +1199,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 rt[2] = global_timer_ns();
                 rt[4] = (uint64_t)(v.end - v.beg);
             }
-            for (int i = v.beg; i < v.end; ++i) {
-                const WorkItem it = v.items[i];
+            for_each_item(v, [&](const WorkItem& it, int i) {
                 const DevProblem* Pg = v.probs + it.problem;
                 if (args.trace && etid == 0 && it.type != kItemGemm) args.trace[8 * i + 0] = global_timer_ns();
                 if (it.type == kItemGemm) {
@@ -1185,7 +1252,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     if (etid == 0) args.trace[8 * i + 3] = global_timer_ns();
                 }
                 if (pend >= 0 && pend != i && ++pend_age >= 1) complete_pending();
-            }
+            });
             if (pend >= 0) complete_pending();
             if (rt && etid == 0) rt[7] = global_timer_ns();
             if (args.resident) {
@@ -1685,12 +1752,14 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
                             int32_t ndep, int32_t flags, bool cached, int64_t* seq_out) {
     auto& r = ex->res;
     int rc;
-    if (!plan->uploaded) {
+    if (plan && !plan->uploaded) {
         if ((rc = upload_plan(ex, *plan, r.upload))) return rc;
         GMX_CUDA(cudaStreamSynchronize(r.upload));
     }
-    plan->stream = r.stream;   // later frees are ordered after the persistent kernel
-    plan->last_use = ++ex->clock;
+    if (plan) {
+        plan->stream = r.stream;   // later frees are ordered after the persistent kernel
+        plan->last_use = ++ex->clock;
+    }
     // Ordering. Steps <= seq - window are complete before this one starts anyway. Inside the
     // window wait for: the producers of the inputs (dep_slots: the last step that wrote each),
     // and the latest step sharing this plan (split-K state) or a slot (outputs). Without
@@ -1713,17 +1782,23 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
         if (sl >= 0 && sl < (int32_t)r.last_write.size()) need(r.last_write[sl]);
     }
     for (size_t i = 0; i < r.recent_keys.size(); ++i)
-        if (r.recent_plans[i] == plan || keys_intersect(r.recent_keys[i], key)) {
+        if ((plan && r.recent_plans[i] == plan) || keys_intersect(r.recent_keys[i], key)) {
             need(r.recent_seq[i]);
             break;
         }
     StepDesc d{};
     d.probs = ex->d_probs;
-    d.items = plan->d_items;
-    d.cta_off = plan->d_off;
-    d.ws = plan->d_ws;
-    d.counters = plan->d_counters;
-    d.grid = plan->stats.grid;
+    if (plan) {
+        d.items = plan->d_items;
+        d.cta_off = plan->d_off;
+        d.ws = plan->d_ws;
+        d.counters = plan->d_counters;
+        d.grid = plan->stats.grid;
+    } else {   // inline step: every CTA list enumerates its share of the members' items
+        d.grid = r.grid;
+        d.inline_n = (int32_t)key.size();
+        for (size_t i = 0; i < key.size(); ++i) d.inline_slots[i] = key[i];
+    }
     d.wait_all = wait_all ? 1 : 0;
     d.nwait = wait_all ? 0 : nw;
     for (int q = 0; q < nw; ++q) d.wait_steps[q] = waits[q];
@@ -1738,8 +1813,10 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
         r.recent_plans.pop_back();
         r.recent_seq.pop_back();
     }
-    plan->stats.cached = cached;
-    ex->last = plan;
+    if (plan) {
+        plan->stats.cached = cached;
+        ex->last = plan;
+    }
     if (seq_out) *seq_out = seq;
     return GMX_OK;
 }
@@ -2096,7 +2173,7 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
     }
     int rc;
     if ((rc = ensure_table(ex, stream))) return rc;
-    if (ex->inline_plans && !ex->res.active && !ex->tracing && n <= kInlineMaxMembers) {
+    if (ex->inline_plans && !ex->tracing && n <= kInlineMaxMembers) {
         // a slot set seen for the first time (wall-clock serving: most step compositions are
         // one-offs) runs as an INLINE step — the device enumerates the work items — instead of
         // paying for a host plan build + upload; a recurring one gets a cached LPT plan
@@ -2119,6 +2196,10 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
                         total += (P.rows + kInlineEltwise - 1) / kInlineEltwise;
                 }
                 const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ex->num_sms, total));
+                if (ex->res.active) {   // resident: the slots ride in the step descriptor
+                    ++ex->inline_launches;
+                    return enqueue_resident(ex, nullptr, key, dep_slots, ndep, flags, false, step_seq);
+                }
                 if ((total + grid - 1) / grid <= kInlineMaxItems) {
                     if ((rc = set_kernel_attrs(ex))) return rc;
                     KernelArgs args{};

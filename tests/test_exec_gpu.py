@@ -381,3 +381,31 @@ def test_inline_steps_device_enumerated(ex):
             ex.unregister(s)
     finally:
         ex.set_option("inline_plans", 0)
+
+
+def test_resident_inline_steps(ex):
+    """Resident + inline: first-seen slot sets ride in the step descriptor (no plan upload),
+    recurring ones get plans; all results correct."""
+    from paper_1901_10008_b200.executor import OperandSet
+    ex.set_option("inline_plans", 1)
+    ex.set_option("inline_promote", 2)
+    try:
+        sets = [[OperandSet("gemm", C2_SHAPES[(5 * r + i) % 13], seed=1300 + 8 * r + i, activation="relu")
+                 for i in range(3)] + [OperandSet("gemv", (512, 1024), dtype="fp32", seed=1390 + r)]
+                for r in range(6)]
+        slots = [[o.register(ex) for o in row] for row in sets]
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            with ex.resident(s):
+                for k in range(24):
+                    ex.launch(slots[k % 6], s, independent=True)
+            s.synchronize()
+        for row in sets:
+            for o in row:
+                _check(o)
+        for row in slots:
+            for sl in row:
+                ex.unregister(sl)
+    finally:
+        ex.set_option("inline_plans", 0)
+        ex.set_option("inline_promote", 1)
