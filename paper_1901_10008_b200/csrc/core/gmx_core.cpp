@@ -429,6 +429,8 @@ struct gmx_sched {
     // observed / predicted dispatch durations; has_win mirrors dict membership
     std::vector<std::deque<double>> ratio_win;
     std::vector<char> has_win;
+    std::vector<int32_t> win_above;   // per stream: ratios in the window above the threshold
+    int64_t streams_above = 0;        // streams with win_above > 0 (0: no straggler possible)
 
     // view storage
     std::vector<gmx_dispatch_rec> v_disp;
@@ -438,6 +440,8 @@ struct gmx_sched {
     std::vector<gmx::ShapeRec> s_recs;
     std::vector<int32_t> s_order, s_live, s_act, s_members, s_tmp;
     std::vector<gmx::Cluster> s_clusters;
+    std::vector<gmx_cost> s_costs;            // superkernel cost per cached cluster ...
+    std::vector<int64_t> s_cost_tenancy;      // ... and the tenancy it was computed for (-1: none)
     std::vector<int64_t> s_slack, s_sig, s_wakeups;
     std::vector<char> s_seen;
 
@@ -762,6 +766,8 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
         rc = cluster_shapes(recs, s->params.pad_budget, s->s_order, s->s_clusters);
         if (rc) return rc;
         s->clustered_version = s->ready_version;
+        s->s_cost_tenancy.assign(s->s_clusters.size(), -1);   // superkernel costs of the new clusters
+        s->s_costs.resize(s->s_clusters.size());
     }
     const auto& order = s->s_order;
     const auto& clusters = s->s_clusters;
@@ -793,10 +799,15 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
     std::vector<int64_t>& sig = s->s_sig;
     for (const Scored& sc : scored) {
         const Cluster& cl = clusters[sc.cluster];
-        gmx_cost cost;
-        rc = superkernel_cost(&s->prof, s->tbl(), cl.op, cl.dtype, cl.padded, cl.nd, cl.end - cl.begin, tenancy,
-                              &cost);
-        if (rc) return rc;
+        // coalesce.py:109-123 is a pure function of (cluster, tenancy): a withhold step and the
+        // wakeup step that follows it on the same ready set reuse the cost
+        gmx_cost& cost = s->s_costs[sc.cluster];
+        if (s->s_cost_tenancy[sc.cluster] != tenancy) {
+            rc = superkernel_cost(&s->prof, s->tbl(), cl.op, cl.dtype, cl.padded, cl.nd, cl.end - cl.begin, tenancy,
+                                  &cost);
+            if (rc) return rc;
+            s->s_cost_tenancy[sc.cluster] = tenancy;
+        }
         members.clear();
         for (int32_t i = cl.begin; i < cl.end; ++i) members.push_back(recs[order[i]].src);
         bool can_delay = !sc.late && cost.efficiency < 1.0;
@@ -1214,12 +1225,20 @@ int gmx_sched_complete_measured(gmx_sched* s, int64_t did, int64_t now, int64_t 
         if (s->ratio_win.size() < s->stream_names.size()) {
             s->ratio_win.resize(s->stream_names.size());
             s->has_win.resize(s->stream_names.size(), 0);
+            s->win_above.resize(s->stream_names.size(), 0);
         }
+        const double thr = s->params.straggler_threshold;
         for (int32_t st : d.streams) {
             auto& w = s->ratio_win[st];
             s->has_win[st] = 1;
+            const int32_t before = s->win_above[st];
             w.push_back(ratio);
-            if (w.size() > win) w.pop_front();   // deque(maxlen=eviction_window)
+            s->win_above[st] += ratio > thr;
+            if (w.size() > win) {   // deque(maxlen=eviction_window)
+                s->win_above[st] -= w.front() > thr;
+                w.pop_front();
+            }
+            s->streams_above += (s->win_above[st] > 0) - (before > 0);
         }
     }
     s->v_ids_a.clear();  // kernel ids
@@ -1257,21 +1276,22 @@ int gmx_sched_complete_measured(gmx_sched* s, int64_t did, int64_t now, int64_t 
 int gmx_sched_find_stragglers(gmx_sched* s, int32_t* out_streams, int32_t cap, int32_t* n_out) {
     if (!s || !n_out) return fail(GMX_EINVAL, "null argument");
     // scheduler.py:237-254: streams with a window, in sorted stream-id order, not evicted, whose
-    // nearest-rank p99 ratio exceeds the threshold (None while the window is short)
-    std::vector<int32_t> order;
+    // nearest-rank p99 ratio exceeds the threshold (None while the window is short). The sorted
+    // window's element at `rank` exceeds the threshold iff at least len - rank + 1 ratios do, so
+    // per-stream counts of above-threshold ratios replace the sort (no candidate: O(1)).
+    *n_out = 0;
+    if (s->streams_above == 0) return GMX_OK;
+    std::vector<int32_t>& order = s->s_tmp;
+    order.clear();
     for (int32_t st = 0; st < (int32_t)s->has_win.size(); ++st)
-        if (s->has_win[st]) order.push_back(st);
+        if (s->has_win[st] && s->win_above[st] > 0 && !s->evicted_stream[st]) order.push_back(st);
     std::sort(order.begin(), order.end(), [s](int32_t a, int32_t b) { return s->stream_less(a, b); });
     int32_t n = 0;
-    std::vector<double> sorted;
     for (int32_t st : order) {
-        if (s->evicted_stream[st]) continue;
-        const auto& w = s->ratio_win[st];
-        if ((int64_t)w.size() < s->params.eviction_min_samples || w.empty()) continue;
-        sorted.assign(w.begin(), w.end());
-        std::sort(sorted.begin(), sorted.end());
-        const int64_t rank = std::max<int64_t>(1, py_ceil(0.99 * (double)sorted.size()));
-        if (sorted[rank - 1] > s->params.straggler_threshold) {
+        const int64_t len = (int64_t)s->ratio_win[st].size();
+        if (len < s->params.eviction_min_samples || len == 0) continue;
+        const int64_t rank = std::max<int64_t>(1, py_ceil(0.99 * (double)len));
+        if (s->win_above[st] >= len - rank + 1) {
             if (n < cap && out_streams) out_streams[n] = st;
             ++n;
         }
