@@ -1059,20 +1059,32 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     advance_unit();
                 };
                 const uint32_t G = gridDim.x;
+                auto grab_base = [&](int64_t k) { return 2u * G * (uint32_t)(k / kQueue); };   // 2 x G grabs per step
+                uint32_t pre = 0;
+                bool have_pre = false;
                 for (int64_t k = 0;; ++k) {
                     if (step_published(args, k)) { push(k, kUnitStop); break; }
                     step_order(args, k);
                     uint64_t* rt = (args.rtrace && k < args.rtrace_steps) ? args.rtrace + (k * G + blockIdx.x) * 8 : nullptr;
                     if (rt) rt[0] = global_timer_ns();
-                    const uint32_t base = 2u * G * (uint32_t)(k / kQueue);   // every step takes 2 x G grabs
+                    const uint32_t base = grab_base(k);
                     uint32_t* grab = &args.dq->grab[k % kQueue];
-                    uint32_t idx = atomicAdd(grab, 1u) - base;
+                    uint32_t idx = have_pre ? pre : atomicAdd(grab, 1u) - base;
+                    have_pre = false;
                     for (;;) {
                         if (idx >= G) { push(k, kUnitEndStep); break; }
                         push(k, (int32_t)idx);
                         // the next grab's L2 round trip overlaps this list's load issue
                         const uint32_t nxt = atomicAdd(grab, 1u) - base;
                         issue_list(list_view(args, k, (int)idx), rt);
+                        if (nxt >= G) {
+                            // no more lists of step k for us: take the first grab of step k + 1
+                            // now, so its round trip overlaps the publication / ordering polls.
+                            // (Its slot's previous round completed long ago: the counter is at
+                            // the new round's base, and no work starts before those polls.)
+                            pre = atomicAdd(&args.dq->grab[(k + 1) % kQueue], 1u) - grab_base(k + 1);
+                            have_pre = true;
+                        }
                         idx = nxt;
                     }
                 }
@@ -1378,7 +1390,7 @@ struct gmx_exec {
     int32_t* counters = nullptr;
     int32_t counters_cap = 0;
     int64_t max_split = 32;
-    int64_t split_pct = 250;     // split a tile into pieces of about this % of the per-CTA share
+    int64_t split_pct = 400;     // split a tile into pieces of about this % of the per-CTA share
     int ctas_per_sm = 1;         // 1, or 2 CTAs of the coalesced kernel per SM (the latter runs as 2 waves)
     bool cache_plans = true;
     bool attr_set = false;

@@ -208,7 +208,7 @@ def test_c2_kernel_shapes_and_split_plans(ex, ctas_per_sm, split_pct):
             ex.unregister(s)
     finally:
         ex.set_option("ctas_per_sm", 1)
-        ex.set_option("split_pct", 250)
+        ex.set_option("split_pct", 400)
 
 
 def test_independent_back_to_back_launches(ex):

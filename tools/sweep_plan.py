@@ -18,7 +18,7 @@ for arg in sys.argv[1:]:
     grid[k] = [int(x) for x in v.split(",")]
 if not grid:
     grid = {"split_pct": [60]}
-b = C2Bench(replicas=8)
+b = C2Bench(replicas=int(os.environ.get("GMX_REPLICAS", "8")))
 nbytes = algorithmic_bytes(b.shapes)
 merge = grid.pop("merge", [1])
 resident = grid.pop("resident", [0])
