@@ -54,6 +54,7 @@ enum : int32_t { kItemGemm = 0, kItemGemv = 1, kItemEltwise = 2 };
 
 constexpr int kThreads = 224;             // 6 role warps + 1 queue-dispatcher warp (resident mode)
 constexpr int kInlineMaxMembers = 32;   // members of an inline (device-enumerated) step
+constexpr size_t kSeenSlots = 4096;     // slot-set sighting counters (inline promotion)
 constexpr int kInlineMaxItems = 48;     // work items one CTA may hold in an inline step
 constexpr int kInlineGemvRows = 64;     // inline GEMV item: rows
 constexpr int kInlineEltwise = 32768;   // inline elementwise item: elements
@@ -1401,7 +1402,7 @@ struct gmx_exec {
     int occupancy[2] = {0, 0};   // measured resident CTAs/SM of the 1- and 2-CTA kernel shapes
     bool inline_plans = false;   // option "inline_plans": first-seen slot sets run as inline steps
     int inline_promote = 1;      // sightings before a slot set gets a cached plan
-    std::unordered_map<uint64_t, int> inline_seen;
+    std::vector<std::pair<uint64_t, int32_t>> inline_seen = std::vector<std::pair<uint64_t, int32_t>>(4096);
     int64_t inline_launches = 0;
     int32_t dbg = 0;
     const gmx::Plan* recent[3] = {nullptr, nullptr, nullptr};   // plans of the last launches
@@ -2194,9 +2195,11 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
         if (pit != ex->plans.end())
             for (auto& p : pit->second) hit |= p->key == key;
         if (!hit) {
-            if (ex->inline_seen.size() > 65536) ex->inline_seen.clear();
-            int& seen = ex->inline_seen[h];
-            if (seen++ < ex->inline_promote) {
+            // sightings per slot set: a direct-mapped table (no rehash / clear pauses on the
+            // serving path); a collision just restarts that set's count
+            auto& e = ex->inline_seen[h & (kSeenSlots - 1)];
+            if (e.first != h) e = {h, 0};
+            if (e.second++ < ex->inline_promote) {
                 int64_t total = 0;
                 for (int32_t sl : key) {
                     const DevProblem& P = ex->probs[sl].dev;

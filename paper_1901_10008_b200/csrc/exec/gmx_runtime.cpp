@@ -135,7 +135,7 @@ int gmx_runtime_create(gmx_sched* sched, gmx_exec* ex, int32_t mode, gmx_runtime
     // steps (device-enumerated work items) instead of paying a host plan build + upload
     if (ex && mode == GMX_RT_REALTIME) {
         gmx_exec_set_option(ex, "inline_plans", 1);
-        gmx_exec_set_option(ex, "inline_promote", 8);
+        gmx_exec_set_option(ex, "inline_promote", 1 << 20);   // plans only for steps too big to inline
     }
     auto* rt = new gmx_runtime();
     rt->sched = sched;
@@ -381,6 +381,13 @@ static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool real
         // dependencies go to the executor as the producers' slots: a per-step launch becomes
         // dependent, a resident step waits only for the steps that wrote those slots
         int64_t seq = -1;
+        // wall clock: a member became ready only after its producers' completion was OBSERVED, so
+        // the launch carries no ordering against earlier steps (it must not wait for unrelated
+        // work queued before it)
+        if (realtime) {
+            rt->launch_deps.clear();
+            independent = true;
+        }
         rc = rt->ex ? gmx_exec_launch_deps(rt->ex, rt->launch_slots.data(), (int32_t)rt->launch_slots.size(),
                                            rt->launch_deps.data(), (int32_t)rt->launch_deps.size(), stream,
                                            independent ? GMX_LAUNCH_INDEPENDENT : 0, &seq)
