@@ -824,7 +824,7 @@ __device__ __forceinline__ StepView list_view(const KernelArgs& a, int64_t k, in
         v.inl_n = inl;
         v.inl_slots = d->inline_slots;
         v.idx = idx;
-        v.G = gridDim.x;
+        v.G = (uint32_t)__ldcg(&d->grid);   // the step's lists (items spread over them)
         return v;
     }
     v.probs = (const DevProblem*)__ldcg((const long long*)&d->probs);
@@ -837,6 +837,18 @@ __device__ __forceinline__ StepView list_view(const KernelArgs& a, int64_t k, in
         v.end = __ldcg(off + idx + 1);
     }
     return v;
+}
+
+// Count one finished item list of step k; the list that completes the step stamps the time and
+// tells the host (host-mapped, system scope). `release`: order the caller's earlier writes.
+__device__ __forceinline__ void count_list_done(const KernelArgs& a, int64_t k) {
+    uint32_t prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&a.dq->done[k % kQueue]) : "memory");
+    if (prev + 1 == gridDim.x * (uint32_t)(k / kQueue + 1)) {   // step k complete
+        atomicMax(reinterpret_cast<unsigned long long*>(&a.dq->t_last), (unsigned long long)global_timer_ns());
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(&a.hdone[k % kQueue]), "l"(k + 1) : "memory");
+    }
 }
 
 // Resident producer: wait until step k is published; returns true for the stop step.
@@ -900,7 +912,7 @@ __device__ void dispatch_steps(const KernelArgs& a) {
         uint32_t nap = 64;   // back off while idle: each poll is a PCIe round trip
         while ((avail = ld_acquire_sys_s64(a.hpub)) <= k) {
             __nanosleep(nap);
-            nap = nap < 2048 ? 2 * nap : nap;
+            nap = nap < 256 ? 2 * nap : nap;   // a new step waits at most ~0.25 us + one PCIe read
             if (global_timer_ns() - t0 > 60000000000ull) __trap();   // host never published
         }
         const int n = (int)(avail - k < kBatch ? avail - k : kBatch);
@@ -1072,8 +1084,15 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     uint32_t* grab = &args.dq->grab[k % kQueue];
                     uint32_t idx = have_pre ? pre : atomicAdd(grab, 1u) - base;
                     have_pre = false;
+                    // lists past the step's used lists are empty: counted here, not handed on
+                    const uint32_t L = (uint32_t)__ldcg(&args.dq->ring[k % kQueue].grid);
                     for (;;) {
                         if (idx >= G) { push(k, kUnitEndStep); break; }
+                        if (idx >= L) {
+                            count_list_done(args, k);
+                            idx = atomicAdd(grab, 1u) - base;
+                            continue;
+                        }
                         push(k, (int32_t)idx);
                         // the next grab's L2 round trip overlaps this list's load issue
                         const uint32_t nxt = atomicAdd(grab, 1u) - base;
@@ -1179,16 +1198,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             if (etid == 0) {
                 bulk_wait_upto(newer_groups);   // TMA stores of that list have landed
                 fence_proxy_async_global();
-                uint32_t prev;
-                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
-                             : "=r"(prev) : "l"(&args.dq->done[kk % kQueue]) : "memory");
-                if (prev + 1 == gridDim.x * (uint32_t)(kk / kQueue + 1)) {   // step kk complete
-                    atomicMax(reinterpret_cast<unsigned long long*>(&args.dq->t_last),
-                              (unsigned long long)global_timer_ns());
-                    asm volatile("fence.acq_rel.sys;" ::: "memory");
-                    asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(&args.hdone[kk % kQueue]), "l"(kk + 1)
-                                 : "memory");
-                }
+                count_list_done(args, kk);
                 if (args.rtrace && kk < args.rtrace_steps)
                     args.rtrace[(kk * gridDim.x + blockIdx.x) * 8 + 3] = global_timer_ns();
             }
@@ -1724,6 +1734,21 @@ static int set_kernel_attrs(gmx_exec* ex) {
     return GMX_OK;
 }
 
+// Virtual work items of an inline step over `key` (see next_item).
+static int64_t inline_item_count(const gmx_exec* ex, const std::vector<int32_t>& key) {
+    int64_t total = 0;
+    for (int32_t sl : key) {
+        const DevProblem& P = ex->probs[sl].dev;
+        if (P.kind == kItemGemm)
+            total += (int64_t)((P.rows + kTileRows - 1) / kTileRows) * ((P.cols + P.bn - 1) / P.bn);
+        else if (P.kind == kItemGemv)
+            total += (P.rows + kInlineGemvRows - 1) / kInlineGemvRows;
+        else
+            total += (P.rows + kInlineEltwise - 1) / kInlineEltwise;
+    }
+    return total;
+}
+
 static bool keys_intersect(const std::vector<int32_t>& a, const std::vector<int32_t>& b) {
     size_t i = 0, j = 0;
     while (i < a.size() && j < b.size()) {
@@ -1807,8 +1832,8 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
         d.ws = plan->d_ws;
         d.counters = plan->d_counters;
         d.grid = plan->stats.grid;
-    } else {   // inline step: every CTA list enumerates its share of the members' items
-        d.grid = r.grid;
+    } else {   // inline step: list i (< #items) enumerates the members' items g with g % grid == i
+        d.grid = (int32_t)std::max<int64_t>(1, std::min<int64_t>(r.grid, inline_item_count(ex, key)));
         d.inline_n = (int32_t)key.size();
         for (size_t i = 0; i < key.size(); ++i) d.inline_slots[i] = key[i];
     }
@@ -2200,16 +2225,7 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
             auto& e = ex->inline_seen[h & (kSeenSlots - 1)];
             if (e.first != h) e = {h, 0};
             if (e.second++ < ex->inline_promote) {
-                int64_t total = 0;
-                for (int32_t sl : key) {
-                    const DevProblem& P = ex->probs[sl].dev;
-                    if (P.kind == kItemGemm)
-                        total += (int64_t)((P.rows + kTileRows - 1) / kTileRows) * ((P.cols + P.bn - 1) / P.bn);
-                    else if (P.kind == kItemGemv)
-                        total += (P.rows + kInlineGemvRows - 1) / kInlineGemvRows;
-                    else
-                        total += (P.rows + kInlineEltwise - 1) / kInlineEltwise;
-                }
+                const int64_t total = inline_item_count(ex, key);
                 const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ex->num_sms, total));
                 if (ex->res.active) {   // resident: the slots ride in the step descriptor
                     ++ex->inline_launches;
