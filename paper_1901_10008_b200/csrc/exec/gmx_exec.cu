@@ -839,16 +839,11 @@ __device__ __forceinline__ StepView list_view(const KernelArgs& a, int64_t k, in
     return v;
 }
 
-// Count one finished item list of step k; the list that completes the step stamps the time and
-// tells the host (host-mapped, system scope). `release`: order the caller's earlier writes.
+// Count one finished item list of step k: a fire-and-forget release reduction (the caller's
+// earlier writes are ordered before it); the dispatcher warp notices completed steps and tells
+// the host, so no list waits for a round trip to L2 here.
 __device__ __forceinline__ void count_list_done(const KernelArgs& a, int64_t k) {
-    uint32_t prev;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&a.dq->done[k % kQueue]) : "memory");
-    if (prev + 1 == gridDim.x * (uint32_t)(k / kQueue + 1)) {   // step k complete
-        atomicMax(reinterpret_cast<unsigned long long*>(&a.dq->t_last), (unsigned long long)global_timer_ns());
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
-        asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(&a.hdone[k % kQueue]), "l"(k + 1) : "memory");
-    }
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&a.dq->done[k % kQueue]) : "memory");
 }
 
 // Resident producer: wait until step k is published; returns true for the stop step.
@@ -906,11 +901,42 @@ __device__ void dispatch_steps(const KernelArgs& a) {
     // step rate)
     constexpr int kBatch = 4;
     int64_t k = 0;
+    // completion reporter (runs while the relay has nothing to do): steps [rep, rep + 16) are scanned (relaxed loads, all in flight); a
+    // step whose lists are all counted gets its host-mapped done flag (system-scope release,
+    // after an acquire fence covering the lists' release reductions); steps complete out of order
+    int64_t rep = 0;
+    uint64_t reported = 0;
+    const uint32_t G = gridDim.x;
+    auto report = [&](int64_t limit) {
+        uint32_t cnt[16];
+        const int span = (int)(limit - rep < 16 ? limit - rep : 16);   // completions run roughly in order
+#pragma unroll 4
+        for (int i = 0; i < span; ++i)
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cnt[i]) : "l"(&a.dq->done[(rep + i) % kQueue]));
+        bool any = false;
+        for (int i = 0; i < span; ++i) {
+            const int64_t j = rep + i;
+            if ((reported >> i) & 1ull) continue;
+            if ((int32_t)(cnt[i] - G * (uint32_t)(j / kQueue + 1)) < 0) continue;
+            if (!any) {
+                asm volatile("fence.acq_rel.sys;" ::: "memory");
+                any = true;
+            }
+            asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(&a.hdone[j % kQueue]), "l"(j + 1) : "memory");
+            reported |= 1ull << i;
+        }
+        if (any) a.dq->t_last = global_timer_ns();
+        while (reported & 1ull) {
+            reported >>= 1;
+            ++rep;
+        }
+    };
     for (;;) {
         int64_t avail;
         const uint64_t t0 = global_timer_ns();
         uint32_t nap = 64;   // back off while idle: each poll is a PCIe round trip
         while ((avail = ld_acquire_sys_s64(a.hpub)) <= k) {
+            report(k);
             __nanosleep(nap);
             nap = nap < 256 ? 2 * nap : nap;   // a new step waits at most ~0.25 us + one PCIe read
             if (global_timer_ns() - t0 > 60000000000ull) __trap();   // host never published
@@ -960,6 +986,13 @@ __device__ void dispatch_steps(const KernelArgs& a) {
         asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(&a.dq->published), "l"(k) : "memory");
         a.dq->t_relay = global_timer_ns();
         if (stop) break;
+    }
+    // after the stop: report every remaining step (the stop entry itself is k - 1)
+    const uint64_t t1 = global_timer_ns();
+    while (rep < k - 1) {
+        report(k - 1);
+        __nanosleep(128);
+        if (global_timer_ns() - t1 > 60000000000ull) __trap();
     }
 }
 
@@ -1326,6 +1359,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+// experiment knob GMX_L2_PROMO=0|64|128|256 (default 256): L2 sector promotion of operand loads
+static CUtensorMapL2promotion l2_promotion() {
+    static CUtensorMapL2promotion v = [] {
+        const char* e = std::getenv("GMX_L2_PROMO");
+        const int x = e ? std::atoi(e) : 256;
+        return x == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : x == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+               : x == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }();
+    return v;
+}
+
 // bf16 [rows x K] row-major operand, leading dim `ld` elements, boxes of 64 (K) x box_rows.
 static int make_tmap(CUtensorMap* map, const void* ptr, int64_t rows, int64_t K, int64_t ld, int box_rows) {
     auto fn = encode_fn();
@@ -1335,7 +1379,7 @@ static int make_tmap(CUtensorMap* map, const void* ptr, int64_t rows, int64_t K,
     cuuint32_t box[2] = {(cuuint32_t)kBlockK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(GMX_EINVAL, "cuTensorMapEncodeTiled failed (alignment/stride?) code " + std::to_string((int)r));
     return GMX_OK;
