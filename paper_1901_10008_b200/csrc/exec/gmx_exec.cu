@@ -160,7 +160,6 @@ struct StepDesc {
 static_assert(sizeof(StepDesc) == 256, "StepDesc layout");
 static_assert(offsetof(StepDesc, inline_n) < 96 && offsetof(StepDesc, inline_slots) == 92,
               "the dispatcher relays a 96-byte head that includes inline_n");
-constexpr int kStepVec = (int)(sizeof(StepDesc) / 16);
 
 struct DevQueue {
     StepDesc ring[kQueue];
