@@ -107,8 +107,10 @@ class ClockSampler:
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, device_index, period_s=0.002):
+    def __init__(self, device_index, period_s=0.002, avoid_core=None, allowed=None):
         self.samples, self.reasons = [], set()
+        self.avoid_core = avoid_core
+        self.allowed = sorted(os.sched_getaffinity(0)) if allowed is None else allowed
         self.period = period_s
         self._stop = threading.Event()
         try:
@@ -122,6 +124,10 @@ class ClockSampler:
             self.max_mhz = None
 
     def _loop(self):
+        if self.avoid_core is not None:   # keep off the serving loop's core (pin_serving_thread)
+            others = set(self.allowed) - {self.avoid_core}
+            if others:
+                os.sched_setaffinity(0, others)
         while not self._stop.is_set():
             self.sample()
             time.sleep(self.period)
@@ -508,6 +514,29 @@ def read_traffic():
         return None
 
 
+def pin_serving_thread(device_index):
+    """Pin the calling (serving-loop) thread to one core: the native runtime is a single-threaded
+    event loop, and migrations / a shared core add run-to-run noise. The core is taken from the
+    GPU's NUMA-local set (NVML CPU affinity) when known, avoiding core 0 (interrupt/housekeeping
+    work lands there). Returns (previous affinity, chosen core)."""
+    cpus = sorted(os.sched_getaffinity(0))
+    if not cpus:
+        return cpus, None
+    local = []
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (max(cpus) // 64) + 1)
+        local = [c for c in cpus if (words[c // 64] >> (c % 64)) & 1]
+    except Exception:  # noqa: BLE001 — fall back to the allowed set
+        local = []
+    pool = [c for c in (local or cpus) if c != 0] or cpus
+    core = pool[len(pool) // 2]
+    os.sched_setaffinity(0, {core})
+    return cpus, core
+
+
 def run_ours(args, world, rank):
     import torch
     torch.backends.cuda.matmul.allow_tf32 = False
@@ -538,7 +567,9 @@ def run_ours(args, world, rank):
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(torch.cuda.current_device()) as clocks:
+    all_cpus, host_core = pin_serving_thread(torch.cuda.current_device())
+    with ClockSampler(torch.cuda.current_device(), avoid_core=host_core,
+                      allowed=all_cpus) as clocks:
         ev0.record(bench.stream)
         if args.launch_per_step:
             st = bench.run_rounds(first, args.steps)
@@ -551,6 +582,8 @@ def run_ours(args, world, rank):
         ev1.record(bench.stream)
         torch.cuda.synchronize()
     barrier()
+    if all_cpus:
+        os.sched_setaffinity(0, set(all_cpus))
     sec_local = ev0.elapsed_time(ev1) * 1e-3
     sec = all_reduce(sec_local, torch.distributed.ReduceOp.MAX) if world > 1 else sec_local
     launches = st["launches"] - before["launches"]
@@ -609,6 +642,7 @@ def run_ours(args, world, rank):
         "launches_per_step": (launches / args.steps) if args.launch_per_step else round(1 / args.steps, 5),
         "slo_misses": st["slo_misses"],
         "gpu_launches": launches if args.launch_per_step else 1,
+        "host_core": host_core,
         "executor": "launch per step" if args.launch_per_step else
                     "resident (one persistent launch; steps queued through pinned host ring)",
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
@@ -669,7 +703,7 @@ def run_reference(args, world, rank):
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--replicas", type=int, default=16)

@@ -222,6 +222,35 @@ static int superkernel_cost(const gmx_profile* p, const gmx_tuning_table* t, int
     return GMX_OK;
 }
 
+// Memo of the pure cost functions (kernels.py:216-222 per kernel shape, coalesce.py:109-123
+// per (cluster shape, batch, tenancy)): the profile and tuning table are fixed for a
+// scheduler's lifetime and recurring workloads repeat the same shapes every round. Direct
+// mapped with full-key verification; a collision just recomputes.
+struct CostMemo {
+    struct Entry {
+        int64_t key[7];
+        gmx_cost cost;
+        bool used = false;
+    };
+    std::vector<Entry> tab = std::vector<Entry>(1024);
+    template <typename F>
+    int get(const int64_t (&key)[7], gmx_cost* out, F compute) {
+        uint64_t h = 0x9E3779B97F4A7C15ull;
+        for (int64_t k : key) h = mix64(h ^ (uint64_t)k);
+        Entry& e = tab[h & (tab.size() - 1)];
+        if (e.used && std::memcmp(e.key, key, sizeof key) == 0) {
+            *out = e.cost;
+            return GMX_OK;
+        }
+        const int rc = compute(out);
+        if (rc) return rc;
+        std::memcpy(e.key, key, sizeof key);
+        e.cost = *out;
+        e.used = true;
+        return GMX_OK;
+    }
+};
+
 // ---------------------------------------------------------------- coalescer
 
 // The coalescer works over a flat array of shape records (one per pending
@@ -440,6 +469,7 @@ struct gmx_sched {
     std::vector<gmx::ShapeRec> s_recs;
     std::vector<int32_t> s_order, s_live, s_act, s_members, s_tmp;
     std::vector<gmx::Cluster> s_clusters;
+    gmx::CostMemo solo_memo, super_memo;      // pure cost functions, memoized per shape
     std::vector<gmx_cost> s_costs;            // superkernel cost per cached cluster ...
     std::vector<int64_t> s_cost_tenancy;      // ... and the tenancy it was computed for (-1: none)
     std::vector<int64_t> s_slack, s_sig, s_wakeups;
@@ -803,8 +833,12 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
         // wakeup step that follows it on the same ready set reuse the cost
         gmx_cost& cost = s->s_costs[sc.cluster];
         if (s->s_cost_tenancy[sc.cluster] != tenancy) {
-            rc = superkernel_cost(&s->prof, s->tbl(), cl.op, cl.dtype, cl.padded, cl.nd, cl.end - cl.begin, tenancy,
-                                  &cost);
+            const int64_t mk[7] = {((int64_t)cl.op << 8) | cl.dtype, cl.nd, cl.padded[0], cl.padded[1], cl.padded[2],
+                                   cl.end - cl.begin, tenancy};
+            rc = s->super_memo.get(mk, &cost, [&](gmx_cost* o) {
+                return superkernel_cost(&s->prof, s->tbl(), cl.op, cl.dtype, cl.padded, cl.nd, cl.end - cl.begin,
+                                        tenancy, o);
+            });
             if (rc) return rc;
             s->s_cost_tenancy[sc.cluster] = tenancy;
         }
@@ -1128,8 +1162,11 @@ int gmx_sched_add_request(gmx_sched* s, int64_t request_id, int32_t stream, int6
         const gmx_kernel_desc& d = ks[i];
         int64_t dims[3] = {0, 0, 0};
         for (int j = 0; j < d.ndims; ++j) dims[j] = d.dims[j];
-        const gmx_tuning_config& cfg = table_lookup(s->tbl(), make_key(d.op, d.dtype, dims, d.ndims), 1);
-        int rc = kernel_cost(&s->prof, d.op, d.dtype, dims, cfg, &c);
+        const int64_t mk[7] = {d.op, d.dtype, d.ndims, dims[0], dims[1], dims[2], 0};
+        int rc = s->solo_memo.get(mk, &c, [&](gmx_cost* o) {
+            const gmx_tuning_config& cfg = table_lookup(s->tbl(), make_key(d.op, d.dtype, dims, d.ndims), 1);
+            return kernel_cost(&s->prof, d.op, d.dtype, dims, cfg, o);
+        });
         if (rc) return rc;
         preds[i] = c.duration;
     }
