@@ -52,7 +52,7 @@ namespace gmx {
 
 enum : int32_t { kItemGemm = 0, kItemGemv = 1, kItemEltwise = 2 };
 
-constexpr int kThreads = 224;             // 6 role warps + 1 queue-dispatcher warp (resident mode)
+constexpr int kThreads = 256;             // 6 role warps + queue dispatcher + list scheduler (resident mode)
 constexpr int kInlineMaxMembers = 32;   // members of an inline (device-enumerated) step
 constexpr size_t kSeenSlots = 4096;     // slot-set sighting counters (inline promotion)
 constexpr int kInlineMaxItems = 48;     // work items one CTA may hold in an inline step
@@ -71,6 +71,7 @@ struct SmemCfg {
     static constexpr int acc_bufs = kCtasPerSm == 1 ? 4 : 2;        // TMEM accumulators (128 cols each)
     static constexpr int tmem_cols = acc_bufs * 128;                // 512 per SM either way
     static constexpr int stage_bufs = kCtasPerSm == 1 ? 2 : 1;      // output staging ping-pong
+    static constexpr int unit_q = kCtasPerSm == 1 ? 6 : 1;          // resident work units (1-CTA shape only)
 };
 constexpr int kTileRows = 128;             // UMMA M
 constexpr int kBlockK = 64;                // 64 bf16 = 128 B = one swizzle atom row
@@ -84,7 +85,7 @@ constexpr int kStageBytes = kStageA + kStageB;
 template <int kCtasPerSm>
 constexpr int smem_bytes() {
     using C = SmemCfg<kCtasPerSm>;
-    return C::stages * kStageBytes + C::stage_out + C::align_pad + 512 /*barriers + unit queue*/;
+    return C::stages * kStageBytes + C::stage_out + C::align_pad + C::unit_q * 256 /*unit ring*/ + 512 /*barriers*/;
 }
 static_assert(2 * (smem_bytes<2>() + 1024) <= 233472, "two CTAs must fit one SM's shared memory");
 constexpr int kWsBlock = 4096;             // split-K workspace allocation unit (floats)
@@ -119,7 +120,7 @@ struct WorkItem {
     uint8_t type;
     uint8_t nsplit;
     uint8_t split;
-    uint8_t _pad;
+    uint8_t bn;              // gemm: the problem's UMMA N (64 / 128)
     int32_t row0;            // gemm: M-side origin; gemv: first row; eltwise: first element
     int32_t col0;            // gemm: N-side origin; gemv: end row;  eltwise: end element
     int32_t kb0, kb1;        // gemm: k-block range of this (split) item
@@ -210,6 +211,7 @@ struct StepView {
     const int32_t* inl_slots;
     int idx;
     uint32_t G;
+    int ibase;   // items[i - ibase] is item i (a resident unit's items live in shared memory)
 };
 
 // Walks one list's work items: a planned list's array, or an inline step's virtual items
@@ -255,7 +257,7 @@ __device__ __forceinline__ bool next_item(const StepView& v, ItemCursor& c, Work
             it.type = (uint8_t)kind;
             it.nsplit = 1;
             it.split = 0;
-            it._pad = 0;
+            it.bn = (uint8_t)P->bn;
             it.kb0 = 0;
             it.tile_slot = -1;
             it.ws_blk = 0;
@@ -284,7 +286,7 @@ template <typename F>
 __device__ __forceinline__ void for_each_item(const StepView& v, F&& f) {
     if (v.inl_n == 0) {
         for (int i = v.beg; i < v.end; ++i) {
-            const WorkItem it = v.items[i];
+            const WorkItem it = v.items[i - v.ibase];
             f(it, i);
         }
     } else {
@@ -876,14 +878,27 @@ __device__ __forceinline__ void step_order(const KernelArgs& a, int64_t k) {
 // item lists of step k from a per-step counter (any CTA may take any list: the device balances
 // the lists dynamically, like the block scheduler does for separate launches), then issues
 // their loads; the MMA issuer and the epilogue consume the same units in order.
-constexpr int kUnitQ = 8;
+// Resident mode: a list-scheduler warp takes the lists, resolves them (the step's plan
+// pointers, the list's item range and items) and hands them to the producer, MMA issuer and
+// epilogue as units in shared memory — the three roles then never wait on a global load for
+// their work, only on their pipelines (measured: the producer used to spend ~40 % of a C2
+// step in dependent L2 round trips: publication / ordering polls, list offsets, items).
+constexpr int kUnitItems = 6;          // items per unit; longer lists span several units
 constexpr int32_t kUnitEndStep = -1;   // this CTA took no more lists of step k
 constexpr int32_t kUnitStop = -2;
-struct Unit {
+struct alignas(16) Unit {
     int64_t k;
-    int32_t idx;
-    int32_t _pad;
+    int32_t idx;            // list index, or kUnitEndStep / kUnitStop
+    int32_t n;              // items in it[] (resident); -1: not resolved, use list_view
+    int32_t beg;            // index of it[0] within the list's items (trace / split bookkeeping)
+    int32_t last;           // 1: the list's last unit (the epilogue counts the list done)
+    const DevProblem* probs;
+    float* ws;
+    int32_t* counters;
+    int64_t _pad;
+    WorkItem it[kUnitItems];
 };
+static_assert(sizeof(Unit) == 256, "Unit layout");
 
 // Dispatcher (resident mode; block 0, warp 6): host ring -> device ring.
 __device__ void dispatch_steps(const KernelArgs& a) {
@@ -1005,6 +1020,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     if (Cfg::align_pad == 0 && smem != smem_raw) __trap();   // SWIZZLE_128B tiles need 1024-byte alignment
     uint8_t* stg = smem + kStages * kStageBytes;                       // epilogue staging (1024-aligned)
+    constexpr int kUnitQ = Cfg::unit_q;
     Unit* uq = reinterpret_cast<Unit*>(stg + kStageOut);               // resident work-unit ring
     uint64_t* full = reinterpret_cast<uint64_t*>(uq + kUnitQ);
     uint64_t* empty = full + kStages;
@@ -1033,7 +1049,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         }
         for (int u = 0; u < kUnitQ; ++u) {
             mbar_init(&ufull[u], 1);
-            mbar_init(&uempty[u], 2);   // MMA issuer + epilogue
+            mbar_init(&uempty[u], 3);   // producer + MMA issuer + epilogue
         }
         mbar_fence_init();
     }
@@ -1051,35 +1067,167 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
     if (args.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     // Units: non-resident = this CTA's own list of the launch's plan, then stop; resident =
-    // the unit ring filled by the producer.
+    // the unit ring filled by the list scheduler. A consumer reads the unit in place and
+    // releases it when done with its items.
     int uslot = 0;
     uint32_t uphase = 0;
-    auto next_unit = [&](bool first) -> Unit {
-        if (!args.resident) return first ? Unit{0, (int32_t)blockIdx.x, 0} : Unit{0, kUnitStop, 0};
+    Unit own{};   // non-resident: synthetic units
+    auto next_unit = [&](bool first) -> const Unit* {
+        if (!args.resident) {
+            own.k = 0;
+            own.idx = first ? (int32_t)blockIdx.x : kUnitStop;
+            own.n = -1;
+            return &own;
+        }
         mbar_wait(&ufull[uslot], uphase);
-        return uq[uslot];
+        return &uq[uslot];
     };
-    auto release_unit = [&]() {   // one consumer thread: done reading the current unit
+    auto release_unit = [&]() {   // one thread per consumer role: done with the current unit
         if (args.resident) mbar_arrive(&uempty[uslot]);
     };
     auto advance_unit = [&]() {
         if (args.resident && ++uslot == kUnitQ) { uslot = 0; uphase ^= 1; }
     };
     auto view = [&](int64_t k, int idx) -> StepView { return list_view(args, k, idx); };
+    auto unit_view = [&](const Unit* u) -> StepView {
+        if (u->n < 0) return list_view(args, u->k, u->idx);
+        StepView v{};
+        v.probs = u->probs;
+        v.ws = u->ws;
+        v.counters = u->counters;
+        v.items = u->it;
+        v.beg = u->beg;
+        v.end = u->beg + u->n;
+        v.ibase = u->beg;
+        return v;
+    };
 
     if (warp == 6) {
         // ---------------- queue dispatcher (resident mode, block 0) ----------------
         if (lane == 0 && args.resident && blockIdx.x == 0) dispatch_steps(args);
+    } else if (warp == 7) {
+        // ---------------- list scheduler (resident mode) ----------------
+        if (lane == 0 && args.resident) {
+            auto unit_slot = [&]() -> Unit* {
+                mbar_wait(&uempty[uslot], uphase ^ 1);
+                return &uq[uslot];
+            };
+            auto publish = [&]() {
+                mbar_arrive(&ufull[uslot]);   // release: the unit is visible to the consumers
+                advance_unit();
+            };
+            auto push_ctl = [&](int64_t k, int32_t code) {
+                Unit* u = unit_slot();
+                u->k = k;
+                u->idx = code;
+                u->n = 0;
+                publish();
+            };
+            const uint32_t G = gridDim.x;
+            auto grab_base = [&](int64_t k) { return 2u * G * (uint32_t)(k / kQueue); };   // 2 x G grabs per step
+            uint32_t pre = 0;
+            bool have_pre = false;
+            for (int64_t k = 0;; ++k) {
+                if (step_published(args, k)) { push_ctl(k, kUnitStop); break; }
+                step_order(args, k);
+                if (args.rtrace && k < args.rtrace_steps)
+                    args.rtrace[(k * G + blockIdx.x) * 8] = global_timer_ns();
+                const uint32_t base = grab_base(k);
+                uint32_t* grab = &args.dq->grab[k % kQueue];
+                uint32_t idx = have_pre ? pre : atomicAdd(grab, 1u) - base;
+                have_pre = false;
+                // the step's plan pointers (independent loads: one round trip)
+                const StepDesc* d = &args.dq->ring[k % kQueue];
+                const uint32_t L = (uint32_t)__ldcg(&d->grid);   // lists past L are empty
+                const int inl = __ldcg(&d->inline_n);
+                const DevProblem* probs = (const DevProblem*)__ldcg((const long long*)&d->probs);
+                const WorkItem* items = (const WorkItem*)__ldcg((const long long*)&d->items);
+                float* ws = (float*)__ldcg((const long long*)&d->ws);
+                int32_t* counters = (int32_t*)__ldcg((const long long*)&d->counters);
+                const int32_t* off = (const int32_t*)__ldcg((const long long*)&d->cta_off);
+                auto begin_unit = [&](int32_t list, int32_t beg) -> Unit* {
+                    Unit* u = unit_slot();
+                    u->k = k;
+                    u->idx = list;
+                    u->beg = beg;
+                    u->probs = probs;
+                    u->ws = ws;
+                    u->counters = counters;
+                    return u;
+                };
+                for (;;) {
+                    if (idx >= G) { push_ctl(k, kUnitEndStep); break; }
+                    if (idx >= L) {
+                        count_list_done(args, k);
+                        idx = atomicAdd(grab, 1u) - base;
+                        continue;
+                    }
+                    // the next grab's round trip overlaps this list's resolution
+                    const uint32_t nxt = atomicAdd(grab, 1u) - base;
+                    if (inl == 0) {
+                        const int32_t beg = __ldcg(off + idx), end = __ldcg(off + idx + 1);
+                        int32_t c = beg;
+                        do {
+                            const int n = min(kUnitItems, end - c);
+                            WorkItem w[kUnitItems];
+#pragma unroll
+                            for (int j = 0; j < kUnitItems; ++j)   // all loads in flight together
+                                if (j < n) {
+                                    const uint4* q = reinterpret_cast<const uint4*>(items + c + j);
+                                    reinterpret_cast<uint4*>(&w[j])[0] = __ldcg(q);
+                                    reinterpret_cast<uint4*>(&w[j])[1] = __ldcg(q + 1);
+                                }
+                            Unit* u = begin_unit((int32_t)idx, c - beg);
+#pragma unroll
+                            for (int j = 0; j < kUnitItems; ++j)
+                                if (j < n) u->it[j] = w[j];
+                            u->n = n;
+                            c += n;
+                            u->last = c >= end ? 1 : 0;
+                            publish();
+                        } while (c < end);
+                    } else {
+                        // inline step: enumerate the list's virtual items into units
+                        const StepView v = list_view(args, k, (int)idx);
+                        ItemCursor cur = item_begin(v);
+                        WorkItem w;
+                        bool have = next_item(v, cur, w);
+                        int32_t cnt = 0;
+                        do {
+                            Unit* u = begin_unit((int32_t)idx, cnt);
+                            int n = 0;
+                            while (have && n < kUnitItems) {
+                                u->it[n++] = w;
+                                have = next_item(v, cur, w);
+                            }
+                            u->n = n;
+                            cnt += n;
+                            u->last = have ? 0 : 1;
+                            publish();
+                        } while (have);
+                    }
+                    if (nxt >= G) {
+                        // no more lists of step k for us: take the first grab of step k + 1
+                        // now, so its round trip overlaps the publication / ordering polls.
+                        // (Its slot's previous round completed long ago: the counter is at
+                        // the new round's base, and no work starts before those polls.)
+                        pre = atomicAdd(&args.dq->grab[(k + 1) % kQueue], 1u) - grab_base(k + 1);
+                        have_pre = true;
+                    }
+                    idx = nxt;
+                }
+            }
+        }
     } else if (warp == 0) {
-        // ---------------- TMA producer (resident: also takes the item lists) ----------------
+        // ---------------- TMA producer ----------------
         if (lane == 0 && has_gemm) {
             int stage = 0;
             uint32_t phase = 0;
-            auto issue_list = [&](const StepView& v, uint64_t* rt) {
+            auto issue_list = [&](const StepView& v) {
                 for_each_item(v, [&](const WorkItem& it, int i) {
                     if (it.type != kItemGemm) return;
                     const DevProblem* P = v.probs + it.problem;
-                    const uint32_t bytes = kStageA + (uint32_t)P->bn * (kBlockK * 2);
+                    const uint32_t bytes = kStageA + (uint32_t)it.bn * (kBlockK * 2);
                     if (args.trace) args.trace[8 * i + 0] = global_timer_ns();
                     tma_prefetch_desc(&P->tm_rows);   // descriptor fetch overlaps the slot wait
                     tma_prefetch_desc(&P->tm_cols);
@@ -1092,54 +1240,17 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
                 });
-                if (rt) rt[1] = global_timer_ns();
             };
-            if (!args.resident) {
-                issue_list(view(0, blockIdx.x), nullptr);
-            } else {
-                auto push = [&](int64_t k, int32_t idx) {
-                    mbar_wait(&uempty[uslot], uphase ^ 1);
-                    uq[uslot] = Unit{k, idx, 0};
-                    mbar_arrive(&ufull[uslot]);   // release: the unit is visible to the consumers
-                    advance_unit();
-                };
-                const uint32_t G = gridDim.x;
-                auto grab_base = [&](int64_t k) { return 2u * G * (uint32_t)(k / kQueue); };   // 2 x G grabs per step
-                uint32_t pre = 0;
-                bool have_pre = false;
-                for (int64_t k = 0;; ++k) {
-                    if (step_published(args, k)) { push(k, kUnitStop); break; }
-                    step_order(args, k);
-                    uint64_t* rt = (args.rtrace && k < args.rtrace_steps) ? args.rtrace + (k * G + blockIdx.x) * 8 : nullptr;
-                    if (rt) rt[0] = global_timer_ns();
-                    const uint32_t base = grab_base(k);
-                    uint32_t* grab = &args.dq->grab[k % kQueue];
-                    uint32_t idx = have_pre ? pre : atomicAdd(grab, 1u) - base;
-                    have_pre = false;
-                    // lists past the step's used lists are empty: counted here, not handed on
-                    const uint32_t L = (uint32_t)__ldcg(&args.dq->ring[k % kQueue].grid);
-                    for (;;) {
-                        if (idx >= G) { push(k, kUnitEndStep); break; }
-                        if (idx >= L) {
-                            count_list_done(args, k);
-                            idx = atomicAdd(grab, 1u) - base;
-                            continue;
-                        }
-                        push(k, (int32_t)idx);
-                        // the next grab's L2 round trip overlaps this list's load issue
-                        const uint32_t nxt = atomicAdd(grab, 1u) - base;
-                        issue_list(list_view(args, k, (int)idx), rt);
-                        if (nxt >= G) {
-                            // no more lists of step k for us: take the first grab of step k + 1
-                            // now, so its round trip overlaps the publication / ordering polls.
-                            // (Its slot's previous round completed long ago: the counter is at
-                            // the new round's base, and no work starts before those polls.)
-                            pre = atomicAdd(&args.dq->grab[(k + 1) % kQueue], 1u) - grab_base(k + 1);
-                            have_pre = true;
-                        }
-                        idx = nxt;
-                    }
-                }
+            for (bool first = true;; first = false) {
+                const Unit* u = next_unit(first);
+                const int32_t uidx = u->idx;
+                const int64_t uk = u->k;
+                if (uidx >= 0) issue_list(unit_view(u));
+                release_unit();
+                advance_unit();
+                if (uidx == kUnitStop) break;
+                if (uidx >= 0 && args.rtrace && uk < args.rtrace_steps)
+                    args.rtrace[(uk * gridDim.x + blockIdx.x) * 8 + 1] = global_timer_ns();
             }
         }
     } else if (warp == 1) {
@@ -1148,15 +1259,18 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             for (bool first = true;; first = false) {
-                const Unit u = next_unit(first);
-                release_unit();
-                advance_unit();
-                if (u.idx == kUnitStop) break;
-                if (u.idx < 0) continue;
-                const StepView v = view(u.k, u.idx);
+                const Unit* u = next_unit(first);
+                const int32_t uidx = u->idx;
+                if (uidx < 0) {
+                    release_unit();
+                    advance_unit();
+                    if (uidx == kUnitStop) break;
+                    continue;
+                }
+                const StepView v = unit_view(u);
                 for_each_item(v, [&](const WorkItem& it, int i) {
                     if (it.type != kItemGemm) return;
-                    const uint32_t idesc = idesc_bf16_m128((uint32_t)v.probs[it.problem].bn);
+                    const uint32_t idesc = idesc_bf16_m128((uint32_t)it.bn);
                     mbar_wait(&tempty[acc], acc_phase ^ 1);
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + (uint32_t)acc * kMaxBN;
@@ -1178,6 +1292,8 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     if (args.trace) args.trace[8 * i + 1] = global_timer_ns();
                     if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
                 });
+                release_unit();
+                advance_unit();
             }
         }
     } else if (warp >= 2 && warp <= 5) {
@@ -1193,7 +1309,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         int pend = -1, pend_age = 0;             // split item whose completion is deferred
         StepView v{};
         auto complete_pending = [&]() {
-            const WorkItem pt = v.items[pend];
+            const WorkItem pt = v.items[pend - v.ibase];
             int32_t* counter = v.counters + pt.tile_slot;
             asm volatile("fence.acq_rel.gpu;" ::: "memory");   // this thread's reductions have landed
             named_bar_sync(1, 128);
@@ -1236,11 +1352,12 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             }
         };
         for (bool first = true;; first = false) {
-            const Unit u = next_unit(first);   // every epilogue thread waits on the unit barrier
-            named_bar_sync(1, 128);            // all have read the unit
-            if (etid == 0) release_unit();
-            advance_unit();
+            const Unit* up = next_unit(first);   // every epilogue thread waits on the unit barrier
+            struct { int64_t k; int32_t idx, last; } u{up->k, up->idx, up->last};
             if (u.idx < 0) {   // end of a step for this CTA, or stop: flush the pending count
+                named_bar_sync(1, 128);   // all have read the unit
+                if (etid == 0) release_unit();
+                advance_unit();
                 if (acct_k >= 0) {
                     account(acct_k, 0);
                     acct_k = -1;
@@ -1248,7 +1365,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 if (u.idx == kUnitStop) break;
                 continue;
             }
-            v = view(u.k, u.idx);
+            v = unit_view(up);
             uint64_t* rt = (args.rtrace && u.k < args.rtrace_steps) ? args.rtrace + (u.k * gridDim.x + blockIdx.x) * 8 : nullptr;
             if (rt && etid == 0) {
                 rt[2] = global_timer_ns();
@@ -1309,8 +1426,11 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 if (pend >= 0 && pend != i && ++pend_age >= 1) complete_pending();
             });
             if (pend >= 0) complete_pending();
+            named_bar_sync(1, 128);   // every epilogue thread is done with the unit's items
+            if (etid == 0) release_unit();
+            advance_unit();
             if (rt && etid == 0) rt[7] = global_timer_ns();
-            if (args.resident) {
+            if (args.resident && u.last) {
                 if (acct_k >= 0) account(acct_k, groups - acct_groups);   // the previous list
                 acct_k = u.k;
                 acct_groups = groups;
@@ -1596,6 +1716,7 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
             it.col0 = t.c0;
             it.kb0 = (int32_t)((int64_t)P.kblocks * sp / nsplit);
             it.kb1 = (int32_t)((int64_t)P.kblocks * (sp + 1) / nsplit);
+            it.bn = (uint8_t)P.bn;
             it.tile_slot = slot;
             it.ws_blk = blk;
             const double c = gemm_tile_cost(P, it.kb1 - it.kb0) + (nsplit > 1 ? kSplitNs : 0.0);

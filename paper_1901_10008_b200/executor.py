@@ -19,6 +19,7 @@ fallback: without an sm_100 GPU or the library, construction raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -79,7 +80,8 @@ _exec_lib = None
 def exec_lib():
     global _exec_lib
     if _exec_lib is None:
-        lib = C.CDLL(_build.build_exec())
+        # GMX_EXEC_SO: A/B experiments load another build of the same ABI
+        lib = C.CDLL(os.environ.get("GMX_EXEC_SO") or _build.build_exec())
         for name, (res, args) in EXEC_SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res
