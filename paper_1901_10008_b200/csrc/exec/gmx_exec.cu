@@ -221,8 +221,8 @@ struct StepView {
 struct ItemCursor;
 __device__ __forceinline__ ItemCursor item_begin(const StepView& v);
 __device__ __forceinline__ bool next_item(const StepView& v, ItemCursor& c, WorkItem& it);
-template <typename F>
-__device__ __forceinline__ void for_each_item(const StepView& v, F&& f);
+template <typename F, typename D>
+__device__ __forceinline__ void for_each_item(const StepView& v, F&& f, D&& done_reading);
 
 struct ItemCursor {
     int i;        // planned: next index
@@ -282,17 +282,23 @@ __device__ __forceinline__ bool next_item(const StepView& v, ItemCursor& c, Work
     return false;
 }
 
-template <typename F>
-__device__ __forceinline__ void for_each_item(const StepView& v, F&& f) {
+// `done_reading()` runs once the last item was read, before it is processed: a resident
+// consumer releases its shared-memory unit there, so the list scheduler can refill the slot
+// while the consumer still works on the list's last item.
+template <typename F, typename D>
+__device__ __forceinline__ void for_each_item(const StepView& v, F&& f, D&& done_reading) {
     if (v.inl_n == 0) {
+        if (v.beg >= v.end) done_reading();
         for (int i = v.beg; i < v.end; ++i) {
             const WorkItem it = v.items[i - v.ibase];
+            if (i + 1 == v.end) done_reading();
             f(it, i);
         }
     } else {
         ItemCursor c = item_begin(v);
         WorkItem it;
         while (next_item(v, c, it)) f(it, -1);
+        done_reading();
     }
 }
 
@@ -554,6 +560,7 @@ __device__ __forceinline__ uint32_t epilogue_staged(const EpiParams& E, int row0
             transform_chunk(v, E, E.swap ? col0 + c * 32 : row0 + trow, E.swap);
             stage_out_chunk(E, v, c - c0, trow, stg_u32);
         }
+
         if (tr && etid == 0 && c0 == 0) tr[5] = global_timer_ns();
         fence_async_smem();
         named_bar_sync(3, 128);
@@ -1010,6 +1017,35 @@ __device__ void dispatch_steps(const KernelArgs& a) {
     }
 }
 
+// Profiling build (-DGMX_INSTR, tools/instr_resident.py): per-CTA cycles each role spends
+// waiting on its inputs, dumped at the stop into the last two rtrace rows.
+enum InstrCounter { kIPUnit, kIPEmpty, kIMUnit, kIMTempty, kIMFull, kIEUnit, kIETfull, kISUempty, kISPub, kISOrder,
+                    kISLists, kIPStages, kIEStaged, kIESplit, kIEComplete, kIEAcct, kIABar, kIAWait, kIARed, kICount };
+constexpr int kInstrRows = (kICount + 7) / 8;
+#ifdef GMX_INSTR
+#define GMX_INSTR_INC(i) (++ic[i])
+#else
+#define GMX_INSTR_INC(i) ((void)0)
+#endif
+template <typename W>
+__device__ __forceinline__ void timed(long long* ic, int i, bool on, W&& w) {
+#ifdef GMX_INSTR
+    const long long t0 = clock64();
+    w();
+    if (on) ic[i] += clock64() - t0;
+#else
+    w();
+#endif
+}
+__device__ __forceinline__ void instr_dump(const KernelArgs& a, const long long* ic, int f0, int f1) {
+#ifdef GMX_INSTR
+    if (a.rtrace && a.rtrace_steps >= kInstrRows) {
+        uint64_t* o = a.rtrace + (int64_t)(a.rtrace_steps - kInstrRows) * gridDim.x * 8;
+        for (int f = f0; f < f1; ++f) o[(f / 8) * gridDim.x * 8 + blockIdx.x * 8 + f % 8] = (uint64_t)ic[f];
+    }
+#endif
+}
+
 // Register cap per shape (the 2-CTA shape keeps two CTAs' registers within one SM's 64K).
 template <int kCtasPerSm>
 __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(const __grid_constant__ KernelArgs args) {
@@ -1029,11 +1065,21 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
     uint64_t* tempty = tfull + kAcc;
     uint64_t* ufull = tempty + kAcc;
     uint64_t* uempty = ufull + kUnitQ;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uempty + kUnitQ);
+    // list-accounting ring (resident, blocks != 0): epilogue -> accountant lane (warp 6)
+    constexpr int kAcctQ = 8;
+    uint64_t* afull = uempty + kUnitQ;
+    uint64_t* aempty = afull + kAcctQ;
+    int64_t* aq = reinterpret_cast<int64_t*>(aempty + kAcctQ);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aq + kAcctQ);
     int32_t* split_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
+#ifdef GMX_INSTR
+    long long ic[kICount] = {};
+#else
+    long long* ic = nullptr;   // counters compiled out
+#endif
 
     // CTA owns GEMM tiles (host-computed; resident / inline steps: any list may bring some)
     const bool has_gemm = args.resident || args.inline_n > 0 || (args.cta_flags[blockIdx.x] & 1) != 0;
@@ -1049,7 +1095,11 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         }
         for (int u = 0; u < kUnitQ; ++u) {
             mbar_init(&ufull[u], 1);
-            mbar_init(&uempty[u], 3);   // producer + MMA issuer + epilogue
+            mbar_init(&uempty[u], 6);   // producer + MMA issuer + 4 epilogue warps
+        }
+        for (int q = 0; q < kAcctQ; ++q) {
+            mbar_init(&afull[q], 1);
+            mbar_init(&aempty[q], 1);
         }
         mbar_fence_init();
     }
@@ -1102,14 +1152,29 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         return v;
     };
 
+    // The gpu-scope release that counts a finished list into its step (~0.9 us under load: it
+    // waits for the CTA's writes to be acknowledged) is taken off the epilogue's critical path:
+    // the epilogue hands the list to an accountant lane through a small mbarrier ring (block 0,
+    // whose warp 6 is the queue dispatcher, counts in the epilogue itself).
+    const bool accountant = args.resident && blockIdx.x != 0;
     if (warp == 6) {
-        // ---------------- queue dispatcher (resident mode, block 0) ----------------
+        // ---------------- queue dispatcher (resident mode, block 0) / accountant ----------------
         if (lane == 0 && args.resident && blockIdx.x == 0) dispatch_steps(args);
+        if (lane == 0 && accountant) {
+            for (int q = 0, ph = 0;; ) {
+                mbar_wait(&afull[q], (uint32_t)ph);
+                const int64_t kk = aq[q];
+                if (kk < 0) break;
+                count_list_done(args, kk);   // release: covers the epilogue's writes (synchronized via afull)
+                mbar_arrive(&aempty[q]);
+                if (++q == kAcctQ) { q = 0; ph ^= 1; }
+            }
+        }
     } else if (warp == 7) {
         // ---------------- list scheduler (resident mode) ----------------
         if (lane == 0 && args.resident) {
             auto unit_slot = [&]() -> Unit* {
-                mbar_wait(&uempty[uslot], uphase ^ 1);
+                timed(ic, kISUempty, true, [&] { mbar_wait(&uempty[uslot], uphase ^ 1); });
                 return &uq[uslot];
             };
             auto publish = [&]() {
@@ -1128,8 +1193,14 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             uint32_t pre = 0;
             bool have_pre = false;
             for (int64_t k = 0;; ++k) {
-                if (step_published(args, k)) { push_ctl(k, kUnitStop); break; }
-                step_order(args, k);
+                bool stop = false;
+                timed(ic, kISPub, k > 0, [&] { stop = step_published(args, k); });
+                if (stop) {
+                    push_ctl(k, kUnitStop);
+                    instr_dump(args, ic, kISUempty, kISLists + 1);
+                    break;
+                }
+                timed(ic, kISOrder, true, [&] { step_order(args, k); });
                 if (args.rtrace && k < args.rtrace_steps)
                     args.rtrace[(k * G + blockIdx.x) * 8] = global_timer_ns();
                 const uint32_t base = grab_base(k);
@@ -1164,6 +1235,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     }
                     // the next grab's round trip overlaps this list's resolution
                     const uint32_t nxt = atomicAdd(grab, 1u) - base;
+                    GMX_INSTR_INC(kISLists);
                     if (inl == 0) {
                         const int32_t beg = __ldcg(off + idx), end = __ldcg(off + idx + 1);
                         int32_t c = beg;
@@ -1232,23 +1304,31 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     tma_prefetch_desc(&P->tm_rows);   // descriptor fetch overlaps the slot wait
                     tma_prefetch_desc(&P->tm_cols);
                     for (int kb = it.kb0; kb < it.kb1; ++kb) {
-                        mbar_wait(&empty[stage], phase ^ 1);
+                        timed(ic, kIPEmpty, true, [&] { mbar_wait(&empty[stage], phase ^ 1); });
+                        GMX_INSTR_INC(kIPStages);
                         uint8_t* tile = smem + stage * kStageBytes;
                         mbar_expect_tx(&full[stage], bytes);
                         tma_load_2d(tile, &P->tm_rows, &full[stage], kb * kBlockK, it.row0);
                         tma_load_2d(tile + kStageA, &P->tm_cols, &full[stage], kb * kBlockK, it.col0);
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
-                });
+                }, [&] { release_unit(); });
             };
             for (bool first = true;; first = false) {
-                const Unit* u = next_unit(first);
+                const Unit* u;
+                timed(ic, kIPUnit, !first, [&] { u = next_unit(first); });
                 const int32_t uidx = u->idx;
                 const int64_t uk = u->k;
-                if (uidx >= 0) issue_list(unit_view(u));
-                release_unit();
+                if (uidx >= 0)
+                    issue_list(unit_view(u));   // releases the unit after reading its last item
+                else
+                    release_unit();
                 advance_unit();
-                if (uidx == kUnitStop) break;
+                if (uidx == kUnitStop) {
+                    instr_dump(args, ic, kIPUnit, kIPEmpty + 1);
+                    instr_dump(args, ic, kIPStages, kIPStages + 1);
+                    break;
+                }
                 if (uidx >= 0 && args.rtrace && uk < args.rtrace_steps)
                     args.rtrace[(uk * gridDim.x + blockIdx.x) * 8 + 1] = global_timer_ns();
             }
@@ -1259,23 +1339,27 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             for (bool first = true;; first = false) {
-                const Unit* u = next_unit(first);
+                const Unit* u;
+                timed(ic, kIMUnit, !first, [&] { u = next_unit(first); });
                 const int32_t uidx = u->idx;
                 if (uidx < 0) {
                     release_unit();
                     advance_unit();
-                    if (uidx == kUnitStop) break;
+                    if (uidx == kUnitStop) {
+                        instr_dump(args, ic, kIMUnit, kIMFull + 1);
+                        break;
+                    }
                     continue;
                 }
                 const StepView v = unit_view(u);
                 for_each_item(v, [&](const WorkItem& it, int i) {
                     if (it.type != kItemGemm) return;
                     const uint32_t idesc = idesc_bf16_m128((uint32_t)it.bn);
-                    mbar_wait(&tempty[acc], acc_phase ^ 1);
+                    timed(ic, kIMTempty, true, [&] { mbar_wait(&tempty[acc], acc_phase ^ 1); });
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + (uint32_t)acc * kMaxBN;
                     for (int kb = it.kb0; kb < it.kb1; ++kb) {
-                        mbar_wait(&full[stage], phase);
+                        timed(ic, kIMFull, true, [&] { mbar_wait(&full[stage], phase); });
                         tc_fence_after();
                         const uint8_t* tile = smem + stage * kStageBytes;
                         const uint64_t a_desc = smem_desc_sw128(tile);
@@ -1291,8 +1375,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     umma_commit(&tfull[acc]);
                     if (args.trace) args.trace[8 * i + 1] = global_timer_ns();
                     if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
-                });
-                release_unit();
+                }, [&] { release_unit(); });
                 advance_unit();
             }
         }
@@ -1307,9 +1390,10 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         Staging S{stg, kStageOut / Cfg::stage_bufs, Cfg::stage_bufs, 0u};
         uint32_t groups = 0;                     // bulk groups committed by etid 0 (tracked by all)
         int pend = -1, pend_age = 0;             // split item whose completion is deferred
+        WorkItem pend_it{};
         StepView v{};
-        auto complete_pending = [&]() {
-            const WorkItem pt = v.items[pend - v.ibase];
+        auto complete_pending_body = [&]() {
+            const WorkItem pt = pend_it;
             int32_t* counter = v.counters + pt.tile_slot;
             asm volatile("fence.acq_rel.gpu;" ::: "memory");   // this thread's reductions have landed
             named_bar_sync(1, 128);
@@ -1334,6 +1418,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             }
             pend = -1;
         };
+        auto complete_pending = [&]() { timed(ic, kIEComplete, true, [&] { complete_pending_body(); }); };
         // Resident accounting: a list counts into its step's done counter once its writes (generic
         // and TMA stores) are complete. To keep the TMA-store round trip off the critical path it
         // is deferred until the CTA finished its next list (then only the older list's store
@@ -1341,28 +1426,52 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         // since a later step may wait for this one.
         int64_t acct_k = -1;
         uint32_t acct_groups = 0;
-        auto account = [&](int64_t kk, uint32_t newer_groups) {
-            named_bar_sync(1, 128);   // every epilogue thread's writes happen-before etid 0's release
+        int aslot = 0;
+        uint32_t aphase = 0;
+        auto hand_over = [&](int64_t kk) {   // etid 0: the accountant counts list kk (or stops, kk < 0)
+            mbar_wait(&aempty[aslot], aphase ^ 1);
+            aq[aslot] = kk;
+            mbar_arrive(&afull[aslot]);   // release.cta: the epilogue's writes happen-before the count
+            if (++aslot == kAcctQ) { aslot = 0; aphase ^= 1; }
+        };
+        auto account_body = [&](int64_t kk, uint32_t newer_groups) {
+            timed(ic, kIABar, true, [&] { named_bar_sync(1, 128); });   // all epilogue writes happen-before etid 0's release
             if (etid == 0) {
-                bulk_wait_upto(newer_groups);   // TMA stores of that list have landed
-                fence_proxy_async_global();
-                count_list_done(args, kk);
+                timed(ic, kIAWait, true, [&] {
+                    bulk_wait_upto(newer_groups);   // TMA stores of that list have landed
+                    fence_proxy_async_global();
+                });
+                timed(ic, kIARed, true, [&] {
+                    if (accountant)
+                        hand_over(kk);
+                    else
+                        count_list_done(args, kk);
+                });
                 if (args.rtrace && kk < args.rtrace_steps)
                     args.rtrace[(kk * gridDim.x + blockIdx.x) * 8 + 3] = global_timer_ns();
             }
         };
+        auto account = [&](int64_t kk, uint32_t newer_groups) { timed(ic, kIEAcct, true, [&] { account_body(kk, newer_groups); }); };
         for (bool first = true;; first = false) {
-            const Unit* up = next_unit(first);   // every epilogue thread waits on the unit barrier
+            const Unit* up;   // every epilogue thread waits on the unit barrier
+            timed(ic, kIEUnit, !first, [&] { up = next_unit(first); });
             struct { int64_t k; int32_t idx, last; } u{up->k, up->idx, up->last};
             if (u.idx < 0) {   // end of a step for this CTA, or stop: flush the pending count
-                named_bar_sync(1, 128);   // all have read the unit
-                if (etid == 0) release_unit();
+                __syncwarp();   // the warp has read the unit
+                if (lane == 0) release_unit();
                 advance_unit();
                 if (acct_k >= 0) {
                     account(acct_k, 0);
                     acct_k = -1;
                 }
-                if (u.idx == kUnitStop) break;
+                if (u.idx == kUnitStop) {
+                    if (etid == 0 && accountant) hand_over(-1);
+                    if (etid == 0) {
+                        instr_dump(args, ic, kIEUnit, kIETfull + 1);
+                        instr_dump(args, ic, kIEStaged, kIARed + 1);
+                    }
+                    break;
+                }
                 continue;
             }
             v = unit_view(up);
@@ -1376,7 +1485,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 if (args.trace && etid == 0 && it.type != kItemGemm) args.trace[8 * i + 0] = global_timer_ns();
                 if (it.type == kItemGemm) {
                     const EpiParams E = load_epi(Pg);
-                    mbar_wait(&tfull[acc], acc_phase);
+                    timed(ic, kIETfull, true, [&] { mbar_wait(&tfull[acc], acc_phase); });
                     tc_fence_after();
                     if (args.trace && etid == 0) args.trace[8 * i + 2] = global_timer_ns();
                     const uint32_t taddr = tmem_base + ((uint32_t)(lgrp * 32) << 16) + (uint32_t)acc * kMaxBN;
@@ -1387,8 +1496,10 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&tempty[acc]);
                     } else if (!split && E.tma_out && !(args.dbg & 8)) {
-                        groups += epilogue_staged(E, it.row0, it.col0, S, trow, etid, taddr, &tempty[acc],
-                                                  args.trace ? args.trace + 8 * i : nullptr);
+                        timed(ic, kIEStaged, true, [&] {
+                            groups += epilogue_staged(E, it.row0, it.col0, S, trow, etid, taddr, &tempty[acc],
+                                                      args.trace ? args.trace + 8 * i : nullptr);
+                        });
                     } else if (!split) {
                         for (int c = 0; c < nchunks; ++c) {
                             float vv[32];
@@ -1402,9 +1513,10 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                         // split-K (planner only splits TMA-store problems): reduce now, complete later
                         if (pend >= 0) complete_pending();   // at most one split in flight
                         float* acc_tile = v.ws + (int64_t)it.ws_blk * kWsBlock;
-                        split_reduce(E, acc_tile, trow, taddr, &tempty[acc]);
+                        timed(ic, kIESplit, true, [&] { split_reduce(E, acc_tile, trow, taddr, &tempty[acc]); });
                         if (args.trace && etid == 0) args.trace[8 * i + 4] = global_timer_ns();
                         pend = i;
+                        pend_it = it;
                         pend_age = 0;
                     }
                     if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
@@ -1424,10 +1536,11 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     if (etid == 0) args.trace[8 * i + 3] = global_timer_ns();
                 }
                 if (pend >= 0 && pend != i && ++pend_age >= 1) complete_pending();
+            }, [&] {
+                __syncwarp();   // the warp has read the unit's last item
+                if (lane == 0) release_unit();
             });
             if (pend >= 0) complete_pending();
-            named_bar_sync(1, 128);   // every epilogue thread is done with the unit's items
-            if (etid == 0) release_unit();
             advance_unit();
             if (rt && etid == 0) rt[7] = global_timer_ns();
             if (args.resident && u.last) {
