@@ -71,7 +71,7 @@ struct SmemCfg {
     static constexpr int acc_bufs = kCtasPerSm == 1 ? 4 : 2;        // TMEM accumulators (128 cols each)
     static constexpr int tmem_cols = acc_bufs * 128;                // 512 per SM either way
     static constexpr int stage_bufs = kCtasPerSm == 1 ? 2 : 1;      // output staging ping-pong
-    static constexpr int unit_q = kCtasPerSm == 1 ? 6 : 1;          // resident work units (1-CTA shape only)
+    static constexpr int unit_q = kCtasPerSm == 1 ? 8 : 1;          // resident work units (1-CTA shape only)
 };
 constexpr int kTileRows = 128;             // UMMA M
 constexpr int kBlockK = 64;                // 64 bf16 = 128 B = one swizzle atom row
@@ -85,7 +85,7 @@ constexpr int kStageBytes = kStageA + kStageB;
 template <int kCtasPerSm>
 constexpr int smem_bytes() {
     using C = SmemCfg<kCtasPerSm>;
-    return C::stages * kStageBytes + C::stage_out + C::align_pad + C::unit_q * 256 /*unit ring*/ + 512 /*barriers*/;
+    return C::stages * kStageBytes + C::stage_out + C::align_pad + C::unit_q * 192 /*unit ring*/ + 512 /*barriers*/;
 }
 static_assert(2 * (smem_bytes<2>() + 1024) <= 233472, "two CTAs must fit one SM's shared memory");
 constexpr int kWsBlock = 4096;             // split-K workspace allocation unit (floats)
@@ -890,7 +890,7 @@ __device__ __forceinline__ void step_order(const KernelArgs& a, int64_t k) {
 // epilogue as units in shared memory — the three roles then never wait on a global load for
 // their work, only on their pipelines (measured: the producer used to spend ~40 % of a C2
 // step in dependent L2 round trips: publication / ordering polls, list offsets, items).
-constexpr int kUnitItems = 6;          // items per unit; longer lists span several units
+constexpr int kUnitItems = 4;          // items per unit; longer lists span several units
 constexpr int32_t kUnitEndStep = -1;   // this CTA took no more lists of step k
 constexpr int32_t kUnitStop = -2;
 struct alignas(16) Unit {
@@ -905,7 +905,7 @@ struct alignas(16) Unit {
     int64_t _pad;
     WorkItem it[kUnitItems];
 };
-static_assert(sizeof(Unit) == 256, "Unit layout");
+static_assert(sizeof(Unit) == 192, "Unit layout");
 
 // Dispatcher (resident mode; block 0, warp 6): host ring -> device ring.
 __device__ void dispatch_steps(const KernelArgs& a) {
