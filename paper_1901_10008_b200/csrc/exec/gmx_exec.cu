@@ -199,6 +199,35 @@ struct KernelArgs {
 };
 
 // The items/tables one step works on, as seen by one CTA.
+// Profiling build (-DGMX_INSTR, tools/instr_resident.py): per-CTA cycles each role spends
+// waiting on its inputs, dumped at the stop into the last two rtrace rows.
+enum InstrCounter { kIPUnit, kIPEmpty, kIMUnit, kIMTempty, kIMFull, kIEUnit, kIETfull, kISUempty, kISPub, kISOrder,
+                    kISLists, kIPStages, kIEStaged, kIESplit, kIEComplete, kIEAcct, kIABar, kIAWait, kIARed, kIXNext, kIXLd, kIXStage, kIXBar2, kIXIssue, kICount };
+constexpr int kInstrRows = (kICount + 7) / 8;
+#ifdef GMX_INSTR
+#define GMX_INSTR_INC(i) (++ic[i])
+#else
+#define GMX_INSTR_INC(i) ((void)0)
+#endif
+template <typename W>
+__device__ __forceinline__ void timed(long long* ic, int i, bool on, W&& w) {
+#ifdef GMX_INSTR
+    const long long t0 = clock64();
+    w();
+    if (on) ic[i] += clock64() - t0;
+#else
+    w();
+#endif
+}
+__device__ __forceinline__ void instr_dump(const KernelArgs& a, const long long* ic, int f0, int f1) {
+#ifdef GMX_INSTR
+    if (a.rtrace && a.rtrace_steps >= kInstrRows) {
+        uint64_t* o = a.rtrace + (int64_t)(a.rtrace_steps - kInstrRows) * gridDim.x * 8;
+        for (int f = f0; f < f1; ++f) o[(f / 8) * gridDim.x * 8 + blockIdx.x * 8 + f % 8] = (uint64_t)ic[f];
+    }
+#endif
+}
+
 struct StepView {
     const DevProblem* probs;
     const WorkItem* items;
@@ -476,10 +505,13 @@ __device__ __forceinline__ void stage_out_chunk(const EpiParams& E, const float 
                              __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
         }
     } else {
+        // swapped tile: the staging holds 128/inner output boxes of [per_pass x 32 m rows][inner n]
+        // (box-major, SWIZZLE_128B rows), so one TMA store per box covers the whole pass
         const int inner = 128 / esz;
+        const uint32_t box_bytes = (uint32_t)(16384 / (128 * 32 * esz)) * 4096u;   // per_pass x 32 rows x 128 B
         const uint32_t sb = (uint32_t)(trow / inner);
         const uint32_t byte = (uint32_t)(trow % inner) * (uint32_t)esz;
-        const uint32_t base = stg_u32 + (uint32_t)slot * (uint32_t)(128 * 32 * esz) + sb * 4096u + (byte & 15u);
+        const uint32_t base = stg_u32 + sb * box_bytes + (uint32_t)slot * 4096u + (byte & 15u);
         const uint32_t unit = byte >> 4;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -526,9 +558,10 @@ __device__ __forceinline__ void issue_out_stores(const EpiParams& E, int row0, i
             } else {
                 tma_store_2d(E.tm_out, stg + slot * 16384, col0 + c * 32, row0);
             }
-        } else {
+        } else if (c == c0) {
+            const int box_bytes = (16384 / (128 * 32 * esz)) * 4096;
             for (int sb = 0; sb < 128 / inner; ++sb)
-                tma_store_2d(E.tm_out, stg + slot * (128 * 32 * esz) + sb * 4096, row0 + sb * inner, col0 + c * 32);
+                tma_store_2d(E.tm_out, stg + sb * box_bytes, row0 + sb * inner, col0 + c0 * 32);
         }
     }
     bulk_commit();
@@ -538,35 +571,42 @@ __device__ __forceinline__ void issue_out_stores(const EpiParams& E, int row0, i
 // accumulator is released to the MMA warp right after its last tcgen05.ld.
 __device__ __forceinline__ uint32_t epilogue_staged(const EpiParams& E, int row0, int col0, Staging& S, int trow,
                                                 int etid, uint32_t taddr, uint64_t* tempty_bar,
-                                                uint64_t* tr = nullptr) {
+                                                uint64_t* tr = nullptr, long long* ic = nullptr) {
     const int nchunks = E.bn / 32;
     const int per_pass = out_chunks_per_pass(E, S.half);
     const int lane = lane_id();
     uint32_t groups = 0;
     for (int c0 = 0; c0 < nchunks; c0 += per_pass) {
         const int cend = min(nchunks, c0 + per_pass);
-        uint8_t* stg = S.next(etid);   // staging free: the store that last used it has read it
+        uint8_t* stg;
+        timed(ic, kIXNext, true, [&] {
+            stg = S.next(etid);   // staging free: the store that last used it has read it
+            named_bar_sync(3, 128);
+        });
         const uint32_t stg_u32 = smem_u32(stg);
-        named_bar_sync(3, 128);
         if (tr && etid == 0 && c0 == 0) tr[4] = global_timer_ns();
         for (int c = c0; c < cend; ++c) {
             float v[32];
-            tmem_ld32(taddr + (uint32_t)(c * 32), v);
+            timed(ic, kIXLd, true, [&] { tmem_ld32(taddr + (uint32_t)(c * 32), v); });
             if (c == nchunks - 1) {
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(tempty_bar);
             }
-            transform_chunk(v, E, E.swap ? col0 + c * 32 : row0 + trow, E.swap);
-            stage_out_chunk(E, v, c - c0, trow, stg_u32);
+            timed(ic, kIXStage, true, [&] {
+                transform_chunk(v, E, E.swap ? col0 + c * 32 : row0 + trow, E.swap);
+                stage_out_chunk(E, v, c - c0, trow, stg_u32);
+            });
         }
 
         if (tr && etid == 0 && c0 == 0) tr[5] = global_timer_ns();
-        fence_async_smem();
-        named_bar_sync(3, 128);
+        timed(ic, kIXBar2, true, [&] {
+            fence_async_smem();
+            named_bar_sync(3, 128);
+        });
         if (tr && etid == 0 && c0 == 0) tr[6] = global_timer_ns();
         if (etid == 0) {
-            issue_out_stores(E, row0, col0, c0, cend, stg);
+            timed(ic, kIXIssue, true, [&] { issue_out_stores(E, row0, col0, c0, cend, stg); });
             if (tr && c0 == 0) tr[7] = global_timer_ns();
         }
         S.done();
@@ -1017,35 +1057,6 @@ __device__ void dispatch_steps(const KernelArgs& a) {
     }
 }
 
-// Profiling build (-DGMX_INSTR, tools/instr_resident.py): per-CTA cycles each role spends
-// waiting on its inputs, dumped at the stop into the last two rtrace rows.
-enum InstrCounter { kIPUnit, kIPEmpty, kIMUnit, kIMTempty, kIMFull, kIEUnit, kIETfull, kISUempty, kISPub, kISOrder,
-                    kISLists, kIPStages, kIEStaged, kIESplit, kIEComplete, kIEAcct, kIABar, kIAWait, kIARed, kICount };
-constexpr int kInstrRows = (kICount + 7) / 8;
-#ifdef GMX_INSTR
-#define GMX_INSTR_INC(i) (++ic[i])
-#else
-#define GMX_INSTR_INC(i) ((void)0)
-#endif
-template <typename W>
-__device__ __forceinline__ void timed(long long* ic, int i, bool on, W&& w) {
-#ifdef GMX_INSTR
-    const long long t0 = clock64();
-    w();
-    if (on) ic[i] += clock64() - t0;
-#else
-    w();
-#endif
-}
-__device__ __forceinline__ void instr_dump(const KernelArgs& a, const long long* ic, int f0, int f1) {
-#ifdef GMX_INSTR
-    if (a.rtrace && a.rtrace_steps >= kInstrRows) {
-        uint64_t* o = a.rtrace + (int64_t)(a.rtrace_steps - kInstrRows) * gridDim.x * 8;
-        for (int f = f0; f < f1; ++f) o[(f / 8) * gridDim.x * 8 + blockIdx.x * 8 + f % 8] = (uint64_t)ic[f];
-    }
-#endif
-}
-
 // Register cap per shape (the 2-CTA shape keeps two CTAs' registers within one SM's 64K).
 template <int kCtasPerSm>
 __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(const __grid_constant__ KernelArgs args) {
@@ -1468,7 +1479,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     if (etid == 0 && accountant) hand_over(-1);
                     if (etid == 0) {
                         instr_dump(args, ic, kIEUnit, kIETfull + 1);
-                        instr_dump(args, ic, kIEStaged, kIARed + 1);
+                        instr_dump(args, ic, kIEStaged, kIXIssue + 1);
                     }
                     break;
                 }
@@ -1498,7 +1509,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     } else if (!split && E.tma_out && !(args.dbg & 8)) {
                         timed(ic, kIEStaged, true, [&] {
                             groups += epilogue_staged(E, it.row0, it.col0, S, trow, etid, taddr, &tempty[acc],
-                                                      args.trace ? args.trace + 8 * i : nullptr);
+                                                      args.trace ? args.trace + 8 * i : nullptr, ic);
                         });
                     } else if (!split) {
                         for (int c = 0; c < nchunks; ++c) {
@@ -2394,7 +2405,8 @@ int gmx_exec_register(gmx_exec* ex, const gmx_problem_desc* d, int32_t* out_slot
             const int inner = (int)(128 / osz);
             cuuint64_t dims[2] = {(cuuint64_t)d->n, (cuuint64_t)d->m};
             cuuint64_t strides[1] = {(cuuint64_t)(d->ldc * osz)};
-            cuuint32_t box[2] = {(cuuint32_t)inner, (cuuint32_t)(swap ? 32 : kTileRows)};
+            // swapped tiles store a whole epilogue pass per box: 16 KB staging / (32 x 128 B) rows
+            cuuint32_t box[2] = {(cuuint32_t)inner, (cuuint32_t)(swap ? 32 * (16384 / (128 * 32 * (int)osz)) : kTileRows)};
             cuuint32_t estr[2] = {1, 1};
             if (fn && fn(&P.tm_out, d->out_dtype == GMX_ST_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                                  : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,

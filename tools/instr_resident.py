@@ -14,7 +14,7 @@ import sys
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(REPO, "paper_1901_10008_b200", "lib", "instr")
 NAMES = ["p_unit", "p_empty", "m_unit", "m_tempty", "m_full", "e_unit", "e_tfull", "s_uempty", "s_pub",
-         "s_order", "s_lists", "p_stages", "e_staged", "e_split", "e_complete", "e_acct", "a_bar", "a_wait", "a_red"]
+         "s_order", "s_lists", "p_stages", "e_staged", "e_split", "e_complete", "e_acct", "a_bar", "a_wait", "a_red", "x_next", "x_ld", "x_stage", "x_bar2", "x_issue"]
 
 
 def build():
