@@ -514,6 +514,29 @@ def read_traffic():
         return None
 
 
+def idlest_core(pool, window_s=0.2):
+    """The core of `pool` with the least busy time over a short window (/proc/stat): a core that
+    another process (or a busy hypervisor thread) keeps busy halves the serving loop's rate."""
+    def busy():
+        out = {}
+        try:
+            with open("/proc/stat") as fh:
+                for line in fh:
+                    if line.startswith("cpu") and line[3:4].isdigit():
+                        f = line.split()
+                        vals = [int(x) for x in f[1:]]
+                        out[int(f[0][3:])] = sum(vals) - vals[3] - (vals[4] if len(vals) > 4 else 0)
+        except OSError:
+            pass
+        return out
+    a = busy()
+    time.sleep(window_s)
+    b = busy()
+    if not a or not b:
+        return pool[len(pool) // 2]
+    return min(pool, key=lambda c: (b.get(c, 0) - a.get(c, 0), c))
+
+
 def pin_serving_thread(device_index):
     """Pin the calling (serving-loop) thread to one core: the native runtime is a single-threaded
     event loop, and migrations / a shared core add run-to-run noise. The core is taken from the
@@ -532,7 +555,12 @@ def pin_serving_thread(device_index):
     except Exception:  # noqa: BLE001 — fall back to the allowed set
         local = []
     pool = [c for c in (local or cpus) if c != 0] or cpus
-    core = pool[len(pool) // 2]
+    core = idlest_core(pool)
+    forced = os.environ.get("GMX_HOST_CORE")   # experiments: a fixed core, or -1 = no pinning
+    if forced is not None:
+        if int(forced) < 0:
+            return cpus, None
+        core = int(forced)
     os.sched_setaffinity(0, {core})
     return cpus, core
 
