@@ -1,0 +1,48 @@
+/* Host cost of the native serving loop (decisions only: no executor) for C2 rounds, the
+ * bench.py timed region without the GPU: 16 tenants x 1 request per round submitted up front,
+ * then gmx_runtime_run over all rounds (arrivals -> add_request -> step -> complete ...).
+ * build: gcc -O2 -I include tools/bench_runtime.c -L paper_1901_10008_b200/lib -lgmx_exec -lgmx_core */
+#include <stdio.h>
+#include <stdlib.h>
+#include <time.h>
+#include "../include/gmx_runtime.h"
+
+static const int64_t SH[13][3] = {{64,3136,147},{64,3136,64},{64,3136,576},{256,3136,64},{128,784,256},
+  {128,784,1152},{512,784,128},{256,196,512},{256,196,2304},{1024,196,256},{512,49,1024},{512,49,4608},{2048,49,512}};
+static double now_us(void) { struct timespec t; clock_gettime(CLOCK_MONOTONIC, &t); return t.tv_sec * 1e6 + t.tv_nsec / 1e3; }
+
+int main(int argc, char** argv) {
+    const int rounds = argc > 1 ? atoi(argv[1]) : 20000, tenants = 16;
+    const int64_t RNS = 1000000, SLO = 10000000;
+    gmx_profile p = {148, 8, 1639.6e12, 74.4e12, 6543.1e9, 4000};
+    gmx_policy_params pp = {0.25, 0.5, 2.0, 32, 8, 0.15, 10000, 0.0};
+    gmx_sched* s;
+    if (gmx_sched_create(&p, GMX_POLICY_OOO, &pp, NULL, 0.6, 0.4, 0, &s)) return 1;
+    gmx_sched_set_retire(s, 1);
+    int32_t codes[64];
+    char name[32];
+    for (int i = 0; i < tenants; ++i) { snprintf(name, sizeof name, "t%03d", i); gmx_sched_intern_stream(s, name, &codes[i]); }
+    gmx_runtime* rt;
+    if (gmx_runtime_create(s, NULL, GMX_RT_LOCKSTEP, &rt)) { printf("create: %s\n", gmx_last_error()); return 1; }
+    for (int r = 0; r < rounds; ++r)
+        for (int i = 0; i < tenants; ++i) {
+            gmx_kernel_desc k = {0};
+            k.kernel_id = (int64_t)r * tenants + i; k.stream = codes[i]; k.op = GMX_OP_GEMM; k.dtype = GMX_DT_FP16;
+            k.ndims = 3; k.dims[0] = SH[i % 13][0]; k.dims[1] = SH[i % 13][1]; k.dims[2] = SH[i % 13][2];
+            k.arrival = (int64_t)r * RNS; k.deadline = k.arrival + SLO;
+            int32_t off[2] = {0, 0}, slot = 0;
+            if (gmx_runtime_submit(rt, k.kernel_id, codes[i], k.arrival, k.deadline, &k, 1, NULL, off, &slot)) {
+                printf("submit: %s\n", gmx_last_error()); return 1; }
+        }
+    gmx_runtime_stats st;
+    const int warm = 200;
+    gmx_runtime_run(rt, (int64_t)warm * RNS - 1, NULL, &st);
+    double t0 = now_us();
+    gmx_runtime_run(rt, (int64_t)rounds * RNS - 1, NULL, &st);
+    double el = now_us() - t0;
+    printf("%.3f us per round (%lld steps, %lld dispatches over %d rounds)\n", el / (rounds - warm),
+           (long long)st.steps, (long long)st.dispatches, rounds);
+    gmx_runtime_destroy(rt);
+    gmx_sched_destroy(s);
+    return 0;
+}
