@@ -1726,7 +1726,7 @@ struct gmx_exec {
         std::vector<int64_t> last_write;       // per slot: last step (seq) that wrote its output
         std::vector<void*> graveyard;          // device tables retired during residency
         std::vector<uint8_t> zeros;            // host zeros for copy-engine clears while resident
-        int window = 10;                       // max steps a CTA may run ahead (option "resident_window")
+        int window = 16;                       // max steps a CTA may run ahead (option "resident_window")
         int64_t relay_ns = 0;                  // last residency: release -> last relay (diagnostic)
         int32_t rtrace_steps = 0;              // option "rtrace": stamp this many steps
         uint64_t* rtrace = nullptr;
