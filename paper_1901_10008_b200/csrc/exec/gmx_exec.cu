@@ -203,7 +203,7 @@ struct KernelArgs {
 // waiting on its inputs, dumped at the stop into the last two rtrace rows.
 enum InstrCounter { kIPUnit, kIPEmpty, kIMUnit, kIMTempty, kIMFull, kIEUnit, kIETfull, kISUempty, kISPub, kISOrder,
                     kISLists, kIPStages, kIEStaged, kIESplit, kIEComplete, kIEAcct, kIABar, kIAWait, kIARed, kIXNext, kIXLd, kIXStage, kIXBar2, kIXIssue, kICount };
-constexpr int kInstrRows = (kICount + 7) / 8;
+[[maybe_unused]] constexpr int kInstrRows = (kICount + 7) / 8;
 #ifdef GMX_INSTR
 #define GMX_INSTR_INC(i) (++ic[i])
 #else

@@ -12,7 +12,10 @@ static const int64_t SH[13][3] = {{64,3136,147},{64,3136,64},{64,3136,576},{256,
 static double now_us(void) { struct timespec t; clock_gettime(CLOCK_MONOTONIC, &t); return t.tv_sec * 1e6 + t.tv_nsec / 1e3; }
 
 int main(int argc, char** argv) {
-    const int rounds = argc > 1 ? atoi(argv[1]) : 20000, tenants = 16;
+    const int rounds = argc > 1 ? atoi(argv[1]) : 700, tenants = 16;
+    const int reps = argc > 2 ? atoi(argv[2]) : 1;   /* fresh runtime per repetition (profiling) */
+    double best = 1e30;
+    for (int rep = 0; rep < reps; ++rep) {
     const int64_t RNS = 1000000, SLO = 10000000;
     gmx_profile p = {148, 8, 1639.6e12, 74.4e12, 6543.1e9, 4000};
     gmx_policy_params pp = {0.25, 0.5, 2.0, 32, 8, 0.15, 10000, 0.0};
@@ -40,9 +43,12 @@ int main(int argc, char** argv) {
     double t0 = now_us();
     gmx_runtime_run(rt, (int64_t)rounds * RNS - 1, NULL, &st);
     double el = now_us() - t0;
-    printf("%.3f us per round (%lld steps, %lld dispatches over %d rounds)\n", el / (rounds - warm),
-           (long long)st.steps, (long long)st.dispatches, rounds);
+    if (el / (rounds - warm) < best) best = el / (rounds - warm);
+    if (rep == reps - 1)
+        printf("%.3f us per round, best of %d (%lld steps, %lld dispatches over %d rounds)\n", best, reps,
+               (long long)st.steps, (long long)st.dispatches, rounds);
     gmx_runtime_destroy(rt);
     gmx_sched_destroy(s);
+    }
     return 0;
 }
