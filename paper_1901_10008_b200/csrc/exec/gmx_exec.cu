@@ -1645,6 +1645,8 @@ struct HostProblem {
 // whose launch is still queued is safe and no eviction ever synchronizes the device.
 struct Plan {
     std::vector<int32_t> key;       // sorted slot list this plan was built for
+    int64_t res_seq = -1;           // resident: last step (seq) that used this plan, in residency res_epoch
+    int64_t res_epoch = -1;
     std::vector<WorkItem> items;
     std::vector<int32_t> cta_off;   // cta_off[grid + 1] then cta_flags[grid]
     void* d_buf = nullptr;          // items + offsets/flags
@@ -1720,9 +1722,7 @@ struct gmx_exec {
         gmx::DevQueue* dq = nullptr;
         int64_t seq = 0;                      // steps enqueued in this residency
         int grid = 0;
-        std::vector<std::vector<int32_t>> recent_keys;   // slot sets of the last kWindow steps
-        std::vector<const gmx::Plan*> recent_plans;
-        std::vector<int64_t> recent_seq;
+        int64_t epoch = 0;                     // residency counter (validates Plan::res_seq)
         std::vector<int64_t> last_write;       // per slot: last step (seq) that wrote its output
         std::vector<void*> graveyard;          // device tables retired during residency
         std::vector<uint8_t> zeros;            // host zeros for copy-engine clears while resident
@@ -2037,14 +2037,6 @@ static int64_t inline_item_count(const gmx_exec* ex, const std::vector<int32_t>&
     return total;
 }
 
-static bool keys_intersect(const std::vector<int32_t>& a, const std::vector<int32_t>& b) {
-    size_t i = 0, j = 0;
-    while (i < a.size() && j < b.size()) {
-        if (a[i] == b[j]) return true;
-        if (a[i] < b[j]) ++i; else ++j;
-    }
-    return false;
-}
 
 // Spin until host ring slot `slot` is free again (its previous step completed on the device).
 static int wait_slot_free(gmx_exec* ex, int64_t seq) {
@@ -2107,11 +2099,9 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
         const int32_t sl = dep_slots[i];
         if (sl >= 0 && sl < (int32_t)r.last_write.size()) need(r.last_write[sl]);
     }
-    for (size_t i = 0; i < r.recent_keys.size(); ++i)
-        if ((plan && r.recent_plans[i] == plan) || keys_intersect(r.recent_keys[i], key)) {
-            need(r.recent_seq[i]);
-            break;
-        }
+    // outputs: the last step that wrote each member slot; split-K state: the last step of this plan
+    for (int32_t sl : key) need(r.last_write[sl]);
+    if (plan && plan->res_epoch == r.epoch) need(plan->res_seq);
     StepDesc d{};
     d.probs = ex->d_probs;
     if (plan) {
@@ -2131,13 +2121,9 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
     if (d.grid > r.grid) return fail(GMX_ESTATE, "plan grid exceeds the resident grid");
     if ((rc = publish_step(ex, d))) return rc;
     for (int32_t sl : key) r.last_write[sl] = seq;
-    r.recent_keys.insert(r.recent_keys.begin(), key);
-    r.recent_plans.insert(r.recent_plans.begin(), plan);
-    r.recent_seq.insert(r.recent_seq.begin(), seq);
-    if ((int)r.recent_keys.size() > r.window) {
-        r.recent_keys.pop_back();
-        r.recent_plans.pop_back();
-        r.recent_seq.pop_back();
+    if (plan) {
+        plan->res_seq = seq;
+        plan->res_epoch = r.epoch;
     }
     if (plan) {
         plan->stats.cached = cached;
@@ -2184,9 +2170,7 @@ int gmx_exec_resident_begin_ex(gmx_exec* ex, void* stream_ptr, int32_t hold) {
     r.grid = ex->num_sms * ex->ctas_per_sm;
     r.seq = 0;
     r.stream = stream;
-    r.recent_keys.clear();
-    r.recent_plans.clear();
-    r.recent_seq.clear();
+    ++r.epoch;
     r.last_write.assign(ex->probs.size(), -1);
     KernelArgs args{};
     args.dbg = ex->dbg;
