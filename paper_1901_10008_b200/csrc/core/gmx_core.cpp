@@ -342,6 +342,45 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
             std::sort(idx.begin() + slot_of_group[g], idx.begin() + slot_of_group[g] + gcount[g],
                       [&](int32_t x, int32_t y) { return recs[x].id < recs[y].id; });
     }
+    // The greedy below depends only on the sorted sequence of (shape, multiplicity): members of
+    // one shape group are interchangeable and taken in id order. Serving rounds repeat the same
+    // shape mix, so the result is memoized as positions into idx (per thread, bounded).
+    struct Memo {
+        std::vector<int64_t> key;
+        std::vector<int32_t> pos;          // member positions (into idx) in output order
+        std::vector<Cluster> clusters;
+    };
+    static thread_local std::unordered_map<uint64_t, std::vector<Memo>> memo;
+    static thread_local std::vector<int64_t> mkey;
+    mkey.clear();
+    uint64_t mh;
+    {
+        int64_t bbits;
+        std::memcpy(&bbits, &budget, sizeof bbits);
+        mkey.push_back(bbits);
+        mkey.push_back(n);
+        for (int32_t g : gorder) {
+            const ShapeRec& r = recs[gfirst[g]];
+            mkey.push_back(((int64_t)r.op << 40) | ((int64_t)r.dtype << 20) | r.nd);
+            mkey.push_back(r.dims[0]);
+            mkey.push_back(r.dims[1]);
+            mkey.push_back(r.dims[2]);
+            mkey.push_back(gcount[g]);
+        }
+        mh = 0x243F6A8885A308D3ull;
+        for (int64_t x : mkey) mh = mix64(mh ^ (uint64_t)x);
+        auto it = memo.find(mh);
+        if (it != memo.end())
+            for (const Memo& m : it->second)
+                if (m.key == mkey) {
+                    order.resize(m.pos.size());
+                    for (size_t q = 0; q < m.pos.size(); ++q) order[q] = idx[m.pos[q]];
+                    clusters = m.clusters;
+                    return GMX_OK;
+                }
+    }
+    static thread_local std::vector<int32_t> posv;   // positions of `order` entries
+    posv.clear();
     taken.assign(n, 0);
     order.clear();
     clusters.clear();
@@ -353,6 +392,7 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
         Cluster c{seed.op, seed.dtype, seed.nd, {seed.dims[0], seed.dims[1], seed.dims[2]},
                   (int32_t)order.size(), 0, 0.0};
         order.push_back(s);
+        posv.push_back(i);
         u128 sum = (u128)seed.flops;
         int64_t count = 1, pf = seed.flops;
         // kernels of one op/dtype are contiguous in sort order
@@ -368,6 +408,7 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
             if (rc) return rc;
             if (waste_ratio(sum + (u128)cand.flops, count + 1, gf) <= budget) {
                 order.push_back(q);
+                posv.push_back(j);
                 taken[q] = 1;
                 sum += (u128)cand.flops;
                 ++count;
@@ -379,6 +420,8 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
         c.waste = waste_ratio(sum, count, pf);
         clusters.push_back(c);
     }
+    if (memo.size() > 4096) memo.clear();
+    memo[mh].push_back(Memo{mkey, posv, clusters});
     return GMX_OK;
 }
 
