@@ -409,3 +409,31 @@ def test_resident_inline_steps(ex):
     finally:
         ex.set_option("inline_plans", 0)
         ex.set_option("inline_promote", 1)
+
+
+def test_resident_long_lists_span_units(ex):
+    """Resident mode with lists of more items than one shared-memory unit holds (4): 720 small
+    GEMM members plus a GEMV and an elementwise member in one step give ~5 items per list, so
+    the list scheduler splits lists across units; every output must be complete and correct."""
+    from paper_1901_10008_b200.executor import OperandSet
+    row = [OperandSet("gemm", (64, 64, 64 * (1 + i % 3)), seed=950 + i) for i in range(720)]
+    row += [OperandSet("gemv", (4096, 1024), dtype="fp32", seed=1951),
+            OperandSet("elementwise", (1 << 20,), dtype="fp32", seed=1952, activation="gelu")]
+    slots = [o.register(ex) for o in row]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ex.launch(slots, s)   # plan built + uploaded outside residency
+        s.synchronize()
+        plan = ex.last_plan()
+        assert plan["n_items"] > 4 * plan["grid"], plan
+        for o in row:
+            o.c.zero_()
+        with ex.resident(s):
+            for _ in range(3):
+                ex.launch(slots, s, independent=False)
+        s.synchronize()
+    assert ex.resident_completed() == 3
+    for o in row:
+        _check(o)
+    for sl in slots:
+        ex.unregister(sl)
