@@ -52,7 +52,8 @@ namespace gmx {
 
 enum : int32_t { kItemGemm = 0, kItemGemv = 1, kItemEltwise = 2 };
 
-constexpr int kThreads = 256;             // 6 role warps + queue dispatcher + list scheduler (resident mode)
+constexpr int kThreads = 256;             // 6 role warps + queue dispatcher / accountant + list scheduler (resident)
+constexpr int kThreadsPerStep = 192;      // per-step launches: the 6 role warps only (warps 6-7 are resident-only)
 constexpr int kInlineMaxMembers = 32;   // members of an inline (device-enumerated) step
 constexpr size_t kSeenSlots = 4096;     // slot-set sighting counters (inline promotion)
 constexpr int kInlineMaxItems = 48;     // work items one CTA may hold in an inline step
@@ -2515,7 +2516,7 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
                     for (int32_t i = 0; i < n; ++i) args.inline_slots[i] = key[i];
                     cudaLaunchConfig_t cfg{};
                     cfg.gridDim = dim3((unsigned)grid);
-                    cfg.blockDim = dim3(kThreads);
+                    cfg.blockDim = dim3(kThreadsPerStep);
                     cfg.dynamicSmemBytes = smem_bytes<1>();
                     cfg.stream = stream;
                     cudaLaunchAttribute attr[1];
@@ -2582,7 +2583,7 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
                     ex->early_trigger ? 1 : 0};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(plan->stats.grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(kThreadsPerStep);
     cfg.dynamicSmemBytes = ex->ctas_per_sm == 2 ? smem_bytes<2>() : smem_bytes<1>();
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
