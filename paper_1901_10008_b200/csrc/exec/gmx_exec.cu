@@ -948,30 +948,19 @@ struct alignas(16) Unit {
 };
 static_assert(sizeof(Unit) == 192, "Unit layout");
 
-// Dispatcher (resident mode; block 0, warp 6): host ring -> device ring.
-__device__ void dispatch_steps(const KernelArgs& a) {
-    // held start: relay nothing until the host sets the go flag (hpub[1]), so a batch queued
-    // beforehand runs back to back and t_first..t_last times the device alone
-    const uint64_t th = global_timer_ns();
-    while (ld_acquire_sys_s64(a.hpub + 1) == 0) {
-        __nanosleep(512);
-        if (global_timer_ns() - th > 60000000000ull) __trap();
-    }
-    a.dq->t_first = global_timer_ns();
-    // relay in batches: one poll of the host count, then up to kBatch entries whose PCIe loads
-    // are all in flight together (a PCIe round trip costs ~1-2 us; one per step would cap the
-    // step rate)
-    constexpr int kBatch = 4;
-    int64_t k = 0;
-    // completion reporter (runs while the relay has nothing to do): steps [rep, rep + 16) are scanned (relaxed loads, all in flight); a
-    // step whose lists are all counted gets its host-mapped done flag (system-scope release,
-    // after an acquire fence covering the lists' release reductions); steps complete out of order
+// Completion reporter: steps [rep, rep + 16) are scanned (relaxed loads, all in flight); a step
+// whose lists are all counted gets its host-mapped done flag (system-scope release, after an
+// acquire fence covering the lists' release reductions); steps complete out of order. It runs on
+// its own lane (block 1, warp 6, between the accountant's hand-overs) so the system-scope
+// fences never delay the dispatcher's relay of newly published steps.
+struct Reporter {
     int64_t rep = 0;
     uint64_t reported = 0;
-    const uint32_t G = gridDim.x;
-    auto report = [&](int64_t limit) {
+    __device__ bool report(const KernelArgs& a, int64_t limit) {   // true if something was reported
+        const uint32_t G = gridDim.x;
         uint32_t cnt[16];
         const int span = (int)(limit - rep < 16 ? limit - rep : 16);   // completions run roughly in order
+        if (span <= 0) return false;
 #pragma unroll 4
         for (int i = 0; i < span; ++i)
             asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cnt[i]) : "l"(&a.dq->done[(rep + i) % kQueue]));
@@ -992,13 +981,43 @@ __device__ void dispatch_steps(const KernelArgs& a) {
             reported >>= 1;
             ++rep;
         }
-    };
+        return any;
+    }
+    __device__ void drain(const KernelArgs& a, int64_t limit) {   // every step before `limit`
+        const uint64_t t1 = global_timer_ns();
+        while (rep < limit) {
+            report(a, limit);
+            __nanosleep(128);
+            if (global_timer_ns() - t1 > 60000000000ull) __trap();
+        }
+    }
+};
+
+// Dispatcher (resident mode; block 0, warp 6): host ring -> device ring.
+__device__ void dispatch_steps(const KernelArgs& a) {
+    // held start: relay nothing until the host sets the go flag (hpub[1]), so a batch queued
+    // beforehand runs back to back and t_first..t_last times the device alone
+    const uint64_t th = global_timer_ns();
+    while (ld_acquire_sys_s64(a.hpub + 1) == 0) {
+        __nanosleep(512);
+        if (global_timer_ns() - th > 60000000000ull) __trap();
+    }
+    a.dq->t_first = global_timer_ns();
+    // relay in batches: one poll of the host count, then up to kBatch entries whose PCIe loads
+    // are all in flight together (a PCIe round trip costs ~1-2 us; one per step would cap the
+    // step rate)
+    constexpr int kBatch = 4;
+    int64_t k = 0;
+    // completions are reported to the host by the reporter lane (block 1, warp 6: see Reporter)
+    // when the grid has more than one block; a single-block grid reports here
+    Reporter rp{};
+    const bool self_report = gridDim.x == 1;
     for (;;) {
         int64_t avail;
         const uint64_t t0 = global_timer_ns();
         uint32_t nap = 64;   // back off while idle: each poll is a PCIe round trip
         while ((avail = ld_acquire_sys_s64(a.hpub)) <= k) {
-            report(k);
+            if (self_report) rp.report(a, k);
             __nanosleep(nap);
             nap = nap < 256 ? 2 * nap : nap;   // a new step waits at most ~0.25 us + one PCIe read
             if (global_timer_ns() - t0 > 60000000000ull) __trap();   // host never published
@@ -1050,12 +1069,7 @@ __device__ void dispatch_steps(const KernelArgs& a) {
         if (stop) break;
     }
     // after the stop: report every remaining step (the stop entry itself is k - 1)
-    const uint64_t t1 = global_timer_ns();
-    while (rep < k - 1) {
-        report(k - 1);
-        __nanosleep(128);
-        if (global_timer_ns() - t1 > 60000000000ull) __trap();
-    }
+    if (self_report) rp.drain(a, k - 1);
 }
 
 // Register cap per shape (the 2-CTA shape keeps two CTAs' registers within one SM's 64K).
@@ -1173,7 +1187,19 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         // ---------------- queue dispatcher (resident mode, block 0) / accountant ----------------
         if (lane == 0 && args.resident && blockIdx.x == 0) dispatch_steps(args);
         if (lane == 0 && accountant) {
+            const bool reporter = blockIdx.x == 1;
+            Reporter rp{};
             for (int q = 0, ph = 0;; ) {
+                if (reporter) {   // report completions while no count is waiting
+                    uint32_t nap = 32;
+                    while (!mbar_test(&afull[q], (uint32_t)ph)) {
+                        const int64_t pub = ld_acquire_gpu_s64(&args.dq->published);
+                        if (!rp.report(args, pub)) {
+                            __nanosleep(nap);
+                            nap = nap < 256 ? 2 * nap : nap;
+                        }
+                    }
+                }
                 mbar_wait(&afull[q], (uint32_t)ph);
                 const int64_t kk = aq[q];
                 if (kk < 0) break;
@@ -1181,6 +1207,8 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 mbar_arrive(&aempty[q]);
                 if (++q == kAcctQ) { q = 0; ph ^= 1; }
             }
+            // this CTA is done; every step but the stop entry still gets reported
+            if (reporter) rp.drain(args, ld_acquire_gpu_s64(&args.dq->published) - 1);
         }
     } else if (warp == 7) {
         // ---------------- list scheduler (resident mode) ----------------
