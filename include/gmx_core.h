@@ -222,6 +222,9 @@ int gmx_sched_complete(gmx_sched* s, int64_t dispatch_id, int64_t now, gmx_compl
  * live ones (decisions are unchanged; finished kernels can no longer be queried by id and kernel
  * ids must not be reused). Off by default: the reference keeps everything (scheduler.py:150-163). */
 int gmx_sched_set_retire(gmx_sched* s, int32_t on);
+/* Kernels currently ready (dependencies met, not dispatched). A step with none dispatches and
+ * withholds nothing under every policy, so a serving loop may skip it. */
+int32_t gmx_sched_ready_count(const gmx_sched* s);
 /* complete() with the observed duration in the straggler window (ratio = measured / predicted)
  * instead of the dispatch's modeled one; measured_ns < 0 is plain complete(). */
 int gmx_sched_complete_measured(gmx_sched* s, int64_t dispatch_id, int64_t now, int64_t measured_ns,

@@ -1380,6 +1380,8 @@ int gmx_sched_find_stragglers(gmx_sched* s, int32_t* out_streams, int32_t cap, i
     return GMX_OK;
 }
 
+int32_t gmx_sched_ready_count(const gmx_sched* s) { return s ? (int32_t)s->ready.size() : 0; }
+
 int gmx_sched_set_retire(gmx_sched* s, int32_t on) {
     if (!s) return fail(GMX_EINVAL, "null argument");
     s->retire = on != 0;

@@ -536,6 +536,12 @@ int gmx_runtime_run(gmx_runtime* rt, int64_t until, void* stream, gmx_runtime_st
         }
         int rc = evict_stragglers(rt, now);
         if (rc) return rc;
+        // a step with no ready kernel decides nothing (every policy): skip it (most of a C2
+        // round's completion events leave the ready set empty)
+        if (gmx_sched_ready_count(rt->sched) == 0) {
+            rt->st.now = now;
+            continue;
+        }
         rc = step_and_launch(rt, now, stream, false, nullptr);
         if (rc) return rc;
     }
