@@ -951,7 +951,7 @@ static_assert(sizeof(Unit) == 192, "Unit layout");
 // Completion reporter: steps [rep, rep + 16) are scanned (relaxed loads, all in flight); a step
 // whose lists are all counted gets its host-mapped done flag (system-scope release, after an
 // acquire fence covering the lists' release reductions); steps complete out of order. It runs on
-// its own lane (block 1, warp 6, between the accountant's hand-overs) so the system-scope
+// its own lane (the last block, warp 6, between the accountant's hand-overs) so the system-scope
 // fences never delay the dispatcher's relay of newly published steps.
 struct Reporter {
     int64_t rep = 0;
@@ -1008,7 +1008,7 @@ __device__ void dispatch_steps(const KernelArgs& a) {
     // step rate)
     constexpr int kBatch = 4;
     int64_t k = 0;
-    // completions are reported to the host by the reporter lane (block 1, warp 6: see Reporter)
+    // completions are reported to the host by the reporter lane (last block, warp 6: see Reporter)
     // when the grid has more than one block; a single-block grid reports here
     Reporter rp{};
     const bool self_report = gridDim.x == 1;
@@ -1187,7 +1187,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         // ---------------- queue dispatcher (resident mode, block 0) / accountant ----------------
         if (lane == 0 && args.resident && blockIdx.x == 0) dispatch_steps(args);
         if (lane == 0 && accountant) {
-            const bool reporter = blockIdx.x == 1;
+            const bool reporter = blockIdx.x == gridDim.x - 1;   // far from the dispatcher (block 0)
             Reporter rp{};
             for (int q = 0, ph = 0;; ) {
                 if (reporter) {   // report completions while no count is waiting
