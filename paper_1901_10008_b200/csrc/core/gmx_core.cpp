@@ -515,6 +515,8 @@ struct gmx_sched {
     gmx::CostMemo solo_memo, super_memo;      // pure cost functions, memoized per shape
     std::vector<gmx_cost> s_costs;            // superkernel cost per cached cluster ...
     std::vector<int64_t> s_cost_tenancy;      // ... and the tenancy it was computed for (-1: none)
+    std::vector<char> s_sig_seen;             // per cluster of the cached clustering: its member
+                                              // signature is known to be in withheld_sigs
     std::vector<int64_t> s_slack, s_sig, s_wakeups;
     std::vector<char> s_seen;
 
@@ -840,6 +842,7 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
         if (rc) return rc;
         s->clustered_version = s->ready_version;
         s->s_cost_tenancy.assign(s->s_clusters.size(), -1);   // superkernel costs of the new clusters
+        s->s_sig_seen.assign(s->s_clusters.size(), 0);
         s->s_costs.resize(s->s_clusters.size());
     }
     const auto& order = s->s_order;
@@ -892,7 +895,10 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
             const KernelRec& k = s->kernels[recs[order[i]].src];
             can_delay = int_ge_float(slack[order[i]], frac * (double)slo_of(s, k));
         }
-        if (can_delay) {
+        // a cluster of the cached clustering whose signature is already in withheld_sigs (e.g. the
+        // wakeup step after its withhold) cannot be withheld again: skip rebuilding the signature
+        if (can_delay && !s->s_sig_seen[sc.cluster]) {
+            s->s_sig_seen[sc.cluster] = 1;   // present after this check either way
             sig.clear();
             for (int32_t slot : members) sig.push_back(s->kernels[slot].id);
             std::sort(sig.begin(), sig.end());
