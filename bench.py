@@ -44,13 +44,28 @@ METRIC = "coalesced ops/sec & TFLOP/s at SLO vs sequential/stream multiplexing, 
 RESNET50_LIKE = [(64, 3136, 147), (64, 3136, 64), (64, 3136, 576), (256, 3136, 64), (128, 784, 256),
                  (128, 784, 1152), (512, 784, 128), (256, 196, 512), (256, 196, 2304),
                  (1024, 196, 256), (512, 49, 1024), (512, 49, 4608), (2048, 49, 512)]
-N_TENANTS = 16
+N_TENANTS = 16              # tenants per GPU at N=1 (C2); N GPUs partition 16*N tenants by default
 SLO_NS = 10_000_000
 ROUND_NS = 1_000_000        # virtual spacing of rounds (every round completes well inside it)
 
 
 def c2_shapes():
     return [RESNET50_LIKE[i % 13] for i in range(N_TENANTS)]
+
+
+def tenant_set(total):
+    """The box's tenant set: stream i = one batch-1 request of resnet50_like[i % 13] per round
+    (C2 at 16 tenants, C5 at 512). Names sort in stream order."""
+    width = max(2, len(str(total - 1)))
+    return [(f"t{i:0{width}d}", RESNET50_LIKE[i % 13]) for i in range(total)]
+
+
+def my_tenants(total, rank, world):
+    """This rank's shard: sorted stream ids dealt round-robin (sharding.shard_streams, SURVEY §8(e));
+    each GPU runs its own scheduler + executor over it, no collective on the hot path."""
+    from paper_1901_10008_b200.sharding import shard_streams
+    shape_of = dict(tenant_set(total))
+    return [(sid, shape_of[sid]) for sid in shard_streams(list(shape_of), world)[rank]]
 
 
 def useful_flops(shapes):
@@ -73,15 +88,18 @@ def load_peaks():
 
 # ---------------------------------------------------------------- distributed plumbing
 
-def dist_setup():
+def dist_setup(gloo=False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -164,7 +182,7 @@ class ClockSampler:
 # ---------------------------------------------------------------- our arm
 
 class C2Bench:
-    def __init__(self, replicas, profile_name="b200", tuning=None):
+    def __init__(self, replicas, profile_name="b200", tuning=None, tenants=None):
         import torch
 
         import paper_1901_10008_b200 as gm
@@ -173,7 +191,8 @@ class C2Bench:
         from paper_1901_10008_b200.runtime import Runtime
 
         self.torch, self.gm, self._lib = torch, gm, _lib
-        self.shapes = c2_shapes()
+        self.tenants = tenants or tenant_set(N_TENANTS)
+        self.shapes = [shape for _, shape in self.tenants]
         self.ex = Executor()
         self.replicas = replicas
         # HBM layout: per replica, the 16 activation matrices (Bt) are views into ONE contiguous
@@ -217,7 +236,7 @@ class C2Bench:
         self.profile = gm.load_profile(profile_name)
         self.policy = gm.SchedulerPolicy("ooo")
         self.rt = Runtime(self.ex, self.profile, self.policy, tuning_table=self.table)
-        self.codes = [self.rt.stream_code(f"t{i:02d}") for i in range(N_TENANTS)]
+        self.codes = [self.rt.stream_code(sid) for sid, _ in self.tenants]
         self.next_round = 0
         self.stream = torch.cuda.current_stream()
 
@@ -227,9 +246,10 @@ class C2Bench:
         import ctypes as C
         t0 = r * ROUND_NS
         rep = r % self.replicas
+        T = len(self.shapes)
         for i, (m, n, k) in enumerate(self.shapes):
             d = (_lib.KernelDesc * 1)()
-            d[0].kernel_id = r * N_TENANTS + i
+            d[0].kernel_id = r * T + i
             d[0].stream = self.codes[i]
             d[0].op = _lib.OP_CODE["gemm"]
             d[0].dtype = _lib.DT_CODE["fp16"]
@@ -240,7 +260,7 @@ class C2Bench:
             off = (C.c_int32 * 2)(0, 0)
             deps = (C.c_int64 * 1)()
             sl = (C.c_int32 * 1)(self.slots[rep][i])
-            self.rt.submit_raw(r * N_TENANTS + i, self.codes[i], t0, t0 + SLO_NS, d, 1, deps, off, sl)
+            self.rt.submit_raw(r * T + i, self.codes[i], t0, t0 + SLO_NS, d, 1, deps, off, sl)
 
     def run_rounds(self, first, count):
         return self.rt.run(until=(first + count) * ROUND_NS - 1, stream=self.stream)
@@ -290,20 +310,28 @@ def time_launch_only(bench, launches):
 def time_resident(bench, steps):
     """Average device time per step of the coalesced kernel in resident mode: `steps` steps
     (rotating operand replicas) are queued to a HELD persistent launch, then released, so they
-    run back to back; device time = release -> last step complete (%globaltimer, in-kernel)."""
+    run back to back. Timed with CUDA events: one recorded on an idle side stream right after the
+    release (the held kernel occupies the launching stream), one on the launching stream after
+    the stop step, i.e. release -> kernel exit; the in-kernel %globaltimer span (release -> last
+    step complete) is returned beside it."""
     torch = bench.torch
-    s = torch.cuda.Stream()
+    s, side = torch.cuda.Stream(), torch.cuda.Stream()
     with torch.cuda.stream(s):
         for j in range(bench.replicas):   # plans built and uploaded before the timed region
             bench.ex.launch(bench.slots[j], s, independent=True)
         s.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         bench.ex.resident_begin(s, hold=True)
         for j in range(steps):
             bench.ex.launch(bench.slots[j % bench.replicas], s, independent=True)
         bench.ex.resident_release()
+        e0.record(side)
         bench.ex.resident_end()
+        e1.record(s)
         s.synchronize()
-    return bench.ex.resident_device_ns() * 1e-9 / steps, bench.ex.last_plan()
+        side.synchronize()
+    ev_sec = e0.elapsed_time(e1) * 1e-3 / steps
+    return ev_sec, bench.ex.resident_device_ns() * 1e-9 / steps, bench.ex.last_plan()
 
 
 def time_comparators(bench, rounds):
@@ -313,7 +341,7 @@ def time_comparators(bench, rounds):
     views = []
     for row in bench.ops:
         views.append([(o.a[:, :o.dims[2]], o.b[:, :o.dims[2]].t(), o.c) for o in row])
-    streams = [torch.cuda.Stream() for _ in range(N_TENANTS)]
+    streams = [torch.cuda.Stream() for _ in range(len(bench.shapes))]
     res = {}
     for mode in ("time_only", "space_only"):
         for warm in (True, False):
@@ -394,6 +422,13 @@ def e2e_rounds(bench, first, count):
     torch.cuda.synchronize()
     sec = t0.elapsed_time(t1) * 1e-3
     return sec, h2d, d2h, first + 3 + count
+
+
+def replicas_for(tenants, requested):
+    """Operand replicas rotated by the timed rounds: enough that the replicas' operands exceed
+    4x the 126 MB L2 (every launch reads cold operands from HBM), at most `requested`."""
+    per_round = algorithmic_bytes([shape for _, shape in tenants])
+    return max(2, min(requested, -(-504_000_000 // per_round)))
 
 
 class CpuReference:
@@ -568,9 +603,16 @@ def pin_serving_thread(device_index):
 def run_ours(args, world, rank):
     import torch
     torch.backends.cuda.matmul.allow_tf32 = False
-    bench = C2Bench(args.replicas, tuning=args.tuning)
+    total_tenants = args.tenants or N_TENANTS * world
+    tenants = my_tenants(total_tenants, rank, world)
+    bench = C2Bench(replicas_for(tenants, args.replicas), tuning=args.tuning, tenants=tenants)
     shapes = bench.shapes
     flops_round = useful_flops(shapes)
+    args.replicas = bench.replicas
+    # the serving loop's core is chosen and pinned BEFORE the warmup, so the timed rounds run on
+    # a core whose caches already hold the decision core's tables (a migration right before a
+    # short window cost ~5 us per round over its first rounds)
+    all_cpus, host_core = pin_serving_thread(torch.cuda.current_device())
     # warmup (plans cached, TMA descriptors hot, clocks up; the resident executor's queue,
     # pinned ring and upload stream allocated by a first residency)
     for r in range(args.warmup):
@@ -584,7 +626,20 @@ def run_ours(args, world, rank):
     if not args.launch_per_step:
         bench.ex.resident_end()
     torch.cuda.synchronize()
-    first = args.warmup
+    # plan pre-population (not warmup steps): one round per operand replica, so every slot set
+    # the timed rounds dispatch already has its cached plan (a recurring composition's plan is
+    # built once). Without it, replicas first seen inside a short timed window
+    # would pay a synchronous plan build + upload there.
+    prewarm = args.replicas
+    for r in range(args.warmup, args.warmup + prewarm):
+        bench.queue_round(r)
+    if not args.launch_per_step:
+        bench.ex.resident_begin(bench.stream)
+    bench.run_rounds(args.warmup, prewarm)
+    if not args.launch_per_step:
+        bench.ex.resident_end()
+    torch.cuda.synchronize()
+    first = args.warmup + prewarm
     bench.next_round = first
     bad = bench.check_round_outputs()
     # ---- timed region: exactly K rounds -------------------------------------------------
@@ -595,7 +650,6 @@ def run_ours(args, world, rank):
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    all_cpus, host_core = pin_serving_thread(torch.cuda.current_device())
     with ClockSampler(torch.cuda.current_device(), avoid_core=host_core,
                       allowed=all_cpus) as clocks:
         ev0.record(bench.stream)
@@ -616,7 +670,8 @@ def run_ours(args, world, rank):
     sec = all_reduce(sec_local, torch.distributed.ReduceOp.MAX) if world > 1 else sec_local
     launches = st["launches"] - before["launches"]
     kernels = st["kernels"] - before["kernels"]
-    total_flops = flops_round * args.steps * world
+    box_flops_round = all_reduce(flops_round, torch.distributed.ReduceOp.SUM) if world > 1 else flops_round
+    total_flops = box_flops_round * args.steps
     value = total_flops / sec / 1e12
     bench.next_round = first + args.steps
     nxt = first + args.steps
@@ -624,10 +679,11 @@ def run_ours(args, world, rank):
     # resident: a held persistent launch runs a queued batch of steps back to back, device-timed
     # (%globaltimer, release -> last step complete); launch-per-step: CUDA graph of launches
     kern_launch_sec, _ = time_launch_only(bench, max(48, min(args.steps, 200)))
+    kern_gt_sec = None
     if args.launch_per_step:
         kern_sec, plan = kern_launch_sec, bench.ex.last_plan()
     else:
-        kern_sec, plan = time_resident(bench, max(64, min(args.steps, 1000)))
+        kern_sec, kern_gt_sec, plan = time_resident(bench, 1000)
     peaks = load_peaks()
     per_launch_bytes = plan["operand_bytes"]
     achieved = per_launch_bytes / kern_sec / 1e9
@@ -635,10 +691,20 @@ def run_ours(args, world, rank):
     e2e_sec, h2d, d2h, nxt = e2e_rounds(bench, nxt, max(10, min(args.steps, 50)))
     e2e_rounds_n = max(10, min(args.steps, 50))
     e2e_val = flops_round * e2e_rounds_n / e2e_sec / 1e12
+    comm = None
     if world > 1:
         import torch.distributed as dist
         e2e_sec_max = all_reduce(e2e_sec, dist.ReduceOp.MAX)
-        e2e_val = flops_round * e2e_rounds_n * world / e2e_sec_max / 1e12
+        e2e_val = box_flops_round * e2e_rounds_n / e2e_sec_max / 1e12
+        # end-of-run gather of per-rank numbers (the only collective; never on the hot path)
+        from paper_1901_10008_b200.sharding import gather_rank_stats
+        per_rank = gather_rank_stats({"rank": rank, "tenants": len(tenants), "seconds": sec_local,
+                                      "flops_per_round": flops_round, "slo_misses": st["slo_misses"],
+                                      "device": torch.cuda.get_device_name()})
+        comm = {"backend": dist.get_backend(), "world": world,
+                "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                "collectives": "all_reduce(MAX time, SUM flops) + all_gather_object after the timed region",
+                "ranks": per_rank}
     # ---- comparators + CPU baseline (rank 0, N=1 only) ------------------------------------------
     comps, cpu = None, None
     if rank == 0 and world == 1 and not args.quick:
@@ -654,18 +720,24 @@ def run_ours(args, world, rank):
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3 / args.steps, 5),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True,
+        "scaling": "strong" if args.tenants else "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic operands (A~N(0,1)/sqrt(k), B~N(0,1)), shapes of resnet50_like",
-        "config": {"workload": "C2: 16 tenant streams x 1 batch-1 request/round, "
-                               "resnet50_like[i%13] im2col GEMMs, bf16, SLO 10ms",
+        "config": {"workload": (f"C2: {total_tenants} tenant streams x 1 batch-1 request/round"
+                                if total_tenants == N_TENANTS * world else
+                                f"C5: {total_tenants} tenant streams x 1 batch-1 request/round")
+                               + (f", partitioned over {world} GPUs ({len(tenants)} on rank 0)" if world > 1 else "")
+                               + ", resnet50_like[i%13] im2col GEMMs, bf16, SLO 10ms",
+                   "tenants": total_tenants,
                    "policy": "ooo (native core, bit-exact vs gpumux)", "decision_profile": "b200",
                    "tuning_table": args.tuning or "none (reference default tiles)",
                    "step": "one scheduling round in lockstep virtual time; each scheduler step "
                            "with dispatches = one coalesced step of the resident sm_100a kernel",
                    "l2": f"inputs rotate over {args.replicas} operand replicas "
                          f"({args.replicas * algorithmic_bytes(shapes) / 1e6:.0f} MB > 126 MB L2)",
-                   "parallelism": f"tenant-shard x{world} (no hot-path collective)"},
-        "ops_per_s": round(N_TENANTS * world * args.steps / sec, 1),
+                   "parallelism": f"tenant-shard x{world} (no hot-path collective)",
+                   "plan_prewarm_rounds": prewarm},
+        "ops_per_s": round(total_tenants * args.steps / sec, 1),
         "steps_dispatched": launches,
         "launches_per_step": (launches / args.steps) if args.launch_per_step else round(1 / args.steps, 5),
         "slo_misses": st["slo_misses"],
@@ -679,8 +751,10 @@ def run_ours(args, world, rank):
                      "kernel": "gmx::coalesced_step_kernel",
                      "kernel_us": round(kern_sec * 1e6, 3),
                      "kernel_us_launch_per_step": round(kern_launch_sec * 1e6, 3),
-                     "timing": "resident: per-step device time of a held batch (%globaltimer)"
-                               if not args.launch_per_step else "CUDA graph of launches, CUDA events",
+                     "kernel_us_globaltimer": None if kern_gt_sec is None else round(kern_gt_sec * 1e6, 3),
+                     "timing": "resident: held batch of 1000 queued steps, CUDA events release -> kernel "
+                               "exit, per step" if not args.launch_per_step
+                               else "CUDA graph of launches, CUDA events",
                      "algorithmic_bytes_per_launch": per_launch_bytes,
                      "peak_source": peaks["source"] + " (MEASURED_PEAKS.json hbm_gbs)",
                      "plan": {k: plan[k] for k in ("grid", "n_items", "n_gemm_tiles", "n_split_items",
@@ -689,6 +763,8 @@ def run_ours(args, world, rank):
                 "d2h_bytes_per_step": d2h},
         "clocks": clocks.summary(),
     }
+    if comm:
+        out["comm"] = comm
     if comps:
         out["comparators"] = {k: {kk: round(vv, 4) for kk, vv in v.items()} for k, v in comps.items()}
         out["comparators"]["coalesced_vs_time_only"] = round(value / comps["time_only"]["tflops"], 2)
@@ -728,13 +804,96 @@ def run_reference(args, world, rank):
     print(json.dumps(out), flush=True)
 
 
+def run_dry(args, world, rank):
+    """--dry-run (CPU, gloo): the multi-GPU path without a GPU. Each rank takes its tenant shard,
+    runs warmup + steps rounds through the native serving loop in decisions-only mode (no
+    executor), checks its shard's per-request completion times against the oracle engine run on
+    the same sub-workload (each shard's trace equals the reference run() on it),
+    and rank 0 prints the line with whole-box numbers (sum of work / max over ranks)."""
+    import torch.distributed as dist
+
+    import paper_1901_10008_b200 as gm
+    from oracle import decisions as od
+    from oracle import sim
+    from paper_1901_10008_b200 import _lib
+    from paper_1901_10008_b200.runtime import Runtime
+    from paper_1901_10008_b200.sharding import gather_rank_stats
+    import ctypes as C
+
+    total = args.tenants or N_TENANTS * world
+    tenants = my_tenants(total, rank, world)
+    rounds = args.warmup + args.steps
+    rt = Runtime(None, gm.load_profile("b200"), gm.SchedulerPolicy("ooo"))
+    codes = [rt.stream_code(sid) for sid, _ in tenants]
+    T = len(tenants)
+    for r in range(rounds):
+        t0 = r * ROUND_NS
+        for i, (_, (m, n, k)) in enumerate(tenants):
+            d = (_lib.KernelDesc * 1)()
+            d[0].kernel_id, d[0].stream = r * T + i, codes[i]
+            d[0].op, d[0].dtype, d[0].ndims = _lib.OP_CODE["gemm"], _lib.DT_CODE["fp16"], 3
+            d[0].dims[0], d[0].dims[1], d[0].dims[2] = m, n, k
+            d[0].arrival, d[0].deadline = t0, t0 + SLO_NS
+            rt.submit_raw(r * T + i, codes[i], t0, t0 + SLO_NS, d, 1, (C.c_int64 * 1)(),
+                          (C.c_int32 * 2)(0, 0), (C.c_int32 * 1)(0))
+    h0 = time.perf_counter()
+    st = rt.run()
+    host_sec = time.perf_counter() - h0
+    got = {(tenants[rid % T][0], (rid // T) * ROUND_NS): t for rid, t in rt.drain_completions(1 << 20)}
+    # oracle engine on this shard's sub-workload (same streams, same per-round arrivals)
+    library = {f"m{j}": [{"op_kind": "gemm", "dims": list(s), "dtype": "fp16"}]
+               for j, s in enumerate(RESNET50_LIKE)}
+    workload = {"duration_ns": rounds * ROUND_NS, "streams": [
+        {"stream_id": sid, "model_name": f"m{RESNET50_LIKE.index(shape)}", "slo_ns": SLO_NS,
+         "arrival": {"kind": "fixed", "schedule": [r * ROUND_NS for r in range(rounds)]}}
+        for sid, shape in tenants]}
+    raw = json.load(open(os.path.join(REPO, "paper_1901_10008_b200", "data", "profiles.json")))
+    _tr, _m, _tl, osched = sim.simulate(workload, library, od.Prof(**raw["profiles"]["b200"]), "ooo")
+    want = {(st_["request"].stream_id, st_["request"].arrival): st_["done_at"] for st_ in osched.reqs.values()}
+    parity = got == want and len(got) == T * rounds
+    flops = useful_flops([s for _, s in tenants]) * rounds
+    stats = gather_rank_stats({"rank": rank, "tenants": [sid for sid, _ in tenants], "parity": parity,
+                               "flops": flops, "host_seconds": host_sec,
+                               "dispatched_steps": st["launches"]})
+    if rank != 0:
+        return
+    t_max = max(x["host_seconds"] for x in stats)
+    out = {"metric": METRIC, "dry_run": True, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "value": round(sum(x["flops"] for x in stats) / t_max / 1e12, 6),
+           "unit": "useful TFLOP/s of decisions (no device; host loop only)",
+           "scaling": "strong" if args.tenants else "weak", "tenants": total,
+           "shard_parity": all(x["parity"] for x in stats),
+           "comm": {"backend": dist.get_backend() if dist.is_initialized() else None, "world": world},
+           "ranks": stats}
+    print(json.dumps(out), flush=True)
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` run without torchrun: launch N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1 and pass rank 0's output through."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--replicas", type=int, default=16)
+    ap.add_argument("--replicas", type=int, default=16,
+                    help="max operand replicas rotated by the rounds (capped at 4x L2 of operands)")
+    ap.add_argument("--tenants", type=int, default=0,
+                    help="total tenant streams of the box, partitioned over the GPUs (default 16 per GPU; "
+                         "C5 = 512)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: decisions-only shards over gloo (tests the multi-rank path on CPU)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--quick", action="store_true", help="skip comparators and CPU baseline")
     ap.add_argument("--tuning", default=None,
@@ -743,9 +902,15 @@ def main():
                     help="one kernel launch per scheduler step instead of the resident executor")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-    world, rank, _ = dist_setup()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    world, rank, _ = dist_setup(gloo=args.dry_run)
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using {world} ranks", file=sys.stderr)
     try:
-        if args.impl == "reference":
+        if args.dry_run:
+            run_dry(args, world, rank)
+        elif args.impl == "reference":
             run_reference(args, world, rank)
         else:
             run_ours(args, world, rank)

@@ -77,11 +77,12 @@ EXEC_SIGNATURES = {
 _exec_lib = None
 
 
-def exec_lib():
+def exec_lib(path=None):
+    """The in-tree libgmx_exec.so. `path` (diagnostic tools only, before the first use) loads an
+    instrumented build of the same ABI instead."""
     global _exec_lib
     if _exec_lib is None:
-        # GMX_EXEC_SO: A/B experiments load another build of the same ABI
-        lib = C.CDLL(os.environ.get("GMX_EXEC_SO") or _build.build_exec())
+        lib = C.CDLL(path or _build.build_exec())
         for name, (res, args) in EXEC_SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

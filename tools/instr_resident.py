@@ -33,15 +33,16 @@ def build():
 
 
 def run(opts, steps=400):
-    os.environ["GMX_EXEC_SO"] = os.path.join(OUT, "libgmx_exec.so")
     sys.path.insert(0, REPO)
+    from paper_1901_10008_b200 import executor
+    executor.exec_lib(os.path.join(OUT, "libgmx_exec.so"))
     from bench import C2Bench, time_resident
     b = C2Bench(replicas=16)
     for k, v in opts.items():
         b.ex.set_option(k, v)
     rows = (len(NAMES) + 7) // 8
     b.ex.set_option("rtrace", steps + rows)
-    t, _ = time_resident(b, steps)
+    _, t, _ = time_resident(b, steps)
     grid = C.c_int32()
     buf = (C.c_uint64 * ((steps + rows) * 148 * 8))()
     rc = b.ex._lib.gmx_exec_resident_read_rtrace(b.ex._h, buf, len(buf), C.byref(grid))

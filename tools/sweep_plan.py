@@ -29,7 +29,7 @@ for rs, mg, combo in itertools.product(resident, merge, itertools.product(*grid.
         b.ex.set_option(k, v)
     # merge=M: one launch covers M replicas' steps (per-step cost = time / M)
     b.slots = [sum((base_slots[(j + q) % len(base_slots)] for q in range(mg)), []) for j in range(len(base_slots))]
-    t, plan = time_resident(b, 400) if rs else time_launch_only(b, 200)
+    t, plan = time_resident(b, 400)[::2] if rs else time_launch_only(b, 200)
     t /= mg
     opts["merge"] = mg
     opts["resident"] = rs

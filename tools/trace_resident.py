@@ -15,7 +15,7 @@ for kv in sys.argv[1:]:
     k, v = kv.split("=")
     b.ex.set_option(k, int(v))
 b.ex.set_option("rtrace", STEPS)
-t, plan = time_resident(b, STEPS)
+t, _, plan = time_resident(b, STEPS)
 grid = C.c_int32()
 buf = (C.c_uint64 * (STEPS * 148 * 2 * 8))()
 rc = b.ex._lib.gmx_exec_resident_read_rtrace(b.ex._h, buf, len(buf), C.byref(grid))
