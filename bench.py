@@ -167,6 +167,13 @@ class ClockSampler:
         self._t.start()
         return self
 
+    def settle(self):
+        """Wait until the sampler thread's first sample is taken, so its NVML initialisation does
+        not overlap the start of the timed region."""
+        t0 = time.perf_counter()
+        while self.nv is not None and not self.samples and time.perf_counter() - t0 < 0.5:
+            time.sleep(0.0005)
+
     def __exit__(self, *exc):
         self._stop.set()
         self._t.join()
@@ -652,6 +659,8 @@ def run_ours(args, world, rank):
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device(), avoid_core=host_core,
                       allowed=all_cpus) as clocks:
+        clocks.settle()
+        h0 = time.perf_counter()
         ev0.record(bench.stream)
         if args.launch_per_step:
             st = bench.run_rounds(first, args.steps)
@@ -659,9 +668,12 @@ def run_ours(args, world, rank):
             # resident executor: ONE persistent launch; every scheduler step the native runtime
             # takes is queued to it (include/gmx_exec.h gmx_exec_resident_begin)
             bench.ex.resident_begin(bench.stream)
+            h1 = time.perf_counter()
             st = bench.run_rounds(first, args.steps)
+            h2 = time.perf_counter()
             bench.ex.resident_end()
         ev1.record(bench.stream)
+        h3 = time.perf_counter()
         torch.cuda.synchronize()
     barrier()
     if all_cpus:
@@ -743,6 +755,10 @@ def run_ours(args, world, rank):
         "slo_misses": st["slo_misses"],
         "gpu_launches": launches if args.launch_per_step else 1,
         "host_core": host_core,
+        "host_us": ({"resident_begin": round((h1 - h0) * 1e6, 1),
+                     "serving_loop_per_round": round((h2 - h1) * 1e6 / args.steps, 3),
+                     "resident_end": round((h3 - h2) * 1e6, 1)} if not args.launch_per_step else
+                    {"serving_loop_per_round": round((h3 - h0) * 1e6 / args.steps, 3)}),
         "executor": "launch per step" if args.launch_per_step else
                     "resident (one persistent launch; steps queued through pinned host ring)",
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],

@@ -51,6 +51,10 @@ namespace gmx {
 // ------------------------------------------------------------------ device-side types
 
 enum : int32_t { kItemGemm = 0, kItemGemv = 1, kItemEltwise = 2 };
+// WorkItem.type flag: a GEMM item over fp32 operands, run as tcgen05.mma kind::tf32 (32-element
+// K blocks: the same 128-byte swizzle rows as 64 bf16, so ring stages and UMMA descriptors are shared)
+constexpr uint8_t kItemTf32 = 0x40;
+__host__ __device__ __forceinline__ int item_kind(uint8_t t) { return t & 0x3f; }
 
 constexpr int kThreads = 256;             // 6 role warps + queue dispatcher / accountant + list scheduler (resident)
 constexpr int kThreadsPerStep = 192;      // per-step launches: the 6 role warps only (warps 6-7 are resident-only)
@@ -75,7 +79,8 @@ struct SmemCfg {
     static constexpr int unit_q = kCtasPerSm == 1 ? 8 : 1;          // resident work units (1-CTA shape only)
 };
 constexpr int kTileRows = 128;             // UMMA M
-constexpr int kBlockK = 64;                // 64 bf16 = 128 B = one swizzle atom row
+constexpr int kBlockK = 64;                // 64 bf16 = 128 B = one swizzle atom row (32 fp32 for tf32 items)
+__host__ __device__ __forceinline__ int kblock_elems(bool tf32) { return tf32 ? kBlockK / 2 : kBlockK; }
 // UMMA N <= 128. (N = 256 would load the rows operand once per 256 columns — 19% fewer C2 tile
 // bytes — but its 48 KB stages leave room for only 4 in the ring, and the lost bytes in flight
 // cost more than the saved loads: 7.9 vs 7.1 us per C2 step, measured.)
@@ -284,7 +289,7 @@ __device__ __forceinline__ bool next_item(const StepView& v, ItemCursor& c, Work
             const int u = c.u++;
             if (gg % v.G != (uint32_t)v.idx) continue;
             it.problem = slot;
-            it.type = (uint8_t)kind;
+            it.type = (uint8_t)kind | (kind == kItemGemm && P->in_dt == GMX_ST_F32 ? kItemTf32 : 0);
             it.nsplit = 1;
             it.split = 0;
             it.bn = (uint8_t)P->bn;
@@ -1337,9 +1342,10 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             uint32_t phase = 0;
             auto issue_list = [&](const StepView& v) {
                 for_each_item(v, [&](const WorkItem& it, int i) {
-                    if (it.type != kItemGemm) return;
+                    if (item_kind(it.type) != kItemGemm) return;
                     const DevProblem* P = v.probs + it.problem;
                     const uint32_t bytes = kStageA + (uint32_t)it.bn * (kBlockK * 2);
+                    const int kel = kblock_elems(it.type & kItemTf32);
                     if (args.trace) args.trace[8 * i + 0] = global_timer_ns();
                     tma_prefetch_desc(&P->tm_rows);   // descriptor fetch overlaps the slot wait
                     tma_prefetch_desc(&P->tm_cols);
@@ -1348,8 +1354,8 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                         GMX_INSTR_INC(kIPStages);
                         uint8_t* tile = smem + stage * kStageBytes;
                         mbar_expect_tx(&full[stage], bytes);
-                        tma_load_2d(tile, &P->tm_rows, &full[stage], kb * kBlockK, it.row0);
-                        tma_load_2d(tile + kStageA, &P->tm_cols, &full[stage], kb * kBlockK, it.col0);
+                        tma_load_2d(tile, &P->tm_rows, &full[stage], kb * kel, it.row0);
+                        tma_load_2d(tile + kStageA, &P->tm_cols, &full[stage], kb * kel, it.col0);
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
                 }, [&] { release_unit(); });
@@ -1393,8 +1399,9 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 }
                 const StepView v = unit_view(u);
                 for_each_item(v, [&](const WorkItem& it, int i) {
-                    if (it.type != kItemGemm) return;
-                    const uint32_t idesc = idesc_bf16_m128((uint32_t)it.bn);
+                    if (item_kind(it.type) != kItemGemm) return;
+                    const bool tf32 = it.type & kItemTf32;
+                    const uint32_t idesc = tf32 ? idesc_tf32_m128((uint32_t)it.bn) : idesc_bf16_m128((uint32_t)it.bn);
                     timed(ic, kIMTempty, true, [&] { mbar_wait(&tempty[acc], acc_phase ^ 1); });
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + (uint32_t)acc * kMaxBN;
@@ -1405,10 +1412,14 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                         const uint64_t a_desc = smem_desc_sw128(tile);
                         const uint64_t b_desc = smem_desc_sw128(tile + kStageA);
 #pragma unroll
-                        for (int kk = 0; kk < kBlockK / 16; ++kk)   // 16-element UMMA K steps = +32 B
-                            if (!(args.dbg & 4))
-                                umma_bf16(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc,
-                                          (kb > it.kb0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < kBlockK / 16; ++kk) {   // UMMA K steps of 32 B (16 bf16 / 8 tf32)
+                            if (args.dbg & 4) continue;
+                            const uint32_t accum = (kb > it.kb0 || kk > 0) ? 1u : 0u;
+                            if (tf32)
+                                umma_tf32(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc, accum);
+                            else
+                                umma_bf16(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc, accum);
+                        }
                         umma_commit(&empty[stage]);
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
@@ -1522,8 +1533,8 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             }
             for_each_item(v, [&](const WorkItem& it, int i) {
                 const DevProblem* Pg = v.probs + it.problem;
-                if (args.trace && etid == 0 && it.type != kItemGemm) args.trace[8 * i + 0] = global_timer_ns();
-                if (it.type == kItemGemm) {
+                if (args.trace && etid == 0 && item_kind(it.type) != kItemGemm) args.trace[8 * i + 0] = global_timer_ns();
+                if (item_kind(it.type) == kItemGemm) {
                     const EpiParams E = load_epi(Pg);
                     timed(ic, kIETfull, true, [&] { mbar_wait(&tfull[acc], acc_phase); });
                     tc_fence_after();
@@ -1642,15 +1653,17 @@ static CUtensorMapL2promotion l2_promotion() {
     return v;
 }
 
-// bf16 [rows x K] row-major operand, leading dim `ld` elements, boxes of 64 (K) x box_rows.
-static int make_tmap(CUtensorMap* map, const void* ptr, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+// bf16 or fp32 [rows x K] row-major operand, leading dim `ld` elements, boxes of one 128-byte
+// swizzle row (64 bf16 / 32 fp32) of K x box_rows.
+static int make_tmap(CUtensorMap* map, const void* ptr, int64_t rows, int64_t K, int64_t ld, int box_rows,
+                     bool f32) {
     auto fn = encode_fn();
     if (!fn) return fail(GMX_ECUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
-    cuuint32_t box[2] = {(cuuint32_t)kBlockK, (cuuint32_t)box_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * (f32 ? 4 : 2))};
+    cuuint32_t box[2] = {(cuuint32_t)kblock_elems(f32), (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+    CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(GMX_EINVAL, "cuTensorMapEncodeTiled failed (alignment/stride?) code " + std::to_string((int)r));
@@ -1862,7 +1875,7 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
         for (int sp = 0; sp < nsplit; ++sp) {
             WorkItem it{};
             it.problem = t.slot;
-            it.type = kItemGemm;
+            it.type = kItemGemm | (P.in_dt == GMX_ST_F32 ? kItemTf32 : 0);
             it.nsplit = (uint8_t)nsplit;
             it.split = (uint8_t)sp;
             it.row0 = t.r0;
@@ -1935,7 +1948,7 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
                               [&](int32_t idx) { return cands[idx].it.nsplit > 1; });
         for (int32_t idx : per_cta[c]) {
             plan.items.push_back(cands[idx].it);
-            if (cands[idx].it.type == kItemGemm) flags[c] |= 1;
+            if (item_kind(cands[idx].it.type) == kItemGemm) flags[c] |= 1;
         }
         plan.cta_off.push_back((int32_t)plan.items.size());
     }
@@ -2379,12 +2392,12 @@ int gmx_exec_register(gmx_exec* ex, const gmx_problem_desc* d, int32_t* out_slot
     if (!d->a || !d->c) return fail(GMX_EINVAL, "operand pointer is NULL");
     const int64_t isz = d->in_dtype == GMX_ST_F32 ? 4 : 2, osz = d->out_dtype == GMX_ST_F32 ? 4 : 2;
     if (d->op == GMX_OP_GEMM) {
-        if (d->in_dtype != GMX_ST_BF16) return fail(GMX_EINVAL, "gemm operands must be bf16");
         if (d->m < 1 || d->n < 1 || d->k < 1) return fail(GMX_EINVAL, "gemm dims must be >= 1");
         if (d->m >= (1 << 30) || d->n >= (1 << 30) || d->k >= (1 << 30)) return fail(GMX_EINVAL, "gemm dims too large");
         if (!d->b) return fail(GMX_EINVAL, "gemm B operand is NULL");
         if (d->lda < d->k || d->ldb < d->k || d->ldc < d->n) return fail(GMX_EINVAL, "leading dimension too small");
-        if (d->lda % 8 || d->ldb % 8) return fail(GMX_EINVAL, "lda/ldb must be multiples of 8 elements (TMA 16-byte strides)");
+        if ((d->lda * isz) % 16 || (d->ldb * isz) % 16)
+            return fail(GMX_EINVAL, "lda/ldb rows must be multiples of 16 bytes (TMA strides)");
         if ((reinterpret_cast<uintptr_t>(d->a) | reinterpret_cast<uintptr_t>(d->b)) & 15)
             return fail(GMX_EINVAL, "A/B must be 16-byte aligned");
         // orientation: the side that needs fewer (128 + BN) x K tile loads goes on UMMA-M
@@ -2403,13 +2416,14 @@ int gmx_exec_register(gmx_exec* ex, const gmx_problem_desc* d, int32_t* out_slot
             if (d->tile_n != 64 && d->tile_n != 128) return fail(GMX_EINVAL, "tile_n must be 0, 64 or 128");
             P.bn = d->tile_n;
         }
-        P.kblocks = (int32_t)((d->k + kBlockK - 1) / kBlockK);
+        const bool f32 = d->in_dtype == GMX_ST_F32;   // fp32 operands: tf32 UMMA
+        P.kblocks = (int32_t)((d->k + kblock_elems(f32) - 1) / kblock_elems(f32));
         const void* rows_ptr = swap ? d->b : d->a;
         const void* cols_ptr = swap ? d->a : d->b;
         const int64_t rows_ld = swap ? d->ldb : d->lda, cols_ld = swap ? d->lda : d->ldb;
         int rc;
-        if ((rc = make_tmap(&P.tm_rows, rows_ptr, P.rows, d->k, rows_ld, kTileRows)) ||
-            (rc = make_tmap(&P.tm_cols, cols_ptr, P.cols, d->k, cols_ld, P.bn)))
+        if ((rc = make_tmap(&P.tm_rows, rows_ptr, P.rows, d->k, rows_ld, kTileRows, f32)) ||
+            (rc = make_tmap(&P.tm_cols, cols_ptr, P.cols, d->k, cols_ld, P.bn, f32)))
             return rc;
         // output tensor map (TMA-store epilogue) when C allows 16-byte-aligned rows
         P.tma_out = 0;
@@ -2428,7 +2442,7 @@ int gmx_exec_register(gmx_exec* ex, const gmx_problem_desc* d, int32_t* out_slot
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
                 P.tma_out = 1;
         }
-        hp.op_bytes = 2 * (d->m * d->k + d->k * d->n) + osz * d->m * d->n;
+        hp.op_bytes = isz * (d->m * d->k + d->k * d->n) + osz * d->m * d->n;
         hp.flops = 2 * d->m * d->n * d->k;
     } else if (d->op == GMX_OP_GEMV) {
         if (d->m < 1 || d->n < 1 || d->m >= (1 << 30) || d->n >= (1 << 30)) return fail(GMX_EINVAL, "bad gemv dims");

@@ -183,6 +183,17 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint
         : "memory");
 }
 
+// D[tmem] (+)= A[smem] * B[smem]^T, fp32 operands read as tf32 (10-bit mantissa), fp32 accumulate.
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // Arrive on `bar` once all previously issued tcgen05.mma of this thread have completed.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -205,6 +216,15 @@ __device__ __forceinline__ uint32_t idesc_bf16_m128(uint32_t n) {
     return (1u << 4)            // D format f32
            | (1u << 7)          // A format bf16
            | (1u << 10)         // B format bf16
+           | ((n >> 3) << 17)   // N / 8
+           | ((128u >> 4) << 24);  // M / 16
+}
+
+// Instruction descriptor: kind::tf32, A=B=tf32 (format 2), D=f32, both K-major, M=128, N=n.
+__device__ __forceinline__ uint32_t idesc_tf32_m128(uint32_t n) {
+    return (1u << 4)            // D format f32
+           | (2u << 7)          // A format tf32
+           | (2u << 10)         // B format tf32
            | ((n >> 3) << 17)   // N / 8
            | ((128u >> 4) << 24);  // M / 16
 }

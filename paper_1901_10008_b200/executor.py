@@ -144,10 +144,11 @@ class Executor:
         return slot.value
 
     def register_gemm(self, a, bt, c, bias=None, activation="none", k=None, tile_n=0):
-        """C[m,n] = act(A[m,k] . Bt[n,k]^T + bias[m]); A/Bt bf16 with row stride % 8 == 0.
+        """C[m,n] = act(A[m,k] . Bt[n,k]^T + bias[m]); A/Bt bf16 (tcgen05 kind::f16) or fp32 (read
+        as tf32, kind::tf32: the reference's "fp32" GEMMs, kernels.py:22), rows 16-byte aligned.
         tile_n: UMMA N of the output tiles (64/128; 0 = automatic, or a measured TuningTable's)."""
-        self._check_tensor(a, "A", (torch.bfloat16,))
-        self._check_tensor(bt, "Bt", (torch.bfloat16,))
+        self._check_tensor(a, "A", (torch.bfloat16, torch.float32))
+        self._check_tensor(bt, "Bt", (a.dtype,))
         self._check_tensor(c, "C", (torch.bfloat16, torch.float32))
         m, n = c.shape
         k = a.shape[1] if k is None else k
@@ -155,7 +156,7 @@ class Executor:
             raise ValueError("gemm operand shapes disagree")
         if a.stride(1) != 1 or bt.stride(1) != 1 or c.stride(1) != 1:
             raise ValueError("gemm operands must be row-major (unit inner stride)")
-        d = ProblemDesc(op=_lib.OP_CODE["gemm"], in_dtype=0, out_dtype=ST[c.dtype],
+        d = ProblemDesc(op=_lib.OP_CODE["gemm"], in_dtype=ST[a.dtype], out_dtype=ST[c.dtype],
                         activation=ACT[activation], m=m, n=n, k=k, a=a.data_ptr(), lda=a.stride(0),
                         b=bt.data_ptr(), ldb=bt.stride(0), c=c.data_ptr(), ldc=c.stride(0),
                         bias=self._bias_ptr(bias, m), tile_n=int(tile_n))
@@ -320,7 +321,8 @@ class Executor:
 class OperandSet:
     """Synthetic per-kernel operands in the executor's HBM layout (bench / tests).
 
-    gemm:  A[m, lda] bf16 ~ N(0,1)/sqrt(k), Bt[n, ldb] bf16 ~ N(0,1), C[m, n]
+    gemm:  A[m, lda] ~ N(0,1)/sqrt(k), Bt[n, ldb] ~ N(0,1), C[m, n]: bf16 operands for the
+           reference's "fp16" kernels, fp32 operands (tf32 UMMA, fp32 C) for its "fp32" ones
     gemv:  W[m, n] ~ U(-1,1), x[n] ~ U(-1,1), y[m]   (fp32 or bf16)
     elementwise: x[n] ~ N(0,1), y[n]
     lda/ldb are padded to 16-byte rows; the pad columns hold garbage (NaN) on
@@ -337,13 +339,13 @@ class OperandSet:
         self.storage = st
         if op_kind == "gemm":
             m, n, k = dims
-            ld = padded_ld(k)
-            a = torch.full((m, ld), float("nan"), dtype=torch.bfloat16)
-            a[:, :k] = (torch.randn(m, k, generator=g) / k ** 0.5).to(torch.bfloat16)
-            bt = torch.full((n, ld), float("nan"), dtype=torch.bfloat16)
-            bt[:, :k] = torch.randn(n, k, generator=g).to(torch.bfloat16)
+            ld = padded_ld(k, st)
+            a = torch.full((m, ld), float("nan"), dtype=st)
+            a[:, :k] = (torch.randn(m, k, generator=g) / k ** 0.5).to(st)
+            bt = torch.full((n, ld), float("nan"), dtype=st)
+            bt[:, :k] = torch.randn(n, k, generator=g).to(st)
             self.a, self.b = a.to(device), bt.to(device)
-            odt = out_dtype or torch.bfloat16
+            odt = out_dtype or st
             # C rows padded to 16 bytes so the epilogue can TMA-store whole tiles
             self.c = torch.empty(m, padded_ld(n, odt), dtype=odt, device=device)[:, :n]
             self.bias = (torch.randn(m, generator=g) * 0.1).to(device) if bias else None
@@ -367,10 +369,10 @@ class OperandSet:
         self.storage = st
         if op_kind == "gemm":
             m, n, k = dims
-            ld = padded_ld(k)
-            self.a = (torch.randn(m, ld, generator=g, device=device) / k ** 0.5).to(torch.bfloat16)
-            self.b = torch.randn(n, ld, generator=g, device=device).to(torch.bfloat16)
-            odt = out_dtype or torch.bfloat16
+            ld = padded_ld(k, st)
+            self.a = (torch.randn(m, ld, generator=g, device=device) / k ** 0.5).to(st)
+            self.b = torch.randn(n, ld, generator=g, device=device).to(st)
+            odt = out_dtype or st
             self.c = torch.empty(m, padded_ld(n, odt), dtype=odt, device=device)[:, :n]
         elif op_kind == "gemv":
             m, n = dims

@@ -4,6 +4,7 @@ Every test launches through the product path (libgmx_exec.so via the C ABI)
 and compares with oracle/numerics.py on the same rounded operands.
 Tolerances (stated in oracle/numerics.py):
   bf16 out: max|C-ref| <= 4e-3*max|ref| + 1e-6 ;  fp32 out: <= 1e-4*max|ref| + 1e-6
+  fp32 GEMM operands (tf32 UMMA) vs float64 on the UNROUNDED fp32 operands: <= 5e-3*max|ref| + 1e-6
 """
 
 import numpy as np
@@ -43,7 +44,8 @@ def _check(ops):
     got = _np(ops.c)
     ref = _ref(ops)
     bf = ops.c.dtype == torch.bfloat16
-    assert on.within(got, ref, bf), (ops.op_kind, ops.dims, on.rel_err(got, ref))
+    tf32 = ops.op_kind == "gemm" and ops.a.dtype == torch.float32
+    assert on.within(got, ref, bf, tf32), (ops.op_kind, ops.dims, on.rel_err(got, ref))
 
 
 def _run(ex, opsets):
@@ -84,6 +86,36 @@ def test_fused_bias_activation(ex, act, out):
     _run(ex, [OperandSet("gemm", (256, 196, 512), seed=3, bias=True, activation=act, out_dtype=out),
               OperandSet("gemm", (64, 3136, 147), seed=4, bias=True, activation=act, out_dtype=out),
               OperandSet("gemm", (512, 49, 4608), seed=5, bias=True, activation=act, out_dtype=out)])
+
+
+@pytest.mark.parametrize("dims", C2_SHAPES + [(1, 1, 1), (7, 5, 3), (130, 33, 65), (33, 130, 200),
+                                  (1000, 1, 2048), (96, 96, 4608)])
+def test_tf32_gemm_fp32_operands(ex, dims):
+    """The reference's "fp32" GEMMs (kernels.py:22,122-124; every models.json model): fp32 A/Bt in
+    HBM, tcgen05 kind::tf32, fp32 C, vs float64 on the unrounded operands."""
+    from paper_1901_10008_b200.executor import OperandSet
+    o = OperandSet("gemm", dims, dtype="fp32", seed=sum(dims) + 7)
+    assert o.a.dtype == torch.float32 and o.c.dtype == torch.float32
+    _run(ex, [o])
+
+
+@pytest.mark.parametrize("act", ["none", "relu", "gelu"])
+def test_tf32_mixed_with_bf16_in_one_launch(ex, act):
+    """fp32 (tf32) and bf16 members, fused bias/activation, split-K candidates, in one launch."""
+    from paper_1901_10008_b200.executor import OperandSet
+    _run(ex, [OperandSet("gemm", (512, 49, 4608), dtype="fp32", seed=11, bias=True, activation=act),
+              OperandSet("gemm", (64, 3136, 147), dtype="fp32", seed=12, bias=True, activation=act),
+              OperandSet("gemm", (256, 196, 512), seed=13, bias=True, activation=act),
+              OperandSet("gemm", (2048, 49, 512), dtype="fp32", seed=14),
+              OperandSet("gemm", (128, 784, 1152), dtype="fp32", seed=15, out_dtype=torch.bfloat16)])
+
+
+def test_tf32_rejects_mixed_operand_dtypes(ex):
+    a = torch.zeros(64, 64, dtype=torch.float32, device="cuda")
+    bt = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
+    c = torch.zeros(64, 64, dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError):
+        ex.register_gemm(a, bt, c)
 
 
 def test_c2_coalesced_single_launch(ex):

@@ -68,7 +68,8 @@ def _run_workload(workload, library, profile_name="b200", params=None, check_num
             else:
                 ref = on.elementwise(a)
             got_c = o.c.float().cpu().numpy()
-            assert on.within(got_c, ref, o.c.dtype == torch.bfloat16), (kid, o.dims)
+            tf32 = o.op_kind == "gemm" and o.a.dtype == torch.float32
+            assert on.within(got_c, ref, o.c.dtype == torch.bfloat16, tf32), (kid, o.dims, on.rel_err(got_c, ref))
     return stats
 
 
@@ -81,6 +82,26 @@ def test_runtime_c2_matches_oracle_engine(resident):
     lib["resnet50_like_fp16"] = [dict(p, dtype="fp16") for p in lib["resnet50_like"]]
     stats = _run_workload(wl, lib, resident=resident)
     assert stats["completed_requests"] == 16 and stats["launches"] >= 1
+
+
+@pytest.mark.parametrize("resident", [False, True])
+def test_runtime_gemm16_fp32_tf32(resident):
+    """The reference's bundled gemm16 workload (16 x gemm(64,3136,576) "fp32"): fp32 operands
+    stay fp32 in HBM and run as tf32 UMMA; decisions vs the oracle engine, numerics vs float64 on
+    the UNROUNDED fp32 operands (5e-3)."""
+    traces = load_golden("traces.json")
+    stats = _run_workload(traces["workloads"]["gemm16"], load_golden("models.json"), resident=resident)
+    assert stats["completed_requests"] == 16
+
+
+@pytest.mark.parametrize("resident", [False, True])
+def test_runtime_resnet50_like_fp32_chains(resident):
+    """models.json resnet50_like as the reference ships it (fp32, 13-kernel chains), 4 streams."""
+    wl = {"duration_ns": 5_000_000, "streams": [
+        {"stream_id": f"r{i}", "model_name": "resnet50_like", "slo_ns": 10_000_000,
+         "arrival": {"kind": "fixed", "schedule": [0, 400_000 * (i + 1)]}} for i in range(4)]}
+    stats = _run_workload(wl, load_golden("models.json"), resident=resident)
+    assert stats["completed_requests"] == 8
 
 
 @pytest.mark.parametrize("resident", [False, True])
