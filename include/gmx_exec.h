@@ -127,6 +127,10 @@ int gmx_exec_resident_begin_ex(gmx_exec* ex, void* stream, int32_t hold);
 int gmx_exec_resident_release(gmx_exec* ex);
 int gmx_exec_resident_device_ns(gmx_exec* ex, int64_t* ns);
 int gmx_exec_resident_end(gmx_exec* ex);
+/* After a residency ended (and its stream was synchronized): the dispatcher SM's average clock
+ * in MHz from the kernel's start to the stop step (%clock64 / %globaltimer on the device), and
+ * that span in ns. Clocks under load without host-side sampling. */
+int gmx_exec_resident_sm_clock(gmx_exec* ex, double* mhz, int64_t* span_ns);
 int gmx_exec_resident_completed(gmx_exec* ex, int64_t* steps_done);
 int gmx_exec_resident_active(const gmx_exec* ex);
 /* 1 once resident step `seq` (from gmx_exec_launch_deps) completed on the device, else 0. */
@@ -141,7 +145,9 @@ int gmx_exec_clear_plans(gmx_exec* ex);
  * then epilogue sub-phases: staging start, staged, barrier, store issued). */
 int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value);
 /* Copy the last traced launch: stamps[8*n_items], items[8*n_items] (raw 32-byte work items),
- * cta_off[grid+1]. Call with capacity 0 to query sizes. Synchronizes the device. */
+ * cta_off[grid+1]. Call with capacity 0 to query sizes. With capacity >= n_items + grid, stamps
+ * also receives grid rows of per-CTA kernel stamps (entry, prologue done, role loops done, exit;
+ * 4 used of 8) after the item rows. Synchronizes the device. */
 int gmx_exec_read_trace(const gmx_exec* ex, uint64_t* stamps, int32_t* items, int32_t* cta_off,
                         int32_t capacity, int32_t* n_items, int32_t* grid);
 

@@ -94,6 +94,7 @@ constexpr int smem_bytes() {
     return C::stages * kStageBytes + C::stage_out + C::align_pad + C::unit_q * 192 /*unit ring*/ + 512 /*barriers*/;
 }
 static_assert(2 * (smem_bytes<2>() + 1024) <= 233472, "two CTAs must fit one SM's shared memory");
+constexpr int kMaxGrid = 512;              // upper bound of a launch's grid (2 x SMs), trace rows
 constexpr int kWsBlock = 4096;             // split-K workspace allocation unit (floats)
 
 struct alignas(64) DevProblem {
@@ -174,7 +175,10 @@ struct DevQueue {
     uint64_t t_first;         // %globaltimer when step 0 was relayed (after a held start's release)
     uint64_t t_last;          // %globaltimer of the latest step completion
     uint64_t t_relay;         // %globaltimer of the dispatcher's latest relay
-    int64_t _pad[4];
+    uint64_t t_stop;          // %globaltimer when the dispatcher relayed the stop entry
+    uint64_t c_first;         // dispatcher SM's %clock64 at t_first / t_stop: the SM clock over
+    uint64_t c_stop;          // the residency, measured on the device (no host-side sampling)
+    int64_t _pad[1];
     uint32_t done[kQueue];    // monotonic count of item lists finished, per slot
     uint32_t grab[kQueue];    // monotonic list-grab counter, per slot (2 x grid per step)
 };
@@ -1008,6 +1012,7 @@ __device__ void dispatch_steps(const KernelArgs& a) {
         if (global_timer_ns() - th > 60000000000ull) __trap();
     }
     a.dq->t_first = global_timer_ns();
+    a.dq->c_first = clock64();
     // relay in batches: one poll of the host count, then up to kBatch entries whose PCIe loads
     // are all in flight together (a PCIe round trip costs ~1-2 us; one per step would cap the
     // step rate)
@@ -1073,6 +1078,8 @@ __device__ void dispatch_steps(const KernelArgs& a) {
         a.dq->t_relay = global_timer_ns();
         if (stop) break;
     }
+    a.dq->t_stop = global_timer_ns();
+    a.dq->c_stop = clock64();
     // after the stop: report every remaining step (the stop entry itself is k - 1)
     if (self_report) rp.drain(a, k - 1);
 }
@@ -1106,6 +1113,11 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
+    // trace mode (per-step launches): per-CTA stamps after the item rows: entry, prologue done,
+    // role loops done, exit
+    uint64_t* ktr = (args.trace && !args.resident)
+                        ? args.trace + 8 * ((int64_t)args.cta_off[gridDim.x] + blockIdx.x) : nullptr;
+    if (ktr && threadIdx.x == 0) ktr[0] = global_timer_ns();
 #ifdef GMX_INSTR
     long long ic[kICount] = {};
 #else
@@ -1139,6 +1151,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = has_gemm ? *tmem_slot : 0u;
+    if (ktr && threadIdx.x == 0) ktr[1] = global_timer_ns();
     // Programmatic dependent launch: everything above overlapped the previous step's tail; a
     // dependent step waits here until that grid has completed and flushed its memory.
     if (!args.independent) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1605,6 +1618,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         if (etid == 0) bulk_wait_read0();
     }
 
+    if (ktr && warp == 2 && lane == 0) ktr[2] = global_timer_ns();
     tc_fence_before();
     __syncthreads();
     // this CTA's work is done: the next step may start taking SMs
@@ -1613,6 +1627,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         tc_fence_after();
         tmem_dealloc(tmem_base, Cfg::tmem_cols);
     }
+    if (ktr && threadIdx.x == 32) ktr[3] = global_timer_ns();
 }
 
 // ------------------------------------------------------------------ host side
@@ -2203,11 +2218,13 @@ int gmx_exec_resident_begin_ex(gmx_exec* ex, void* stream_ptr, int32_t hold) {
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
     int rc;
     if ((rc = ensure_table(ex, stream))) return rc;
-    std::memset(r.hring, 0, kQueue * sizeof(StepDesc));
+    // ring entries are read only once published (hpub), so neither ring needs clearing; the
+    // completion flags and the device counters restart from zero with the new residency's seq
     std::memset(r.hdone, 0, kQueue * sizeof(int64_t));
     __atomic_store_n(r.hpub, (int64_t)0, __ATOMIC_RELEASE);
     __atomic_store_n(r.hpub + 1, (int64_t)(hold ? 0 : 1), __ATOMIC_RELEASE);   // go flag
-    GMX_CUDA(cudaMemsetAsync(r.dq, 0, sizeof(DevQueue), stream));
+    GMX_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(r.dq) + offsetof(DevQueue, published), 0,
+                             sizeof(DevQueue) - offsetof(DevQueue, published), stream));
     if ((rc = set_kernel_attrs(ex))) return rc;
     r.grid = ex->num_sms * ex->ctas_per_sm;
     r.seq = 0;
@@ -2284,6 +2301,18 @@ int gmx_exec_resident_step_done(gmx_exec* ex, int64_t seq) {
     if (!r.hdone) return 0;
     if (seq < r.seq - kQueue) return 1;   // its ring slot was recycled, so it completed
     return ((volatile int64_t*)r.hdone)[seq % kQueue] >= seq + 1 ? 1 : 0;
+}
+
+int gmx_exec_resident_sm_clock(gmx_exec* ex, double* mhz, int64_t* span_ns) {
+    if (!ex || !mhz) return fail(GMX_EINVAL, "null argument");
+    if (!ex->res.dq) return fail(GMX_ESTATE, "never resident");
+    if (ex->res.active) return fail(GMX_ESTATE, "residency still active");
+    uint64_t t[6];   // t_first t_last t_relay t_stop c_first c_stop
+    GMX_CUDA(cudaMemcpy(t, &ex->res.dq->t_first, sizeof t, cudaMemcpyDeviceToHost));
+    const double dt = (double)(t[3] - t[0]);
+    *mhz = dt > 0 ? (double)(t[5] - t[4]) / dt * 1e3 : 0.0;
+    if (span_ns) *span_ns = (int64_t)dt;
+    return GMX_OK;
 }
 
 int gmx_exec_resident_relay_ns(gmx_exec* ex, int64_t* out) {
@@ -2610,7 +2639,8 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
     if (ex->tracing && (int64_t)plan->items.size() > ex->trace_cap) {
         if (ex->trace) GMX_CUDA(cudaFree(ex->trace));
         ex->trace_cap = std::max<int64_t>(1024, (int64_t)plan->items.size());
-        GMX_CUDA(cudaMalloc(&ex->trace, ex->trace_cap * 8 * sizeof(uint64_t)));
+        // item rows + one row of kernel stamps per CTA
+        GMX_CUDA(cudaMalloc(&ex->trace, (ex->trace_cap + 2 * kMaxGrid) * 8 * sizeof(uint64_t)));
     }
     if (ex->tracing) {
         GMX_CUDA(cudaMemsetAsync(ex->trace, 0, plan->items.size() * 8 * sizeof(uint64_t), stream));
@@ -2745,7 +2775,9 @@ int gmx_exec_read_trace(const gmx_exec* ex, uint64_t* stamps, int32_t* items, in
     *grid = ex->last->stats.grid;
     if (capacity < n) return GMX_OK;
     GMX_CUDA(cudaDeviceSynchronize());
-    GMX_CUDA(cudaMemcpy(stamps, ex->trace, (size_t)n * 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    // capacity >= n + grid: the per-CTA kernel stamp rows (entry, prologue done, loops done, exit) too
+    const int64_t rows = capacity >= n + *grid ? (int64_t)n + *grid : n;
+    GMX_CUDA(cudaMemcpy(stamps, ex->trace, (size_t)rows * 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     for (int32_t i = 0; i < n; ++i) std::memcpy(items + 8 * i, &ex->last->items[i], sizeof(WorkItem));
     for (int32_t c = 0; c <= ex->last->stats.grid; ++c) cta_off[c] = ex->last->cta_off[c];
     return GMX_OK;

@@ -69,6 +69,7 @@ EXEC_SIGNATURES = {
     "gmx_exec_resident_read_rtrace": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int32)]),
     "gmx_exec_resident_device_ns": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "gmx_exec_resident_completed": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "gmx_exec_resident_sm_clock": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "gmx_exec_read_trace": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int32),
                                       C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32),
                                       C.POINTER(C.c_int32)]),
@@ -258,6 +259,19 @@ class Executor:
         _check(self._lib.gmx_exec_resident_device_ns(self._h, C.byref(n)))
         return n.value
 
+    def resident_sm_clock(self):
+        """(MHz, span ns): the SM clock over the last residency, measured on the device."""
+        mhz, ns = C.c_double(), C.c_int64()
+        _check(self._lib.gmx_exec_resident_sm_clock(self._h, C.byref(mhz), C.byref(ns)))
+        return mhz.value, ns.value
+
+    def _relay_ns(self) -> int:
+        """Diagnostics: %globaltimer from step 0's relay to the dispatcher's latest relay (valid
+        after resident_device_ns)."""
+        n = C.c_int64()
+        _check(self._lib.gmx_exec_resident_relay_ns(self._h, C.byref(n)))
+        return n.value
+
     def resident_end(self):
         """Queue the stop step; work later on the resident stream is ordered after all steps."""
         _check(self._lib.gmx_exec_resident_end(self._h))
@@ -292,11 +306,13 @@ class Executor:
         kb1, split, nsplit, cta, t_prod, t_mma_done, t_epi, t_end (ns, absolute)."""
         n, grid = C.c_int32(), C.c_int32()
         _check(self._lib.gmx_exec_read_trace(self._h, None, None, None, 0, C.byref(n), C.byref(grid)))
-        stamps = (C.c_uint64 * (8 * max(1, n.value)))()
+        stamps = (C.c_uint64 * (8 * (max(1, n.value) + grid.value)))()
         raw = (C.c_int32 * (8 * max(1, n.value)))()
         off = (C.c_int32 * (grid.value + 1))()
-        _check(self._lib.gmx_exec_read_trace(self._h, stamps, raw, off, n.value, C.byref(n),
+        _check(self._lib.gmx_exec_read_trace(self._h, stamps, raw, off, n.value + grid.value, C.byref(n),
                                              C.byref(grid)))
+        # per-CTA kernel stamps: entry, prologue done, role loops done, exit
+        self.kernel_stamps = [tuple(stamps[8 * (n.value + c) + j] for j in range(4)) for c in range(grid.value)]
         cta_of = {}
         for c in range(grid.value):
             for i in range(off[c], off[c + 1]):
