@@ -84,10 +84,13 @@ int gmx_runtime_set_profiling(gmx_runtime* rt, int32_t on);   /* off by default 
 int gmx_runtime_set_measured_stragglers(gmx_runtime* rt, int32_t on);
 int64_t gmx_runtime_clock_ns(const gmx_runtime* rt);
 /* Replay log (realtime mode). Records, in order:
- *   kind 0: complete(dispatch_id=a) at time t      kind 1: add_request(request_id=a) at t
+ *   kind 0: complete(dispatch_id=a) at time t; off = the observed duration fed to the straggler
+ *           windows (set_measured_stragglers), -1 when the modeled duration was used
+ *   kind 1: add_request(request_id=a) at t
  *   kind 2: step(t) -> dispatch a with kernels [off, off+n) of kernel_ids
  *   kind 3: step(t) withheld group [off, off+n)       kind 4: step(t) wakeup a (-1: none)
  *   kind 5: step(t) (marks the step boundary; precedes its kind 2/3/4 records)
+ *   kind 6: straggler eviction of stream a at t (before the step at t)
  * Copies up to `capacity` records; *n_out = total available. */
 typedef struct gmx_replay_rec {
     int32_t kind;

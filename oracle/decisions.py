@@ -312,11 +312,14 @@ class OracleScheduler:
         return k.deadline - now - self.predicted_remaining(k)
 
     # completion: scheduler.py:210-235
-    def complete(self, did, now):
+    def complete(self, did, now, measured=None):
+        """`measured`: an observed duration (ns) replacing the modeled one in the straggler
+        ratio (the build's wall-clock engine; the reference always uses
+        d.duration, i.e. measured=None)."""
         d = self.in_flight.pop(did)
         self.free_sms += d.sm_allocation
         finished = []
-        ratio = d.duration / max(d.predicted_duration, 1)
+        ratio = (d.duration if measured is None else measured) / max(d.predicted_duration, 1)
         for kid in d.kernel_ids:
             self.done.add(kid)
             st = self.reqs[self.owner[kid]]

@@ -455,11 +455,10 @@ static int run_realtime(gmx_runtime* rt, int64_t until, void* stream, gmx_runtim
                     continue;
                 }
                 gmx_complete_view cv;
-                int rc = rt->measured_ratios
-                             ? gmx_sched_complete_measured(rt->sched, did, now, now - rt->inflight[i].start, &cv)
-                             : gmx_sched_complete(rt->sched, did, now, &cv);
+                const int64_t measured = rt->measured_ratios ? now - rt->inflight[i].start : -1;
+                int rc = gmx_sched_complete_measured(rt->sched, did, now, measured, &cv);
                 if (rc) return fail(rc, std::string("complete: ") + gmx_last_error());
-                log_rec(rt, 0, now, did);
+                log_rec(rt, 0, now, did, 0, measured);
                 on_finished(rt, cv, now);
             }
             if (rt->inflight[i].seq < 0) rt->event_pool.push_back(rt->inflight[i].ev);

@@ -202,6 +202,17 @@ class Runtime:
         return [(r.kind, r.t, r.a, tuple(kids[r.off:r.off + r.n]) if r.kind in (2, 3) else ())
                 for r in recs[:n.value]]
 
+    def measured_durations(self) -> dict:
+        """dispatch id -> the observed duration (ns) its completion fed to the straggler windows
+        (wall-clock mode with set_measured_stragglers; replay-log kind 0)."""
+        lib = _rt_lib()
+        n, nk = C.c_int64(), C.c_int64()
+        _check(lib.gmx_runtime_replay_log(self._rt, None, 0, C.byref(n), None, 0, C.byref(nk)))
+        recs = (ReplayRec * max(1, n.value))()
+        kids = (C.c_int64 * max(1, nk.value))()
+        _check(lib.gmx_runtime_replay_log(self._rt, recs, n.value, C.byref(n), kids, nk.value, C.byref(nk)))
+        return {r.a: r.off for r in recs[:n.value] if r.kind == 0 and r.off >= 0}
+
     def drain_completions(self, capacity=65536):
         ids = (C.c_int64 * capacity)()
         ts = (C.c_int64 * capacity)()
