@@ -88,6 +88,15 @@ constexpr int kMaxBN = 128;
 constexpr int kStageA = kTileRows * kBlockK * 2;   // 16 KB
 constexpr int kStageB = kMaxBN * kBlockK * 2;      // 16 KB
 constexpr int kStageBytes = kStageA + kStageB;
+// GEMV rows staged through the TMA ring (bulk copies into the 32 KB stages): whole rows of at
+// most one stage, up to 16 per stage. Returns 0 when a problem cannot be staged (row larger than
+// a stage, or rows / base not 16-byte aligned): its items stream rows with 16-byte loads instead.
+__host__ __device__ __forceinline__ int gemv_rows_per_stage(int64_t row_bytes, int64_t pitch_bytes, uintptr_t base) {
+    if (row_bytes <= 0 || row_bytes > kStageBytes || (row_bytes & 15) || (pitch_bytes & 15) || (base & 15)) return 0;
+    const int64_t r = kStageBytes / row_bytes;
+    return (int)(r < 16 ? r : 16);
+}
+
 template <int kCtasPerSm>
 constexpr int smem_bytes() {
     using C = SmemCfg<kCtasPerSm>;
@@ -307,7 +316,10 @@ __device__ __forceinline__ bool next_item(const StepView& v, ItemCursor& c, Work
             } else if (kind == kItemGemv) {
                 it.row0 = u * kInlineGemvRows;
                 it.col0 = min(rows, it.row0 + kInlineGemvRows);
-                it.kb1 = 0;
+                const int64_t esz = P->in_dt == GMX_ST_F32 ? 4 : 2;
+                const int rps = gemv_rows_per_stage(P->cols * esz, P->ld_in0 * esz,
+                                                    reinterpret_cast<uintptr_t>(P->in0));
+                it.kb1 = rps ? (it.col0 - it.row0 + rps - 1) / rps : 0;   // ring stages (0: unstaged)
             } else {
                 it.row0 = u * kInlineEltwise;
                 it.col0 = min(rows, it.row0 + kInlineEltwise);
@@ -824,6 +836,49 @@ __device__ void gemv_rows(const DevProblem* Pg, int r0, int r1, int ew) {
     }
 }
 
+// Staged GEMV item (4 epilogue warps): rows arrive in ring stages (bulk copies issued by the
+// producer lane); warp ew reduces rows ew, ew + 4, ... of each stage against x (L1-resident),
+// then the 4 warps release the stage together.
+template <typename T>
+__device__ void gemv_staged(const DevProblem* Pg, const WorkItem& it, int ew, int etid, uint8_t* smem,
+                            uint64_t* full, uint64_t* empty, int& rstage, uint32_t& rphase, int kStages) {
+    constexpr int kVec = 16 / sizeof(T);
+    const int n = Pg->cols;
+    const int64_t row = (int64_t)n * sizeof(T);
+    const int rps = gemv_rows_per_stage(row, Pg->ld_in0 * (int64_t)sizeof(T), reinterpret_cast<uintptr_t>(Pg->in0));
+    const uint4* xv = reinterpret_cast<const uint4*>(Pg->in1);
+    void* out = Pg->out;
+    const float* bias = Pg->bias;
+    const int32_t act = Pg->act, out_dt = Pg->out_dt;
+    const int lane = lane_id();
+    const int nv = n / kVec;
+    for (int st = 0; st < it.kb1; ++st) {
+        mbar_wait(&full[rstage], rphase);
+        const uint32_t base = smem_u32(smem + rstage * kStageBytes);
+        const int ra = it.row0 + st * rps, rb = min(it.col0, ra + rps);
+        for (int r = ra + ew; r < rb; r += 4) {
+            const uint32_t rowa = base + (uint32_t)((r - ra) * row);
+            float acc = 0.0f;
+            int j = lane;
+            for (; j + 32 < nv; j += 64) {
+                const uint4 w0 = ld_shared_v4(rowa + 16u * j), w1 = ld_shared_v4(rowa + 16u * (j + 32));
+                const uint4 x0 = __ldg(xv + j), x1 = __ldg(xv + j + 32);
+                acc += dot_v4(w0, x0, T()) + dot_v4(w1, x1, T());
+            }
+            for (; j < nv; j += 32) acc += dot_v4(ld_shared_v4(rowa + 16u * j), __ldg(xv + j), T());
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) {
+                const float b = bias ? __ldg(bias + r) : 0.0f;
+                store_one(out, r, out_dt, apply_act(acc + b, act));
+            }
+        }
+        named_bar_sync(4, 128);   // every warp is done reading the stage
+        if (etid == 0) mbar_arrive(&empty[rstage]);
+        if (++rstage == kStages) { rstage = 0; rphase ^= 1; }
+    }
+}
+
 template <typename T>
 __device__ void eltwise_range(const DevProblem* Pg, int e0, int e1, int tid, int nthreads) {
     const T* __restrict__ x = reinterpret_cast<const T*>(Pg->in0);
@@ -1126,6 +1181,8 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
 
     // CTA owns GEMM tiles (host-computed; resident / inline steps: any list may bring some)
     const bool has_gemm = args.resident || args.inline_n > 0 || (args.cta_flags[blockIdx.x] & 1) != 0;
+    // CTA streams GEMV rows (planner flag 2): its producer lane prefetches them into L2 up front
+    const bool has_gemv = args.resident || args.inline_n > 0 || (args.cta_flags[blockIdx.x] & 2) != 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -1350,11 +1407,59 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         }
     } else if (warp == 0) {
         // ---------------- TMA producer ----------------
-        if (lane == 0 && has_gemm) {
+        if (lane == 0 && (has_gemm || has_gemv)) {
             int stage = 0;
             uint32_t phase = 0;
+            // GEMV rows are streamed by the 4 epilogue warps with 16-byte loads (~32 KB in flight
+            // per SM: latency-bound at ~2.5 TB/s); one bulk L2 prefetch per row range, issued for
+            // every GEMV item of the list before any other work, keeps HBM streaming at full rate
+            // and turns the warps' loads into L2 hits.
+            auto prefetch_gemv = [&](const StepView& v) {
+                auto one = [&](const WorkItem& it) {
+                    if (item_kind(it.type) != kItemGemv || it.kb1 > 0) return;   // staged rows stream by TMA
+                    const DevProblem* P = v.probs + it.problem;
+                    const char* w = reinterpret_cast<const char*>(P->in0);
+                    const int64_t esz = P->in_dt == GMX_ST_F32 ? 4 : 2;
+                    const int64_t row = (int64_t)P->cols * esz, pitch = P->ld_in0 * esz;
+                    if (row == pitch) {   // contiguous rows: one range
+                        prefetch_l2_range(w + it.row0 * pitch, (it.col0 - it.row0) * pitch);
+                    } else {
+                        for (int r = it.row0; r < it.col0; ++r) prefetch_l2_range(w + r * pitch, row);
+                    }
+                };
+                if (v.inl_n == 0) {
+                    for (int i = v.beg; i < v.end; ++i) one(v.items[i - v.ibase]);
+                } else {
+                    ItemCursor c = item_begin(v);
+                    WorkItem it;
+                    while (next_item(v, c, it)) one(it);
+                }
+            };
             auto issue_list = [&](const StepView& v) {
+                prefetch_gemv(v);
                 for_each_item(v, [&](const WorkItem& it, int i) {
+                    if (item_kind(it.type) == kItemGemv && it.kb1 > 0) {
+                        // staged GEMV: whole rows by bulk copy into the ring, consumed by the epilogue warps
+                        const DevProblem* P = v.probs + it.problem;
+                        const char* w = reinterpret_cast<const char*>(P->in0);
+                        const int64_t esz = P->in_dt == GMX_ST_F32 ? 4 : 2;
+                        const int64_t row = (int64_t)P->cols * esz, pitch = P->ld_in0 * esz;
+                        const int rps = gemv_rows_per_stage(row, pitch, reinterpret_cast<uintptr_t>(w));
+                        for (int st = 0; st < it.kb1; ++st) {
+                            mbar_wait(&empty[stage], phase ^ 1);
+                            const int ra = it.row0 + st * rps, rb = min(it.col0, ra + rps);
+                            uint8_t* tile = smem + stage * kStageBytes;
+                            mbar_expect_tx(&full[stage], (uint32_t)((rb - ra) * row));
+                            if (row == pitch) {
+                                bulk_load(tile, w + ra * pitch, (uint32_t)((rb - ra) * row), &full[stage]);
+                            } else {
+                                for (int r = ra; r < rb; ++r)
+                                    bulk_load(tile + (r - ra) * row, w + r * pitch, (uint32_t)row, &full[stage]);
+                            }
+                            if (++stage == kStages) { stage = 0; phase ^= 1; }
+                        }
+                        return;
+                    }
                     if (item_kind(it.type) != kItemGemm) return;
                     const DevProblem* P = v.probs + it.problem;
                     const uint32_t bytes = kStageA + (uint32_t)it.bn * (kBlockK * 2);
@@ -1412,6 +1517,11 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 }
                 const StepView v = unit_view(u);
                 for_each_item(v, [&](const WorkItem& it, int i) {
+                    if (item_kind(it.type) == kItemGemv) {   // staged GEMV: its ring stages are the epilogue's
+                        for (int st = 0; st < it.kb1; ++st)
+                            if (++stage == kStages) { stage = 0; phase ^= 1; }
+                        return;
+                    }
                     if (item_kind(it.type) != kItemGemm) return;
                     const bool tf32 = it.type & kItemTf32;
                     const uint32_t idesc = tf32 ? idesc_tf32_m128((uint32_t)it.bn) : idesc_bf16_m128((uint32_t)it.bn);
@@ -1456,6 +1566,8 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         int pend = -1, pend_age = 0;             // split item whose completion is deferred
         WorkItem pend_it{};
         StepView v{};
+        int rstage = 0;                          // TMA ring position (staged GEMV items read from it)
+        uint32_t rphase = 0;
         auto complete_pending_body = [&]() {
             const WorkItem pt = pend_it;
             int32_t* counter = v.counters + pt.tile_slot;
@@ -1548,6 +1660,8 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 const DevProblem* Pg = v.probs + it.problem;
                 if (args.trace && etid == 0 && item_kind(it.type) != kItemGemm) args.trace[8 * i + 0] = global_timer_ns();
                 if (item_kind(it.type) == kItemGemm) {
+                    for (int kb = it.kb0; kb < it.kb1; ++kb)   // the MMA's stages: keep the ring position
+                        if (++rstage == kStages) { rstage = 0; rphase ^= 1; }
                     const EpiParams E = load_epi(Pg);
                     timed(ic, kIETfull, true, [&] { mbar_wait(&tfull[acc], acc_phase); });
                     tc_fence_after();
@@ -1584,6 +1698,11 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                         pend_age = 0;
                     }
                     if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
+                } else if (it.type == kItemGemv && it.kb1 > 0) {
+                    if (Pg->in_dt == GMX_ST_F32)
+                        gemv_staged<float>(Pg, it, ew, etid, smem, full, empty, rstage, rphase, kStages);
+                    else
+                        gemv_staged<__nv_bfloat16>(Pg, it, ew, etid, smem, full, empty, rstage, rphase, kStages);
                 } else if (it.type == kItemGemv) {
                     if (Pg->in_dt == GMX_ST_F32)
                         gemv_rows<float>(Pg, it.row0, it.col0, ew);
@@ -1748,6 +1867,10 @@ struct gmx_exec {
     int32_t counters_cap = 0;
     int64_t max_split = 32;
     int64_t split_pct = 400;     // split a tile into pieces of about this % of the per-CTA share
+    // GEMV rows through the TMA ring (bulk copies) when stageable. Off by default: faster for a
+    // held batch of C1 steps (11.7 vs 13.3 us/step) but slower lone and live-fed (C1 through the
+    // resident runtime 17.7 vs 11.6 us per round; tools/c1_kernel.py, tools/ab_c1.sh)
+    bool gemv_staged = false;
     int ctas_per_sm = 1;         // 1, or 2 CTAs of the coalesced kernel per SM (the latter runs as 2 waves)
     bool cache_plans = true;
     bool attr_set = false;
@@ -1921,6 +2044,10 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
                 it.type = kItemGemv;
                 it.row0 = r0;
                 it.col0 = std::min(P.rows, r0 + rows_per);
+                const int64_t esz = P.in_dt == GMX_ST_F32 ? 4 : 2;
+                const int rps = ex->gemv_staged ? gemv_rows_per_stage((int64_t)P.cols * esz, P.ld_in0 * esz,
+                                                                      reinterpret_cast<uintptr_t>(P.in0)) : 0;
+                it.kb1 = rps ? (it.col0 - it.row0 + rps - 1) / rps : 0;   // ring stages (0: unstaged)
                 cands.push_back({it, row_bytes * (it.col0 - it.row0) / 1024.0 * kNsPerKB + kCudaCoreFixedNs});
                 ++st.n_gemv_items;
             }
@@ -1964,6 +2091,7 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
         for (int32_t idx : per_cta[c]) {
             plan.items.push_back(cands[idx].it);
             if (item_kind(cands[idx].it.type) == kItemGemm) flags[c] |= 1;
+            if (item_kind(cands[idx].it.type) == kItemGemv) flags[c] |= 2;
         }
         plan.cta_off.push_back((int32_t)plan.items.size());
     }
@@ -2721,6 +2849,8 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
     } else if (n == "ctas_per_sm") {
         if (value != 1 && value != 2) return fail(GMX_EINVAL, "ctas_per_sm must be 1 or 2");
         ex->ctas_per_sm = (int)value;
+    } else if (n == "gemv_staged") {
+        ex->gemv_staged = value != 0;   // applies to plans built afterwards (clear_plans)
     } else if (n == "split_pct") {
         if (value < 10 || value > 2000) return fail(GMX_EINVAL, "split_pct must be in [10, 2000]");
         ex->split_pct = value;

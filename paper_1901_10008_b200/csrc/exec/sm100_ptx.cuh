@@ -117,6 +117,17 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* gsrc, uint32_t 
                  "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// Bulk prefetch of [p, p + bytes) into L2 (no smem, no completion tracking); 16-byte granules,
+// chunks of at most 64 KB per instruction.
+__device__ __forceinline__ void prefetch_l2_range(const void* p, int64_t bytes) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + (uintptr_t)bytes + 15) & ~uintptr_t(15);
+    for (uintptr_t a = a0; a < a1; a += 65536) {
+        const uint32_t n = (uint32_t)((a1 - a) < 65536 ? (a1 - a) : 65536);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+    }
+}
+
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }

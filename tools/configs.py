@@ -140,7 +140,11 @@ def main():
     ap.add_argument("--rounds", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--resident", action="store_true", help="run the steps through the resident executor")
+    ap.add_argument("--exec-lib", default=None, help="A/B runs: another build of libgmx_exec.so")
     args = ap.parse_args()
+    if args.exec_lib:
+        from paper_1901_10008_b200 import executor
+        executor.exec_lib(args.exec_lib)
     for cfg in args.configs.split(","):
         run = ConfigRun(cfg)
         res = run.run(args.rounds, args.warmup, args.resident)
