@@ -101,6 +101,17 @@ int gmx_exec_launch(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream)
  * writes, so the step also skips griddepcontrol.wait and its CTAs start on SMs as the
  * previous step's CTAs retire (the executor still waits when split-K state could alias). */
 #define GMX_LAUNCH_INDEPENDENT 1
+/* GMX_LAUNCH_FENCE: members read outputs of earlier steps whose completion the caller already
+ * OBSERVED (wall-clock serving), so no ordering wait is needed, only the generic -> async proxy
+ * fence before the step's TMA loads (resident mode). */
+#define GMX_LAUNCH_FENCE 2
+/* Hazards are tracked by the executor over the slots: a per-step launch that writes a slot
+ * read or written, or reads a slot written, by any launch since the last fully ordered one is
+ * itself launched fully ordered (no PDL: it starts after ALL earlier work on the stream); a
+ * resident step waits for the last steps that wrote (RAW/WAW) or read (WAR) its slots. Slots
+ * may therefore be reused by later requests on one stream; across the streams of a
+ * multi-stream caller, reuse needs the earlier user's completion (the wall-clock runtime only
+ * launches a member after observing its producers). */
 int gmx_exec_launch_ex(gmx_exec* ex, const int32_t* slots, int32_t n, void* stream, int32_t flags);
 /* As launch_ex, plus the slots whose OUTPUTS this step's members read (their producers): in
  * resident mode the step then waits only for the steps that last wrote those slots (and for

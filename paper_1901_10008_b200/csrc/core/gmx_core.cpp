@@ -960,8 +960,19 @@ static void compact(S* s) {
     std::vector<RequestRec> nr;
     std::vector<int64_t> nd;
     nk.reserve(s->kernels.size() / 2 + 16);
+    // evicted requests are dropped too, unless one of their kernels is still in a live
+    // (multi-stream) dispatch: nothing else can reference them again
+    std::vector<char> in_flight(s->kernels.size(), 0);
+    for (const DispatchRec& d : s->pool)
+        if (d.live)
+            for (int32_t slot : d.kernels) in_flight[slot] = 1;
     for (const RequestRec& r0 : s->requests) {
         if (r0.finished) continue;
+        if (r0.evicted) {
+            bool held = false;
+            for (int32_t slot = r0.first; slot < r0.first + r0.count; ++slot) held |= in_flight[slot] != 0;
+            if (!held) continue;
+        }
         RequestRec r = r0;
         r.first = (int32_t)nk.size();
         const int32_t rslot = (int32_t)nr.size();

@@ -979,10 +979,10 @@ __device__ __forceinline__ void step_order(const KernelArgs& a, int64_t k) {
         // bounded skew, plus the listed steps: producers of this step's inputs and the latest
         // earlier users of its plan or slots (those waited for any earlier sharer, transitively)
         wait_step_done(a.dq, k - a.window, gridDim.x);
-        const int nw = __ldcg(&d->nwait);
+        const int nw = __ldcg(&d->nwait);   // -1: nothing to wait for, fence only
         for (int q = 0; q < nw; ++q)
             wait_step_done(a.dq, (int64_t)__ldcg((const long long*)&d->wait_steps[q]), gridDim.x);
-        if (nw > 0) fence_proxy_async_global();   // later TMA loads may read what they wrote
+        if (nw != 0) fence_proxy_async_global();   // later TMA loads may read what they wrote
     }
 }
 
@@ -1885,6 +1885,9 @@ struct gmx_exec {
     int64_t inline_launches = 0;
     int32_t dbg = 0;
     const gmx::Plan* recent[3] = {nullptr, nullptr, nullptr};   // plans of the last launches
+    // per-step launches: slots written / read by launches since the last fully ordered launch
+    std::vector<uint8_t> hz_wr, hz_rd;
+    std::vector<int32_t> hz_touched;
     uint64_t* trace = nullptr;
     int64_t trace_cap = 0;
     int64_t trace_items = 0;
@@ -1904,6 +1907,7 @@ struct gmx_exec {
         int grid = 0;
         int64_t epoch = 0;                     // residency counter (validates Plan::res_seq)
         std::vector<int64_t> last_write;       // per slot: last step (seq) that wrote its output
+        std::vector<int64_t> last_read;        // per slot: last step (seq) that read its output (WAR)
         std::vector<void*> graveyard;          // device tables retired during residency
         std::vector<uint8_t> zeros;            // host zeros for copy-engine clears while resident
         int window = 16;                       // max steps a CTA may run ahead (option "resident_window")
@@ -2280,12 +2284,17 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
         waits[nw++] = j;
     };
     if (r.last_write.size() < ex->probs.size()) r.last_write.resize(ex->probs.size(), -1);
+    if (r.last_read.size() < ex->probs.size()) r.last_read.resize(ex->probs.size(), -1);
     for (int32_t i = 0; i < ndep; ++i) {
         const int32_t sl = dep_slots[i];
         if (sl >= 0 && sl < (int32_t)r.last_write.size()) need(r.last_write[sl]);
     }
-    // outputs: the last step that wrote each member slot; split-K state: the last step of this plan
-    for (int32_t sl : key) need(r.last_write[sl]);
+    // outputs: the last step that wrote (WAW) or read (WAR) each member slot; split-K state:
+    // the last step of this plan
+    for (int32_t sl : key) {
+        need(r.last_write[sl]);
+        need(r.last_read[sl]);
+    }
     if (plan && plan->res_epoch == r.epoch) need(plan->res_seq);
     StepDesc d{};
     d.probs = ex->d_probs;
@@ -2301,11 +2310,14 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
         for (size_t i = 0; i < key.size(); ++i) d.inline_slots[i] = key[i];
     }
     d.wait_all = wait_all ? 1 : 0;
-    d.nwait = wait_all ? 0 : nw;
+    // nwait -1: no wait, only the proxy fence (inputs of already-observed producers)
+    d.nwait = wait_all ? 0 : (nw == 0 && ((flags & GMX_LAUNCH_FENCE) || ndep > 0) ? -1 : nw);
     for (int q = 0; q < nw; ++q) d.wait_steps[q] = waits[q];
     if (d.grid > r.grid) return fail(GMX_ESTATE, "plan grid exceeds the resident grid");
     if ((rc = publish_step(ex, d))) return rc;
     for (int32_t sl : key) r.last_write[sl] = seq;
+    for (int32_t i = 0; i < ndep; ++i)
+        if (dep_slots[i] >= 0 && dep_slots[i] < (int32_t)r.last_read.size()) r.last_read[dep_slots[i]] = seq;
     if (plan) {
         plan->res_seq = seq;
         plan->res_epoch = r.epoch;
@@ -2316,6 +2328,38 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
     }
     if (seq_out) *seq_out = seq;
     return GMX_OK;
+}
+
+// Per-step launches: true if this launch writes a slot read or written, or reads a slot written,
+// by a launch since the last fully ordered one (PDL launches of independent steps may overlap).
+// A hazard resets the window to this launch (it will be launched fully ordered).
+static bool per_step_hazard(gmx_exec* ex, const std::vector<int32_t>& key, const int32_t* dep_slots, int32_t ndep) {
+    const size_t ns = ex->probs.size();
+    if (ex->hz_wr.size() < ns) {
+        ex->hz_wr.resize(ns, 0);
+        ex->hz_rd.resize(ns, 0);
+    }
+    bool hazard = false;
+    for (int32_t sl : key) hazard |= ex->hz_wr[sl] || ex->hz_rd[sl];
+    for (int32_t i = 0; i < ndep; ++i) {
+        const int32_t sl = dep_slots[i];
+        if (sl >= 0 && (size_t)sl < ns) hazard |= ex->hz_wr[sl] != 0;
+    }
+    if (hazard) {
+        for (int32_t sl : ex->hz_touched) ex->hz_wr[sl] = ex->hz_rd[sl] = 0;
+        ex->hz_touched.clear();
+    }
+    for (int32_t sl : key) {
+        if (!ex->hz_wr[sl] && !ex->hz_rd[sl]) ex->hz_touched.push_back(sl);
+        ex->hz_wr[sl] = 1;
+    }
+    for (int32_t i = 0; i < ndep; ++i) {
+        const int32_t sl = dep_slots[i];
+        if (sl < 0 || (size_t)sl >= ns) continue;
+        if (!ex->hz_wr[sl] && !ex->hz_rd[sl]) ex->hz_touched.push_back(sl);
+        ex->hz_rd[sl] = 1;
+    }
+    return hazard;
 }
 
 }  // namespace gmx
@@ -2359,6 +2403,7 @@ int gmx_exec_resident_begin_ex(gmx_exec* ex, void* stream_ptr, int32_t hold) {
     r.stream = stream;
     ++r.epoch;
     r.last_write.assign(ex->probs.size(), -1);
+    r.last_read.assign(ex->probs.size(), -1);
     KernelArgs args{};
     args.dbg = ex->dbg;
     args.independent = 1;
@@ -2706,6 +2751,7 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
                 }
                 if ((total + grid - 1) / grid <= kInlineMaxItems) {
                     if ((rc = set_kernel_attrs(ex))) return rc;
+                    const bool hazard = per_step_hazard(ex, key, dep_slots, ndep);
                     KernelArgs args{};
                     args.probs = ex->d_probs;
                     args.dbg = ex->dbg;
@@ -2720,7 +2766,7 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
                     cfg.stream = stream;
                     cudaLaunchAttribute attr[1];
                     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-                    attr[0].val.programmaticStreamSerializationAllowed = ex->pdl ? 1 : 0;
+                    attr[0].val.programmaticStreamSerializationAllowed = ex->pdl && !hazard ? 1 : 0;
                     cfg.attrs = attr;
                     cfg.numAttrs = 1;
                     GMX_CUDA(cudaLaunchKernelEx(&cfg, coalesced_step_kernel<1>, args));
@@ -2778,6 +2824,8 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
     // use by a still-running recent launch
     bool independent = (flags & GMX_LAUNCH_INDEPENDENT) != 0 && !ex->tracing;
     for (const Plan* r : ex->recent) independent &= (r != plan);
+    // a slot hazard with any launch since the last fully ordered one: launch fully ordered
+    const bool hazard = per_step_hazard(ex, key, dep_slots, ndep);
     KernelArgs args{ex->d_probs, plan->d_items, plan->d_off, plan->d_off + plan->stats.grid + 1, plan->d_ws,
                     plan->d_counters, ex->tracing ? ex->trace : nullptr, ex->dbg, independent ? 1 : 0,
                     ex->early_trigger ? 1 : 0};
@@ -2788,7 +2836,7 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = ex->pdl ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = ex->pdl && !hazard ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (ex->ctas_per_sm == 2)

@@ -109,9 +109,19 @@ static void log_rec(gmx_runtime* rt, int32_t kind, int64_t t, int64_t a, int32_t
     rt->log.push_back(gmx_replay_rec{kind, n, t, a, off});
 }
 
-static void release_request(gmx_runtime* rt, int64_t rid) {
+// purge: an evicted request's undispatched kernels never reach a launch, so their slot and
+// producer-slot entries are dropped here (a finished request's were consumed at dispatch)
+static void release_request(gmx_runtime* rt, int64_t rid, bool purge = false) {
     const int32_t pi = rt->req_index.find(rid);
     if (pi < 0) return;
+    if (purge) {
+        const Pending& p = rt->pool[pi];
+        for (int32_t i = 0; i < p.n; ++i) {
+            const int64_t kid = rt->k_arena[p.k_off + i].kernel_id;
+            rt->slot_of.erase(kid);
+            rt->depslots_of.erase(kid);
+        }
+    }
     rt->req_index.erase(rid);
     rt->pool_free.push_back(pi);
     if (--rt->live_requests == 0) {   // nothing outstanding: recycle the arenas
@@ -279,7 +289,7 @@ static int evict_stragglers(gmx_runtime* rt, int64_t now) {
         }
         for (int32_t i = 0; i < ev.n_evicted; ++i) {
             ++rt->st.evicted_requests;
-            release_request(rt, ev.evicted_request_ids[i]);
+            release_request(rt, ev.evicted_request_ids[i], true);
         }
         log_rec(rt, 6, now, st);
     }
@@ -317,7 +327,7 @@ static int on_arrival(gmx_runtime* rt, int64_t rid) {
     if (rc) return fail(rc, std::string("add_request: ") + gmx_last_error());
     if (!accepted) {   // stream already evicted (engine.py:338-342, "stream-evicted")
         ++rt->st.evicted_requests;
-        release_request(rt, rid);
+        release_request(rt, rid, true);
     }
     return GMX_OK;
 }
@@ -384,13 +394,16 @@ static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool real
         // wall clock: a member became ready only after its producers' completion was OBSERVED, so
         // the launch carries no ordering against earlier steps (it must not wait for unrelated
         // work queued before it)
-        if (realtime) {
+        int32_t lflags = 0;
+        if (realtime) {   // ... but its TMA loads still need the proxy fence (resident mode)
+            if (!independent) lflags |= GMX_LAUNCH_FENCE;
             rt->launch_deps.clear();
             independent = true;
         }
+        if (independent) lflags |= GMX_LAUNCH_INDEPENDENT;
         rc = rt->ex ? gmx_exec_launch_deps(rt->ex, rt->launch_slots.data(), (int32_t)rt->launch_slots.size(),
                                            rt->launch_deps.data(), (int32_t)rt->launch_deps.size(), stream,
-                                           independent ? GMX_LAUNCH_INDEPENDENT : 0, &seq)
+                                           lflags, &seq)
                     : GMX_OK;   // decisions-only runtime (no executor): nothing to launch
         rt->last_seq = seq;
         if (rt->prof_on) rt->prof_ns[3] += steady_ns() - t_l;
