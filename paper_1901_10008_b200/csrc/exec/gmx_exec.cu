@@ -1038,6 +1038,8 @@ struct Reporter {
                 any = true;
             }
             asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(&a.hdone[j % kQueue]), "l"(j + 1) : "memory");
+            if (a.rtrace && j < a.rtrace_steps)   // diagnostics: when step j was reported to the host
+                a.rtrace[(int64_t)a.rtrace_steps * G * 8 + a.rtrace_steps + j] = global_timer_ns();
             reported |= 1ull << i;
         }
         if (any) a.dq->t_last = global_timer_ns();
@@ -1131,6 +1133,9 @@ __device__ void dispatch_steps(const KernelArgs& a) {
         k += n;
         asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(&a.dq->published), "l"(k) : "memory");
         a.dq->t_relay = global_timer_ns();
+        if (a.rtrace)   // diagnostics: when steps k-n..k-1 were relayed (published + one PCIe read)
+            for (int64_t j = k - n; j < k && j < a.rtrace_steps; ++j)
+                a.rtrace[(int64_t)a.rtrace_steps * gridDim.x * 8 + j] = a.dq->t_relay;
         if (stop) break;
     }
     a.dq->t_stop = global_timer_ns();
@@ -1407,7 +1412,9 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         }
     } else if (warp == 0) {
         // ---------------- TMA producer ----------------
-        if (lane == 0 && (has_gemm || has_gemv)) {
+        // Whole warp, uniform control flow on broadcast item fields, one elected lane issues
+        // (tensor-map pointers and coordinates in uniform registers: see warp_uni).
+        if (has_gemm || has_gemv) {
             int stage = 0;
             uint32_t phase = 0;
             // GEMV rows are streamed by the 4 epilogue warps with 16-byte loads (~32 KB in flight
@@ -1427,6 +1434,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                         for (int r = it.row0; r < it.col0; ++r) prefetch_l2_range(w + r * pitch, row);
                     }
                 };
+                if (lane != 0) return;
                 if (v.inl_n == 0) {
                     for (int i = v.beg; i < v.end; ++i) one(v.items[i - v.ibase]);
                 } else {
@@ -1437,119 +1445,155 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             };
             auto issue_list = [&](const StepView& v) {
                 prefetch_gemv(v);
+                __syncwarp();
                 for_each_item(v, [&](const WorkItem& it, int i) {
-                    if (item_kind(it.type) == kItemGemv && it.kb1 > 0) {
+                    const int32_t type = warp_uni((int32_t)it.type);
+                    const int32_t kb0 = warp_uni(it.kb0), kb1 = warp_uni(it.kb1);
+                    const DevProblem* P = reinterpret_cast<const DevProblem*>(
+                        warp_uni(reinterpret_cast<uint64_t>(v.probs + it.problem)));
+                    if (item_kind(type) == kItemGemv && kb1 > 0) {
                         // staged GEMV: whole rows by bulk copy into the ring, consumed by the epilogue warps
-                        const DevProblem* P = v.probs + it.problem;
+                        const int32_t row0 = warp_uni(it.row0), row1 = warp_uni(it.col0);
                         const char* w = reinterpret_cast<const char*>(P->in0);
                         const int64_t esz = P->in_dt == GMX_ST_F32 ? 4 : 2;
                         const int64_t row = (int64_t)P->cols * esz, pitch = P->ld_in0 * esz;
                         const int rps = gemv_rows_per_stage(row, pitch, reinterpret_cast<uintptr_t>(w));
-                        for (int st = 0; st < it.kb1; ++st) {
+                        for (int st = 0; st < kb1; ++st) {
                             mbar_wait(&empty[stage], phase ^ 1);
-                            const int ra = it.row0 + st * rps, rb = min(it.col0, ra + rps);
-                            uint8_t* tile = smem + stage * kStageBytes;
-                            mbar_expect_tx(&full[stage], (uint32_t)((rb - ra) * row));
-                            if (row == pitch) {
-                                bulk_load(tile, w + ra * pitch, (uint32_t)((rb - ra) * row), &full[stage]);
-                            } else {
-                                for (int r = ra; r < rb; ++r)
-                                    bulk_load(tile + (r - ra) * row, w + r * pitch, (uint32_t)row, &full[stage]);
+                            if (lane == 0) {
+                                const int ra = row0 + st * rps, rb = min(row1, ra + rps);
+                                uint8_t* tile = smem + stage * kStageBytes;
+                                mbar_expect_tx(&full[stage], (uint32_t)((rb - ra) * row));
+                                if (row == pitch) {
+                                    bulk_load(tile, w + ra * pitch, (uint32_t)((rb - ra) * row), &full[stage]);
+                                } else {
+                                    for (int r = ra; r < rb; ++r)
+                                        bulk_load(tile + (r - ra) * row, w + r * pitch, (uint32_t)row, &full[stage]);
+                                }
                             }
+                            __syncwarp();
                             if (++stage == kStages) { stage = 0; phase ^= 1; }
                         }
                         return;
                     }
-                    if (item_kind(it.type) != kItemGemm) return;
-                    const DevProblem* P = v.probs + it.problem;
-                    const uint32_t bytes = kStageA + (uint32_t)it.bn * (kBlockK * 2);
-                    const int kel = kblock_elems(it.type & kItemTf32);
-                    if (args.trace) args.trace[8 * i + 0] = global_timer_ns();
-                    tma_prefetch_desc(&P->tm_rows);   // descriptor fetch overlaps the slot wait
-                    tma_prefetch_desc(&P->tm_cols);
-                    for (int kb = it.kb0; kb < it.kb1; ++kb) {
+                    if (item_kind(type) != kItemGemm) return;
+                    const int32_t row0 = warp_uni(it.row0), col0 = warp_uni(it.col0);
+                    const uint32_t bytes = kStageA + warp_uni((uint32_t)it.bn) * (kBlockK * 2);
+                    const int kel = kblock_elems(type & kItemTf32);
+                    if (args.trace && lane == 0) args.trace[8 * i + 0] = global_timer_ns();
+                    if (elect_one()) {
+                        tma_prefetch_desc(&P->tm_rows);   // descriptor fetch overlaps the slot wait
+                        tma_prefetch_desc(&P->tm_cols);
+                    }
+                    __syncwarp();
+                    for (int kb = kb0; kb < kb1; ++kb) {
                         timed(ic, kIPEmpty, true, [&] { mbar_wait(&empty[stage], phase ^ 1); });
                         GMX_INSTR_INC(kIPStages);
                         uint8_t* tile = smem + stage * kStageBytes;
-                        mbar_expect_tx(&full[stage], bytes);
-                        tma_load_2d(tile, &P->tm_rows, &full[stage], kb * kel, it.row0);
-                        tma_load_2d(tile + kStageA, &P->tm_cols, &full[stage], kb * kel, it.col0);
+                        if (elect_one()) {
+                            mbar_expect_tx(&full[stage], bytes);
+                            tma_load_2d(tile, &P->tm_rows, &full[stage], kb * kel, row0);
+                            tma_load_2d(tile + kStageA, &P->tm_cols, &full[stage], kb * kel, col0);
+                        }
+                        __syncwarp();
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
-                }, [&] { release_unit(); });
+                }, [&] {
+                    __syncwarp();
+                    if (lane == 0) release_unit();
+                });
             };
             for (bool first = true;; first = false) {
                 const Unit* u;
                 timed(ic, kIPUnit, !first, [&] { u = next_unit(first); });
-                const int32_t uidx = u->idx;
+                const int32_t uidx = warp_uni(u->idx);
                 const int64_t uk = u->k;
-                if (uidx >= 0)
+                if (uidx >= 0) {
                     issue_list(unit_view(u));   // releases the unit after reading its last item
-                else
-                    release_unit();
+                } else {
+                    __syncwarp();
+                    if (lane == 0) release_unit();
+                }
                 advance_unit();
                 if (uidx == kUnitStop) {
-                    instr_dump(args, ic, kIPUnit, kIPEmpty + 1);
-                    instr_dump(args, ic, kIPStages, kIPStages + 1);
+                    if (lane == 0) {
+                        instr_dump(args, ic, kIPUnit, kIPEmpty + 1);
+                        instr_dump(args, ic, kIPStages, kIPStages + 1);
+                    }
                     break;
                 }
-                if (uidx >= 0 && args.rtrace && uk < args.rtrace_steps)
+                if (uidx >= 0 && args.rtrace && uk < args.rtrace_steps && lane == 0)
                     args.rtrace[(uk * gridDim.x + blockIdx.x) * 8 + 1] = global_timer_ns();
             }
         }
     } else if (warp == 1) {
         // ---------------- UMMA issuer ----------------
-        if (lane == 0 && has_gemm) {
+        // The whole warp runs the loop (uniform control flow on broadcast values) and one
+        // elected lane issues: the descriptors then live in uniform registers and consecutive
+        // UTCHMMAs issue back to back.
+        if (has_gemm) {
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
+            const uint32_t tbase = warp_uni(tmem_base);
             for (bool first = true;; first = false) {
                 const Unit* u;
                 timed(ic, kIMUnit, !first, [&] { u = next_unit(first); });
-                const int32_t uidx = u->idx;
+                const int32_t uidx = warp_uni(u->idx);
                 if (uidx < 0) {
-                    release_unit();
+                    __syncwarp();
+                    if (lane == 0) release_unit();
                     advance_unit();
                     if (uidx == kUnitStop) {
-                        instr_dump(args, ic, kIMUnit, kIMFull + 1);
+                        if (lane == 0) instr_dump(args, ic, kIMUnit, kIMFull + 1);
                         break;
                     }
                     continue;
                 }
                 const StepView v = unit_view(u);
                 for_each_item(v, [&](const WorkItem& it, int i) {
-                    if (item_kind(it.type) == kItemGemv) {   // staged GEMV: its ring stages are the epilogue's
-                        for (int st = 0; st < it.kb1; ++st)
+                    const int32_t type = warp_uni((int32_t)it.type);
+                    const int32_t kb0 = warp_uni(it.kb0), kb1 = warp_uni(it.kb1);
+                    if (item_kind(type) == kItemGemv) {   // staged GEMV: its ring stages are the epilogue's
+                        for (int st = 0; st < kb1; ++st)
                             if (++stage == kStages) { stage = 0; phase ^= 1; }
                         return;
                     }
-                    if (item_kind(it.type) != kItemGemm) return;
-                    const bool tf32 = it.type & kItemTf32;
-                    const uint32_t idesc = tf32 ? idesc_tf32_m128((uint32_t)it.bn) : idesc_bf16_m128((uint32_t)it.bn);
+                    if (item_kind(type) != kItemGemm) return;
+                    const bool tf32 = type & kItemTf32;
+                    const uint32_t bn = warp_uni((uint32_t)it.bn);
+                    const uint32_t idesc = tf32 ? idesc_tf32_m128(bn) : idesc_bf16_m128(bn);
                     timed(ic, kIMTempty, true, [&] { mbar_wait(&tempty[acc], acc_phase ^ 1); });
                     tc_fence_after();
-                    const uint32_t d_tmem = tmem_base + (uint32_t)acc * kMaxBN;
-                    for (int kb = it.kb0; kb < it.kb1; ++kb) {
+                    const uint32_t d_tmem = tbase + (uint32_t)acc * kMaxBN;
+                    for (int kb = kb0; kb < kb1; ++kb) {
                         timed(ic, kIMFull, true, [&] { mbar_wait(&full[stage], phase); });
                         tc_fence_after();
                         const uint8_t* tile = smem + stage * kStageBytes;
                         const uint64_t a_desc = smem_desc_sw128(tile);
                         const uint64_t b_desc = smem_desc_sw128(tile + kStageA);
+                        if (elect_one()) {
 #pragma unroll
-                        for (int kk = 0; kk < kBlockK / 16; ++kk) {   // UMMA K steps of 32 B (16 bf16 / 8 tf32)
-                            if (args.dbg & 4) continue;
-                            const uint32_t accum = (kb > it.kb0 || kk > 0) ? 1u : 0u;
-                            if (tf32)
-                                umma_tf32(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc, accum);
-                            else
-                                umma_bf16(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc, accum);
+                            for (int kk = 0; kk < kBlockK / 16; ++kk) {   // UMMA K steps of 32 B (16 bf16 / 8 tf32)
+                                if (args.dbg & 4) continue;
+                                const uint32_t accum = (kb > kb0 || kk > 0) ? 1u : 0u;
+                                if (tf32)
+                                    umma_tf32(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc, accum);
+                                else
+                                    umma_bf16(d_tmem, a_desc + 2 * kk, b_desc + 2 * kk, idesc, accum);
+                            }
+                            umma_commit(&empty[stage]);
                         }
-                        umma_commit(&empty[stage]);
+                        __syncwarp();
                         if (++stage == kStages) { stage = 0; phase ^= 1; }
                     }
-                    umma_commit(&tfull[acc]);
-                    if (args.trace) args.trace[8 * i + 1] = global_timer_ns();
+                    if (elect_one()) umma_commit(&tfull[acc]);
+                    __syncwarp();
+                    if (args.trace && lane == 0) args.trace[8 * i + 1] = global_timer_ns();
                     if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
-                }, [&] { release_unit(); });
+                }, [&] {
+                    __syncwarp();
+                    if (lane == 0) release_unit();
+                });
                 advance_unit();
             }
         }
@@ -2415,8 +2459,10 @@ int gmx_exec_resident_begin_ex(gmx_exec* ex, void* stream_ptr, int32_t hold) {
     args.hdone = r.hdone_d;
     args.window = r.window;
     if (r.rtrace_steps > 0) {
-        if (!r.rtrace) GMX_CUDA(cudaMalloc(&r.rtrace, (size_t)r.rtrace_steps * r.grid * 8 * sizeof(uint64_t)));
-        GMX_CUDA(cudaMemsetAsync(r.rtrace, 0, (size_t)r.rtrace_steps * r.grid * 8 * sizeof(uint64_t), stream));
+        // (step, CTA) stamps + one row of relay stamps + one row of host-report stamps
+        const size_t nb = ((size_t)r.rtrace_steps * r.grid * 8 + 2 * (size_t)r.rtrace_steps) * sizeof(uint64_t);
+        if (!r.rtrace) GMX_CUDA(cudaMalloc(&r.rtrace, nb));
+        GMX_CUDA(cudaMemsetAsync(r.rtrace, 0, nb, stream));
         args.rtrace = r.rtrace;
         args.rtrace_steps = r.rtrace_steps;
     }
@@ -2459,7 +2505,7 @@ int gmx_exec_resident_read_rtrace(gmx_exec* ex, uint64_t* out, int64_t capacity,
     if (!ex || !grid) return fail(GMX_EINVAL, "null argument");
     auto& r = ex->res;
     *grid = r.grid;
-    const int64_t n = (int64_t)r.rtrace_steps * r.grid * 8;
+    const int64_t n = (int64_t)r.rtrace_steps * r.grid * 8 + 2 * (int64_t)r.rtrace_steps;
     if (!r.rtrace || capacity < n) return fail(GMX_EINVAL, "no rtrace or capacity too small");
     GMX_CUDA(cudaDeviceSynchronize());
     GMX_CUDA(cudaMemcpy(out, r.rtrace, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));

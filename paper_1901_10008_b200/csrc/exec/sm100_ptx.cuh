@@ -15,6 +15,26 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// Warp-uniform broadcast of lane 0's value: ptxas then knows the result is uniform and keeps it
+// (and what is derived from it) in uniform registers, so tcgen05/TMA instructions issued by an
+// elected lane take their operands directly instead of through a per-instruction
+// ELECT/R2UR.BROADCAST/BRA.U.ANY loop (measured: ~200 cycles per UTCHMMA that way).
+__device__ __forceinline__ int32_t warp_uni(int32_t x) { return __shfl_sync(0xffffffffu, x, 0); }
+__device__ __forceinline__ uint32_t warp_uni(uint32_t x) { return __shfl_sync(0xffffffffu, x, 0); }
+__device__ __forceinline__ uint64_t warp_uni(uint64_t x) {
+    return ((uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(x >> 32), 0) << 32) | __shfl_sync(0xffffffffu, (uint32_t)x, 0);
+}
+// One lane of a converged warp (the lowest active one, i.e. lane 0 under uniform control flow).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 l;\n\t"
+        "elect.sync l|p, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // ---- mbarrier ------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

@@ -67,4 +67,6 @@ for c in pick:
     for it in by_cta[c]:
         r_ = lambda t: f"{rel(t):6.2f}" if t else "   -  "
         print(f"   p{it['problem']:3d} {str(shapes[it['problem'] % 16]):18s} kb {it['kb1']-it['kb0']:3d} ns {it['nsplit']} |"
-              f" {r_(it['t_prod'])} {r_(it['t_mma_done'])} {r_(it['t_epi'])} {r_(it['t_end'])}")
+              f" {r_(it['t_prod'])} {r_(it['t_mma_done'])} {r_(it['t_epi'])} {r_(it['t_end'])}"
+              + (f" | reduced {r_(it['t_e_start'])} ticket {r_(it['t_e_staged'])} finalized {r_(it['t_e_bar'])}"
+                 if it['nsplit'] > 1 else ""))
