@@ -209,6 +209,8 @@ struct KernelArgs {
     const int64_t* hpub;
     int64_t* hdone;          // host-mapped: step seq + 1 written when a slot's step completed
     int32_t window;          // resident: max steps a CTA may run ahead of the slowest
+    int32_t grab_ahead;      // resident: units the list scheduler may keep ahead of the producer
+                             // before it grabs another list of the same step
     uint64_t* rtrace;        // resident diagnostics: 4 stamps per (step, CTA), or null
     int32_t rtrace_steps;
     // inline step (no host plan): the members' work items are enumerated on the device, item
@@ -1170,6 +1172,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
     int64_t* aq = reinterpret_cast<int64_t*>(aempty + kAcctQ);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aq + kAcctQ);
     int32_t* split_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
+    volatile uint32_t* prod_units = reinterpret_cast<volatile uint32_t*>(split_flag + 1);   // units the producer took
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
@@ -1207,6 +1210,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             mbar_init(&aempty[q], 1);
         }
         mbar_fence_init();
+        *prod_units = 0u;
     }
     if (warp == 1 && has_gemm) tmem_alloc(tmem_slot, Cfg::tmem_cols);
     tc_fence_before();
@@ -1297,9 +1301,11 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 timed(ic, kISUempty, true, [&] { mbar_wait(&uempty[uslot], uphase ^ 1); });
                 return &uq[uslot];
             };
+            uint32_t pub_units = 0;
             auto publish = [&]() {
                 mbar_arrive(&ufull[uslot]);   // release: the unit is visible to the consumers
                 advance_unit();
+                ++pub_units;
             };
             auto push_ctl = [&](int64_t k, int32_t code) {
                 Unit* u = unit_slot();
@@ -1353,8 +1359,6 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                         idx = atomicAdd(grab, 1u) - base;
                         continue;
                     }
-                    // the next grab's round trip overlaps this list's resolution
-                    const uint32_t nxt = atomicAdd(grab, 1u) - base;
                     GMX_INSTR_INC(kISLists);
                     if (inl == 0) {
                         const int32_t beg = __ldcg(off + idx), end = __ldcg(off + idx + 1);
@@ -1398,6 +1402,12 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                             publish();
                         } while (have);
                     }
+                    // Another list of this step only once the producer has (nearly) caught up:
+                    // grabbing eagerly let the first CTAs to arrive take two lists each while
+                    // others got none (a lone step ran ~2x its plan's critical path). The grab's
+                    // round trip then overlaps the producer's last k-blocks of this list.
+                    while ((int32_t)(pub_units - *prod_units) > args.grab_ahead) {}
+                    const uint32_t nxt = atomicAdd(grab, 1u) - base;
                     if (nxt >= G) {
                         // no more lists of step k for us: take the first grab of step k + 1
                         // now, so its round trip overlaps the publication / ordering polls.
@@ -1508,6 +1518,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 timed(ic, kIPUnit, !first, [&] { u = next_unit(first); });
                 const int32_t uidx = warp_uni(u->idx);
                 const int64_t uk = u->k;
+                if (lane == 0) *prod_units = *prod_units + 1u;   // the list scheduler paces its grabs on this
                 if (uidx >= 0) {
                     issue_list(unit_view(u));   // releases the unit after reading its last item
                 } else {
@@ -1955,6 +1966,7 @@ struct gmx_exec {
         std::vector<void*> graveyard;          // device tables retired during residency
         std::vector<uint8_t> zeros;            // host zeros for copy-engine clears while resident
         int window = 16;                       // max steps a CTA may run ahead (option "resident_window")
+        int grab_ahead = 1;                    // option "grab_ahead": see KernelArgs::grab_ahead
         int64_t relay_ns = 0;                  // last residency: release -> last relay (diagnostic)
         int32_t rtrace_steps = 0;              // option "rtrace": stamp this many steps
         uint64_t* rtrace = nullptr;
@@ -2458,6 +2470,7 @@ int gmx_exec_resident_begin_ex(gmx_exec* ex, void* stream_ptr, int32_t hold) {
     args.hpub = r.hpub_d;
     args.hdone = r.hdone_d;
     args.window = r.window;
+    args.grab_ahead = ex->res.grab_ahead;
     if (r.rtrace_steps > 0) {
         // (step, CTA) stamps + one row of relay stamps + one row of host-report stamps
         const size_t nb = ((size_t)r.rtrace_steps * r.grid * 8 + 2 * (size_t)r.rtrace_steps) * sizeof(uint64_t);
@@ -2935,6 +2948,10 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
     } else if (n == "inline_promote") {
         if (value < 0 || value > 1000000) return fail(GMX_EINVAL, "inline_promote must be >= 0");
         ex->inline_promote = (int)value;
+        return GMX_OK;
+    } else if (n == "grab_ahead") {
+        if (value < 0 || value > 64) return fail(GMX_EINVAL, "grab_ahead must be in [0, 64]");
+        ex->res.grab_ahead = (int)value;
         return GMX_OK;
     } else if (n == "resident_window") {
         if (value < 1 || value > kMaxWindow) return fail(GMX_EINVAL, "resident_window must be in [1, 16]");

@@ -103,7 +103,8 @@ for k in (0, 1, 2, 3, S // 2):
         f = [buf[(k * G + c) * 8 + i] for i in range(8)]
         if not f[0]:
             continue
-        rows.append((c, (f[0] - t0) / 1e3, (f[1] - t0) / 1e3, (f[2] - t0) / 1e3, (f[3] - t0) / 1e3, f[4], f[5], f[6]))
+        rel = lambda x: (x - t0) / 1e3 if x else -1.0
+        rows.append((c, rel(f[0]), rel(f[1]), rel(f[2]), rel(f[3]), f[4], rel(f[7])))
     if not rows:
         continue
     q = lambda xs: " ".join(f"{x:7.2f}" for x in (min(xs), sorted(xs)[len(xs) // 4], sorted(xs)[len(xs) // 2],
@@ -113,7 +114,8 @@ for k in (0, 1, 2, 3, S // 2):
     print("   prod issued ", q([r[2] for r in rows]))
     print("   epi start   ", q([r[3] for r in rows]))
     print("   epi done    ", q([r[4] for r in rows]))
-    print("   slowest:", [tuple(round(x, 2) if isinstance(x, float) else x for x in r) for r in sorted(rows, key=lambda r: r[4])[-5:]])
+    print("   items done  ", q([r[6] for r in rows]))
+    print("   slowest (cta, prod start, prod issued, epi start, accounted, n items, items done):", [tuple(round(x, 2) if isinstance(x, float) else x for x in r) for r in sorted(rows, key=lambda r: r[4])[-5:]])
 
 b.ex.set_option("rtrace", 0)
 ev, gt, plan = bench.time_resident(b, 400)
