@@ -1,0 +1,3 @@
+timeout 200 python tools/chain_latency.py resnet50 resident=0 > gpurun_out/r02q.txt 2>&1
+timeout 200 python tools/chain_latency.py resnet50 resident=1 >> gpurun_out/r02q.txt 2>&1
+timeout 200 python tools/chain_latency.py bert_base resident=1 >> gpurun_out/r02q.txt 2>&1
