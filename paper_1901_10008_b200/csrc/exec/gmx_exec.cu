@@ -385,9 +385,13 @@ __device__ __forceinline__ void wait_step_done(const DevQueue* q, int64_t seq, u
     }
 }
 
+// GELU (erf form) out of line: erff inlined at every activation site made up over a quarter of
+// the kernel's SASS, spreading the hot code (instruction-cache misses were the top stall)
+__device__ __noinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+
 __device__ __forceinline__ float apply_act(float x, int32_t act) {
     if (act == GMX_ACT_RELU) return fmaxf(x, 0.0f);
-    if (act == GMX_ACT_GELU) return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+    if (act == GMX_ACT_GELU) return gelu_erf(x);
     return x;
 }
 
@@ -430,7 +434,6 @@ __device__ __forceinline__ EpiParams load_epi(const DevProblem* P) {
     return e;
 }
 
-__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
 // bias + activation over one 32-column accumulator chunk, with every branch hoisted out of
 // the (fully unrolled) element loops: the epilogue runs one warp per SMSP, so per-element

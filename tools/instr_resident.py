@@ -44,7 +44,7 @@ def run(opts, steps=400):
     b.ex.set_option("rtrace", steps + rows)
     _, t, _ = time_resident(b, steps)
     grid = C.c_int32()
-    buf = (C.c_uint64 * ((steps + rows) * 148 * 8))()
+    buf = (C.c_uint64 * ((steps + rows) * 148 * 8 + 2 * (steps + rows)))()
     rc = b.ex._lib.gmx_exec_resident_read_rtrace(b.ex._h, buf, len(buf), C.byref(grid))
     assert rc == 0
     G = grid.value
