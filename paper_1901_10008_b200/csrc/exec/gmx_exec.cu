@@ -7,14 +7,16 @@
 //   GEMM items   128 x BN output tiles (BN in {32..128}), K streamed in 64-element blocks:
 //                TMA (SWIZZLE_128B) -> 6-stage smem ring -> tcgen05.mma (M=128, fp32 accumulate
 //                in TMEM, double-buffered accumulators) -> tcgen05.ld epilogue with fused bias +
-//                activation -> bf16/fp32 stores. Long-K tiles are split along K; partials meet in
-//                an fp32 workspace and the last-arriving CTA reduces them in split order
-//                (deterministic). The larger of m/n goes on the UMMA-M side ("role swap").
+//                activation -> bf16/fp32 stores. Long-K tiles are split along K; partials are
+//                added into an fp32 L2 workspace (red.global.add, arrival order: NOT bitwise
+//                deterministic run to run; option max_split=1 is) and the last-arriving split
+//                finalizes. The side needing fewer tile loads goes on UMMA-M ("role swap").
 //   GEMV items   row blocks of y = W x, streamed with 16-byte non-allocating loads.
 //   Eltwise      vectorised y = act(x) ranges.
 //
-// Warp roles (6 warps, 1 CTA per SM, grid <= #SMs, persistent):
-//   warp 0  TMA producer (one lane)       warp 1  TMEM owner + UMMA issuer (one lane)
+// Warp roles (6 warps per step launch, 8 resident; 1 CTA per SM, grid <= #SMs):
+//   warp 0  TMA producer (warp-wide, one elected lane issues)
+//   warp 1  TMEM owner + UMMA issuer (warp-wide, one elected lane issues)
 //   warps 2-5  epilogue: TMEM -> registers -> global, and the CUDA-core GEMV / eltwise items.
 // Each role walks the same per-CTA item list; only the roles an item needs act on it.
 //

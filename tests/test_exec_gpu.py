@@ -399,8 +399,17 @@ def test_measured_autotuner_writes_reference_format_table(tmp_path):
     sched = gm.Scheduler(gm.load_profile("b200"), gm.SchedulerPolicy("ooo"), tuning_table=back)
     k = gm.KernelSpec(0, "s0", "gemm", keys[0].dims, "fp16", arrival=0, deadline=10_000_000)
     sched.add_request(gm.InferenceRequest(0, "s0", (k,), 0, gm.LatencyConstraint(10_000_000)))
-    dispatches, _, _ = sched.step(0)
-    assert dispatches or True   # decisions come from the same cost model with the tuned entry
+    # the tuned entry prices the dispatch: its predicted duration is the superkernel cost that
+    # form_superkernel computes from the loaded table (coalesce.py:109-131)
+    now, dispatches = 0, []
+    for _ in range(4):
+        dispatches, _, wake = sched.step(now)
+        if dispatches:
+            break
+        now = wake
+    assert len(dispatches) == 1 and dispatches[0].kernel_ids == (0,)
+    sk = gm.form_superkernel(gm.cluster_shapes([k])[0], back, gm.load_profile("b200"), co_tenancy=1)
+    assert dispatches[0].predicted_duration == sk.cost.duration
 
 
 def test_inline_steps_device_enumerated(ex):
