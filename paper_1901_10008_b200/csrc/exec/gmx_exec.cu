@@ -90,13 +90,17 @@ constexpr int kMaxBN = 128;
 constexpr int kStageA = kTileRows * kBlockK * 2;   // 16 KB
 constexpr int kStageB = kMaxBN * kBlockK * 2;      // 16 KB
 constexpr int kStageBytes = kStageA + kStageB;
-// GEMV rows staged through the TMA ring (bulk copies into the 32 KB stages): whole rows of at
-// most one stage, up to 16 per stage. Returns 0 when a problem cannot be staged (row larger than
-// a stage, or rows / base not 16-byte aligned): its items stream rows with 16-byte loads instead.
-__host__ __device__ __forceinline__ int gemv_rows_per_stage(int64_t row_bytes, int64_t pitch_bytes, uintptr_t base) {
-    if (row_bytes <= 0 || row_bytes > kStageBytes || (row_bytes & 15) || (pitch_bytes & 15) || (base & 15)) return 0;
-    const int64_t r = kStageBytes / row_bytes;
-    return (int)(r < 16 ? r : 16);
+// GEMV W streamed through the TMA ring as 2D TENSOR tiles (a 1D bulk copy moves ~30 GB/s per
+// SM, a tensor box ~3x that): a stage is two {256-element x R-row} boxes side by side (R = 16
+// fp32 / 32 bf16 rows, 16 KB per box), i.e. R rows x 512 columns; an item is a whole number of
+// R-row blocks, each block one stage per 512 columns. Problems whose W / x cannot be described
+// by a tensor map (16-byte alignment) stream rows with 16-byte loads instead (gemv_rows).
+constexpr int kGvBoxCols = 256;
+constexpr int kGvStageCols = 2 * kGvBoxCols;
+__host__ __device__ constexpr int gv_box_rows(bool f32) { return f32 ? 16 : 32; }
+__host__ __device__ __forceinline__ int gv_stages(int rows, int cols, bool f32) {
+    const int R = gv_box_rows(f32);
+    return ((rows + R - 1) / R) * ((cols + kGvStageCols - 1) / kGvStageCols);
 }
 
 template <int kCtasPerSm>
@@ -320,10 +324,8 @@ __device__ __forceinline__ bool next_item(const StepView& v, ItemCursor& c, Work
             } else if (kind == kItemGemv) {
                 it.row0 = u * kInlineGemvRows;
                 it.col0 = min(rows, it.row0 + kInlineGemvRows);
-                const int64_t esz = P->in_dt == GMX_ST_F32 ? 4 : 2;
-                const int rps = gemv_rows_per_stage(P->cols * esz, P->ld_in0 * esz,
-                                                    reinterpret_cast<uintptr_t>(P->in0));
-                it.kb1 = rps ? (it.col0 - it.row0 + rps - 1) / rps : 0;   // ring stages (0: unstaged)
+                // ring stages (0: unstaged); P->bn = 1 when W has its tensor map
+                it.kb1 = P->bn ? gv_stages(it.col0 - it.row0, P->cols, P->in_dt == GMX_ST_F32) : 0;
             } else {
                 it.row0 = u * kInlineEltwise;
                 it.col0 = min(rows, it.row0 + kInlineEltwise);
@@ -843,47 +845,75 @@ __device__ void gemv_rows(const DevProblem* Pg, int r0, int r1, int ew) {
     }
 }
 
-// Staged GEMV item (4 epilogue warps): rows arrive in ring stages (bulk copies issued by the
-// producer lane); warp ew reduces rows ew, ew + 4, ... of each stage against x (L1-resident),
-// then the 4 warps release the stage together.
+// Staged GEMV item (4 epilogue warps): W arrives in ring stages of two tensor boxes (R rows x
+// 512 columns); warp ew accumulates rows ew*R/4 .. of each R-row block against x (L1-resident),
+// the 4 warps release each stage together, and a block's rows are reduced across the lanes and
+// stored once its last column stage is done.
+// The ring position comes in by value and the new one is returned packed (stage | phase << 16).
+// (Measured: these CUDA-core item functions out of line — __noinline__ — cost C2 5 % through
+// the call ABI's spills; inlined they cost it ~1 %.)
 template <typename T>
-__device__ void gemv_staged(const DevProblem* Pg, const WorkItem& it, int ew, int etid, uint8_t* smem,
-                            uint64_t* full, uint64_t* empty, int& rstage, uint32_t& rphase, int kStages) {
-    constexpr int kVec = 16 / sizeof(T);
+__device__ __forceinline__ uint32_t gemv_staged(const DevProblem* Pg, const WorkItem it, int ew, int etid, uint8_t* smem,
+                                             uint64_t* full, uint64_t* empty, int rstage, uint32_t rphase, int kStages) {
+    constexpr bool kF32 = sizeof(T) == 4;
+    constexpr int R = gv_box_rows(kF32), RW = R / 4;             // block rows, rows per warp
+    constexpr int kVec = 16 / sizeof(T);                         // elements per 16-byte vector
+    constexpr uint32_t kRowBytes = kGvBoxCols * sizeof(T);       // one box row
+    constexpr uint32_t kBoxBytes = kRowBytes * R;                // 16 KB
+    constexpr int kPerLane = kGvBoxCols / (32 * kVec);           // vectors per lane per box row
     const int n = Pg->cols;
-    const int64_t row = (int64_t)n * sizeof(T);
-    const int rps = gemv_rows_per_stage(row, Pg->ld_in0 * (int64_t)sizeof(T), reinterpret_cast<uintptr_t>(Pg->in0));
+    const int nck = (n + kGvStageCols - 1) / kGvStageCols;
+    const int nb = (it.col0 - it.row0 + R - 1) / R;
     const uint4* xv = reinterpret_cast<const uint4*>(Pg->in1);
     void* out = Pg->out;
     const float* bias = Pg->bias;
     const int32_t act = Pg->act, out_dt = Pg->out_dt;
     const int lane = lane_id();
-    const int nv = n / kVec;
-    for (int st = 0; st < it.kb1; ++st) {
-        mbar_wait(&full[rstage], rphase);
-        const uint32_t base = smem_u32(smem + rstage * kStageBytes);
-        const int ra = it.row0 + st * rps, rb = min(it.col0, ra + rps);
-        for (int r = ra + ew; r < rb; r += 4) {
-            const uint32_t rowa = base + (uint32_t)((r - ra) * row);
-            float acc = 0.0f;
-            int j = lane;
-            for (; j + 32 < nv; j += 64) {
-                const uint4 w0 = ld_shared_v4(rowa + 16u * j), w1 = ld_shared_v4(rowa + 16u * (j + 32));
-                const uint4 x0 = __ldg(xv + j), x1 = __ldg(xv + j + 32);
-                acc += dot_v4(w0, x0, T()) + dot_v4(w1, x1, T());
-            }
-            for (; j < nv; j += 32) acc += dot_v4(ld_shared_v4(rowa + 16u * j), __ldg(xv + j), T());
+    for (int rb = 0; rb < nb; ++rb) {
+        float acc[RW];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) {
-                const float b = bias ? __ldg(bias + r) : 0.0f;
-                store_one(out, r, out_dt, apply_act(acc + b, act));
+        for (int r = 0; r < RW; ++r) acc[r] = 0.0f;
+        for (int cc = 0; cc < nck; ++cc) {
+            mbar_wait(&full[rstage], rphase);
+            const uint32_t base = smem_u32(smem + rstage * kStageBytes);
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                const int c0 = cc * kGvStageCols + b * kGvBoxCols;
+                uint4 xx[kPerLane];
+#pragma unroll
+                for (int q = 0; q < kPerLane; ++q) {
+                    const int col = c0 + (lane + 32 * q) * kVec;   // n % kVec == 0 (registration)
+                    xx[q] = col < n ? __ldg(xv + col / kVec) : make_uint4(0u, 0u, 0u, 0u);
+                }
+#pragma unroll
+                for (int r = 0; r < RW; ++r) {
+                    const uint32_t ra = base + (uint32_t)b * kBoxBytes + (uint32_t)(ew * RW + r) * kRowBytes;
+#pragma unroll
+                    for (int q = 0; q < kPerLane; ++q)
+                        acc[r] += dot_v4(ld_shared_v4(ra + 16u * (uint32_t)(lane + 32 * q)), xx[q], T());
+                }
+            }
+            named_bar_sync(4, 128);   // every warp is done reading the stage
+            if (etid == 0) mbar_arrive(&empty[rstage]);
+            if (++rstage == kStages) { rstage = 0; rphase ^= 1; }
+        }
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const int row = it.row0 + rb * R + ew * RW + r;
+                if (row < it.col0) {
+                    const float bv = bias ? __ldg(bias + row) : 0.0f;
+                    store_one(out, row, out_dt, apply_act(acc[r] + bv, act));
+                }
             }
         }
-        named_bar_sync(4, 128);   // every warp is done reading the stage
-        if (etid == 0) mbar_arrive(&empty[rstage]);
-        if (++rstage == kStages) { rstage = 0; rphase ^= 1; }
     }
+    return (uint32_t)rstage | (rphase << 16);
 }
 
 template <typename T>
@@ -1136,7 +1166,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
     int64_t* aq = reinterpret_cast<int64_t*>(aempty + kAcctQ);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aq + kAcctQ);
     int32_t* split_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
-    volatile uint32_t* prod_units = reinterpret_cast<volatile uint32_t*>(split_flag + 1);   // units the producer took
+    uint32_t* prod_units = reinterpret_cast<uint32_t*>(split_flag + 1);   // units the producer took (shared atomics)
 
     const int warp = threadIdx.x >> 5;
     const int lane = lane_id();
@@ -1356,7 +1386,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     // grabbing eagerly let the first CTAs to arrive take two lists each while
                     // others got none (a lone step ran ~2x its plan's critical path). The grab's
                     // round trip then overlaps the producer's last k-blocks of this list.
-                    while ((int32_t)(pub_units - *prod_units) > args.grab_ahead) {}
+                    while ((int32_t)(pub_units - atomicOr(prod_units, 0u)) > args.grab_ahead) {}
                     const uint32_t nxt = atomicAdd(grab, 1u) - base;
                     if (nxt >= G) {
                         // no more lists of step k for us: take the first grab of step k + 1
@@ -1412,24 +1442,21 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     const DevProblem* P = reinterpret_cast<const DevProblem*>(
                         warp_uni(reinterpret_cast<uint64_t>(v.probs + it.problem)));
                     if (item_kind(type) == kItemGemv && kb1 > 0) {
-                        // staged GEMV: whole rows by bulk copy into the ring, consumed by the epilogue warps
-                        const int32_t row0 = warp_uni(it.row0), row1 = warp_uni(it.col0);
-                        const char* w = reinterpret_cast<const char*>(P->in0);
-                        const int64_t esz = P->in_dt == GMX_ST_F32 ? 4 : 2;
-                        const int64_t row = (int64_t)P->cols * esz, pitch = P->ld_in0 * esz;
-                        const int rps = gemv_rows_per_stage(row, pitch, reinterpret_cast<uintptr_t>(w));
+                        // staged GEMV: W as tensor boxes (two per stage), consumed by the epilogue warps
+                        const bool f32 = warp_uni(P->in_dt) == GMX_ST_F32;
+                        const int R = gv_box_rows(f32);
+                        const int nck = (warp_uni(P->cols) + kGvStageCols - 1) / kGvStageCols;
+                        const int32_t row0 = warp_uni(it.row0);
+                        const uint32_t box_bytes = (uint32_t)(kGvBoxCols * R * (f32 ? 4 : 2));
                         for (int st = 0; st < kb1; ++st) {
                             mbar_wait(&empty[stage], phase ^ 1);
-                            if (lane == 0) {
-                                const int ra = row0 + st * rps, rb = min(row1, ra + rps);
-                                uint8_t* tile = smem + stage * kStageBytes;
-                                mbar_expect_tx(&full[stage], (uint32_t)((rb - ra) * row));
-                                if (row == pitch) {
-                                    bulk_load(tile, w + ra * pitch, (uint32_t)((rb - ra) * row), &full[stage]);
-                                } else {
-                                    for (int r = ra; r < rb; ++r)
-                                        bulk_load(tile + (r - ra) * row, w + r * pitch, (uint32_t)row, &full[stage]);
-                                }
+                            const int rb = st / nck, cc = st % nck;
+                            uint8_t* tile = smem + stage * kStageBytes;
+                            if (elect_one()) {
+                                mbar_expect_tx(&full[stage], 2 * box_bytes);   // OOB parts arrive zero-filled
+                                tma_load_2d(tile, &P->tm_rows, &full[stage], cc * kGvStageCols, row0 + rb * R);
+                                tma_load_2d(tile + box_bytes, &P->tm_rows, &full[stage], cc * kGvStageCols + kGvBoxCols,
+                                            row0 + rb * R);
                             }
                             __syncwarp();
                             if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -1468,7 +1495,7 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 timed(ic, kIPUnit, !first, [&] { u = next_unit(first); });
                 const int32_t uidx = warp_uni(u->idx);
                 const int64_t uk = u->k;
-                if (lane == 0) *prod_units = *prod_units + 1u;   // the list scheduler paces its grabs on this
+                if (lane == 0) atomicAdd(prod_units, 1u);   // the list scheduler paces its grabs on this
                 if (uidx >= 0) {
                     issue_list(unit_view(u));   // releases the unit after reading its last item
                 } else {
@@ -1514,9 +1541,15 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 for_each_item(v, [&](const WorkItem& it, int i) {
                     const int32_t type = warp_uni((int32_t)it.type);
                     const int32_t kb0 = warp_uni(it.kb0), kb1 = warp_uni(it.kb1);
-                    if (item_kind(type) == kItemGemv) {   // staged GEMV: its ring stages are the epilogue's
-                        for (int st = 0; st < kb1; ++st)
+                    if (item_kind(type) == kItemGemv) {
+                        // staged GEMV: its ring stages are the epilogue's. Still wait for each one to
+                        // be filled: a role that skipped stages without waiting could run more than
+                        // one lap ahead of the producer, and a parity wait cannot tell lap L from
+                        // lap L + 2 (it would take a GEMV stage's data for its next k-block).
+                        for (int st = 0; st < kb1; ++st) {
+                            mbar_wait(&full[stage], phase);
                             if (++stage == kStages) { stage = 0; phase ^= 1; }
+                        }
                         return;
                     }
                     if (item_kind(type) != kItemGemm) return;
@@ -1704,10 +1737,13 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     }
                     if (++acc == kAcc) { acc = 0; acc_phase ^= 1; }
                 } else if (it.type == kItemGemv && it.kb1 > 0) {
+                    uint32_t rs;
                     if (Pg->in_dt == GMX_ST_F32)
-                        gemv_staged<float>(Pg, it, ew, etid, smem, full, empty, rstage, rphase, kStages);
+                        rs = gemv_staged<float>(Pg, it, ew, etid, smem, full, empty, rstage, rphase, kStages);
                     else
-                        gemv_staged<__nv_bfloat16>(Pg, it, ew, etid, smem, full, empty, rstage, rphase, kStages);
+                        rs = gemv_staged<__nv_bfloat16>(Pg, it, ew, etid, smem, full, empty, rstage, rphase, kStages);
+                    rstage = (int)(rs & 0xFFFFu);
+                    rphase = rs >> 16;
                 } else if (it.type == kItemGemv) {
                     if (Pg->in_dt == GMX_ST_F32)
                         gemv_rows<float>(Pg, it.row0, it.col0, ew);
@@ -1875,7 +1911,7 @@ struct gmx_exec {
     // GEMV rows through the TMA ring (bulk copies) when stageable. Off by default: faster for a
     // held batch of C1 steps (11.7 vs 13.3 us/step) but slower lone and live-fed (C1 through the
     // resident runtime 17.7 vs 11.6 us per round; tools/c1_kernel.py, tools/ab_c1.sh)
-    bool gemv_staged = false;
+    bool gemv_staged = true;              // option "gemv_staged": W as tensor boxes through the ring
     int ctas_per_sm = 1;         // 1, or 2 CTAs of the coalesced kernel per SM (the latter runs as 2 waves)
     bool cache_plans = true;
     bool attr_set = false;
@@ -2045,19 +2081,20 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
         if (P.kind == kItemGemv) {
             const double row_bytes = (double)P.cols * (P.in_dt == GMX_ST_F32 ? 4 : 2);
             const double item_bytes = std::max(32768.0, (target * 0.5 - kCudaCoreFixedNs) / kNsPerKB * 1024.0);
-            // multiples of 16 rows: 4 epilogue warps x 4 rows in flight each (gemv_rows)
-            int rows_per = (int)std::max(16.0, std::floor(item_bytes / row_bytes));
-            rows_per = std::max(16, (rows_per / 16) * 16);
+            // whole row blocks: 16 rows (4 epilogue warps x 4 rows in flight, gemv_rows) or the
+            // staged path's R-row tensor boxes
+            const bool f32 = P.in_dt == GMX_ST_F32;
+            const bool staged = ex->gemv_staged && P.bn != 0;
+            const int blk = staged ? gv_box_rows(f32) : 16;
+            int rows_per = (int)std::max((double)blk, std::floor(item_bytes / row_bytes));
+            rows_per = std::max(blk, (rows_per / blk) * blk);
             for (int r0 = 0; r0 < P.rows; r0 += rows_per) {
                 WorkItem it{};
                 it.problem = s;
                 it.type = kItemGemv;
                 it.row0 = r0;
                 it.col0 = std::min(P.rows, r0 + rows_per);
-                const int64_t esz = P.in_dt == GMX_ST_F32 ? 4 : 2;
-                const int rps = ex->gemv_staged ? gemv_rows_per_stage((int64_t)P.cols * esz, P.ld_in0 * esz,
-                                                                      reinterpret_cast<uintptr_t>(P.in0)) : 0;
-                it.kb1 = rps ? (it.col0 - it.row0 + rps - 1) / rps : 0;   // ring stages (0: unstaged)
+                it.kb1 = staged ? gv_stages(it.col0 - it.row0, P.cols, f32) : 0;   // ring stages (0: unstaged)
                 cands.push_back({it, row_bytes * (it.col0 - it.row0) / 1024.0 * kNsPerKB + kCudaCoreFixedNs});
                 ++st.n_gemv_items;
             }
@@ -2665,6 +2702,21 @@ int gmx_exec_register(gmx_exec* ex, const gmx_problem_desc* d, int32_t* out_slot
         P.in0 = d->a;
         P.in1 = d->b;
         P.ld_in0 = d->lda;
+        // W as a 2D tensor ({256-element x R-row} boxes, no swizzle) for the staged path
+        P.bn = 0;
+        const bool f32 = d->in_dtype == GMX_ST_F32;
+        if (((reinterpret_cast<uintptr_t>(d->a) | reinterpret_cast<uintptr_t>(d->b)) & 15) == 0 &&
+            (d->lda * isz) % 16 == 0 && d->n % (16 / isz) == 0) {
+            auto fn = encode_fn();
+            cuuint64_t dims[2] = {(cuuint64_t)d->n, (cuuint64_t)d->m};
+            cuuint64_t strides[1] = {(cuuint64_t)(d->lda * isz)};
+            cuuint32_t box[2] = {(cuuint32_t)kGvBoxCols, (cuuint32_t)gv_box_rows(f32)};
+            cuuint32_t estr[2] = {1, 1};
+            if (fn && fn(&P.tm_rows, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                         const_cast<void*>(d->a), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+                P.bn = 1;
+        }
         hp.op_bytes = isz * (d->m * d->n + d->n) + osz * d->m;
         hp.flops = 2 * d->m * d->n;
     } else if (d->op == GMX_OP_ELEMENTWISE) {

@@ -169,19 +169,22 @@ def test_elementwise(ex, n, dtype, act):
 
 
 def test_gemv_staged_through_tma_ring(ex):
-    """Option gemv_staged: GEMV rows by bulk copy into the TMA ring, reduced by the epilogue
-    warps, interleaved with GEMM items that share the ring (stage accounting in all roles)."""
+    """Option gemv_staged: GEMV W as 2D tensor boxes through the TMA ring (incl. a fully
+    out-of-bounds second box, n=1280), reduced by the epilogue warps, interleaved with GEMM items
+    that share the ring (stage accounting in all roles); n=17 falls back to row streaming."""
     from paper_1901_10008_b200.executor import OperandSet
-    ex.set_option("gemv_staged", 1)
-    ex.clear_plans()
     try:
-        _run(ex, [OperandSet("gemv", (1000, 2048), dtype="fp32", seed=21 + i) for i in range(4)])
-        _run(ex, [OperandSet("gemm", (256, 196, 512), seed=31), OperandSet("gemv", (1000, 2048), dtype="fp32", seed=32),
-                  OperandSet("gemv", (777, 1280), seed=33, bias=True, activation="relu"),
-                  OperandSet("gemm", (512, 49, 4608), seed=34), OperandSet("gemv", (33, 17), dtype="fp32", seed=35),
-                  OperandSet("gemm", (64, 3136, 147), seed=36)])
+        for staged in (1, 0):   # default: staged; 0: every GEMV streams rows with 16-byte loads
+            ex.set_option("gemv_staged", staged)
+            ex.clear_plans()
+            _run(ex, [OperandSet("gemv", (1000, 2048), dtype="fp32", seed=21 + i) for i in range(4)])
+            _run(ex, [OperandSet("gemm", (256, 196, 512), seed=31),
+                      OperandSet("gemv", (1000, 2048), dtype="fp32", seed=32),
+                      OperandSet("gemv", (777, 1280), seed=33, bias=True, activation="relu"),
+                      OperandSet("gemm", (512, 49, 4608), seed=34), OperandSet("gemv", (33, 17), dtype="fp32", seed=35),
+                      OperandSet("gemm", (64, 3136, 147), seed=36)])
     finally:
-        ex.set_option("gemv_staged", 0)
+        ex.set_option("gemv_staged", 1)
         ex.clear_plans()
 
 

@@ -1,0 +1,10 @@
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/r02ag_test.txt
+O=gpurun_out/sanitizer_r02b.txt
+echo "# compute-sanitizer on the coalesced kernel (round 2 after the tensor-staged GEMV + warp-uniform issue changes, B200, tools/sanitize_target.py)" > $O
+for w in step resident; do for t in memcheck racecheck synccheck; do
+  echo "## san_${w}_${t}" >> $O
+  timeout 600 compute-sanitizer --tool $t python tools/sanitize_target.py $w 2>&1 | grep -E "ok$|SUMMARY|Invalid|Error|error" | head -20 >> $O
+  echo "rc=${PIPESTATUS[0]}" >> $O
+done; done
+timeout 300 python tools/configs.py --configs c1 >> gpurun_out/r02ag_c1.txt 2>&1
+timeout 300 python tools/configs.py --configs c1 --resident >> gpurun_out/r02ag_c1.txt 2>&1
