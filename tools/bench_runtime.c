@@ -40,10 +40,17 @@ int main(int argc, char** argv) {
     gmx_runtime_stats st;
     const int warm = 200;
     gmx_runtime_run(rt, (int64_t)warm * RNS - 1, NULL, &st);
+    if (getenv("GMX_PROF")) gmx_runtime_set_profiling(rt, 1);
     double t0 = now_us();
     gmx_runtime_run(rt, (int64_t)rounds * RNS - 1, NULL, &st);
     double el = now_us() - t0;
     if (el / (rounds - warm) < best) best = el / (rounds - warm);
+    if (rep == reps - 1 && getenv("GMX_PROF")) {
+        int64_t p[4];
+        gmx_runtime_host_profile(rt, p);
+        printf("per round (us): add_request %.3f step %.3f complete %.3f launch %.3f\n", p[0] / 1e3 / (rounds - warm),
+               p[1] / 1e3 / (rounds - warm), p[2] / 1e3 / (rounds - warm), p[3] / 1e3 / (rounds - warm));
+    }
     if (rep == reps - 1)
         printf("%.3f us per round, best of %d (%lld steps, %lld dispatches over %d rounds)\n", best, reps,
                (long long)st.steps, (long long)st.dispatches, rounds);
