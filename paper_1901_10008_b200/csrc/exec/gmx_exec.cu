@@ -162,7 +162,7 @@ static_assert(sizeof(WorkItem) == 32, "WorkItem layout");
 // step flagged `wait_all` (dependent members, or slots/plans reused inside the window) waits
 // for every earlier step.
 constexpr int kQueue = 1024;  // ring slots (host and device)
-constexpr int kMaxWindow = 16;   // max steps a CTA may run ahead of the slowest (option, <= this)
+constexpr int kMaxWindow = 512;   // max steps a CTA may run ahead of the slowest (option, <= this; < kQueue)
 
 struct StepDesc {
     const DevProblem* probs;
@@ -172,7 +172,8 @@ struct StepDesc {
     int32_t* counters;
     int32_t grid;             // CTAs holding items in this step (<= gridDim.x)
     int32_t wait_all;         // a member depends on earlier outputs of unknown steps: all first
-    int32_t stop;
+    int32_t stop;             // bit 0: stop entry; bit 1: the plan is still being uploaded — wait for
+                              // DevQueue::plan_ready[slot] == seq + 1 (copy-engine stream write)
     int32_t nwait;            // entries of wait_steps in use
     int64_t wait_steps[4];    // earlier steps that must be complete first: producers of this
                               // step's inputs, users of its plan (split-K state) or slots (outputs)
@@ -196,6 +197,7 @@ struct DevQueue {
     int64_t _pad[1];
     uint32_t done[kQueue];    // monotonic count of item lists finished, per slot
     uint32_t grab[kQueue];    // monotonic list-grab counter, per slot (2 x grid per step)
+    uint32_t plan_ready[kQueue];   // seq + 1 once a plan uploaded during the residency has landed
 };
 
 struct KernelArgs {
@@ -362,6 +364,11 @@ __device__ __forceinline__ void for_each_item(const StepView& v, F&& f, D&& done
 __device__ __forceinline__ int64_t ld_acquire_gpu_s64(const int64_t* p) {
     int64_t v;
     asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ int64_t ld_acquire_sys_s64(const int64_t* p) {
@@ -1015,7 +1022,7 @@ __device__ __forceinline__ bool step_published(const KernelArgs& a, int64_t k) {
         __nanosleep(128);
         if (global_timer_ns() - t0 > 60000000000ull) __trap();   // host never published
     }
-    return __ldcg(&a.dq->ring[k % kQueue].stop) != 0;
+    return (__ldcg(&a.dq->ring[k % kQueue].stop) & 1) != 0;
 }
 
 // Resident producer: bounded skew + explicit ordering before taking lists of step k.
@@ -1125,7 +1132,7 @@ __device__ void dispatch_steps(const KernelArgs& a) {
                         __stcg(dst + q, x);
                     }
                 }
-                stop = head->stop != 0;
+                stop = (head->stop & 1) != 0;
             }
         }
         k += n;
@@ -1307,6 +1314,14 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                     break;
                 }
                 timed(ic, kISOrder, true, [&] { step_order(args, k); });
+                if (__ldcg(&args.dq->ring[k % kQueue].stop) & 2) {   // plan still uploading: wait for its flag
+                    const uint32_t want = (uint32_t)(k + 1);
+                    const uint64_t t0 = global_timer_ns();
+                    while (ld_acquire_sys_u32(&args.dq->plan_ready[k % kQueue]) != want) {
+                        __nanosleep(64);
+                        if (global_timer_ns() - t0 > 8000000000ull) __trap();
+                    }
+                }
                 if (args.rtrace && k < args.rtrace_steps)
                     args.rtrace[(k * G + blockIdx.x) * 8] = global_timer_ns();
                 const uint32_t base = grab_base(k);
@@ -1817,6 +1832,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+using StreamWriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static StreamWriteValue32Fn stream_write_fn() {
+    static StreamWriteValue32Fn fn = [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<StreamWriteValue32Fn>(p);
+        return (StreamWriteValue32Fn) nullptr;
+    }();
+    return fn;
+}
+
 // experiment knob GMX_L2_PROMO=0|64|128|256 (default 256): L2 sector promotion of operand loads
 static CUtensorMapL2promotion l2_promotion() {
     static CUtensorMapL2promotion v = [] {
@@ -1860,6 +1888,8 @@ struct HostProblem {
 // Device buffers of a plan come from the stream-ordered allocator (cudaMallocAsync) and are
 // released with cudaFreeAsync on the stream of the plan's last launch, so evicting a plan
 // whose launch is still queued is safe and no eviction ever synchronizes the device.
+constexpr size_t kPinZeros = (size_t)4 << 20;   // residency pinned staging: leading zero block
+
 struct Plan {
     std::vector<int32_t> key;       // sorted slot list this plan was built for
     int64_t res_seq = -1;           // resident: last step (seq) that used this plan, in residency res_epoch
@@ -1873,6 +1903,7 @@ struct Plan {
     float* d_ws = nullptr;
     int32_t* d_counters = nullptr;
     bool uploaded = false;
+    bool in_arena = false;          // device memory is the residency arena's (never freed per plan)
     int64_t ws_floats = 0;
     int32_t n_counters = 0;
     cudaStream_t stream = nullptr;  // stream of the last launch
@@ -1880,8 +1911,8 @@ struct Plan {
     uint64_t last_use = 0;          // LRU clock
     gmx_plan_stats stats{};
     ~Plan() {
-        if (d_buf) cudaFreeAsync(d_buf, stream);
-        if (d_state) cudaFreeAsync(d_state, stream);
+        if (d_buf && !in_arena) cudaFreeAsync(d_buf, stream);
+        if (d_state && !in_arena) cudaFreeAsync(d_state, stream);
         if (done_ev) cudaEventDestroy(done_ev);
     }
 };
@@ -1951,7 +1982,19 @@ struct gmx_exec {
         std::vector<int64_t> last_read;        // per slot: last step (seq) that read its output (WAR)
         std::vector<void*> graveyard;          // device tables retired during residency
         std::vector<uint8_t> zeros;            // host zeros for copy-engine clears while resident
+        // plans first built DURING a residency: device memory from a bump arena allocated before the
+        // persistent launch (no stream-ordered allocation behind the kernel), uploaded on `upload`
+        // without blocking the serving thread; the step waits on the device for a copy-engine
+        // stream write of plan_ready (cuStreamWriteValue32 after the copies)
+        char* arena = nullptr;
+        size_t arena_size = 0, arena_used = 0;
+        // pinned staging for those uploads (a pageable source can make cudaMemcpyAsync wait): a
+        // zero block for copy-engine clears, then a bump region reset at each resident_begin (the
+        // previous residency's copies completed before its kernel did)
+        char* pin = nullptr;
+        size_t pin_size = 0, pin_used = 0;
         int window = 16;                       // max steps a CTA may run ahead (option "resident_window")
+        int64_t wait_ns = 0, waits = 0, pub_ns = 0, pubs = 0, up_ns = 0, ups = 0, wr_ns = 0;   // diagnostics (dbg bit 16)
         int grab_ahead = 1;                    // option "grab_ahead": see KernelArgs::grab_ahead
         int64_t relay_ns = 0;                  // last residency: release -> last relay (diagnostic)
         int32_t rtrace_steps = 0;              // option "rtrace": stamp this many steps
@@ -2161,35 +2204,78 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
 // Upload the plan (one stream-ordered allocation + one copy) and allocate its split-K state.
 // Split-K state is owned by the plan, so steps of different plans that overlap under PDL never
 // share accumulators; a plan launched again while a recent launch of it may still run waits.
+// Bump allocation from the residency arena (256-byte aligned); nullptr when it is full.
+static void* arena_alloc(gmx_exec* ex, size_t bytes) {
+    auto& r = ex->res;
+    const size_t b = (bytes + 255) & ~size_t(255);
+    if (!r.arena || r.arena_used + b > r.arena_size) return nullptr;
+    void* p = r.arena + r.arena_used;
+    r.arena_used += b;
+    return p;
+}
+
 static int upload_plan(gmx_exec* ex, Plan& plan, cudaStream_t stream) {
     if (plan.uploaded) return GMX_OK;
+    auto& r = ex->res;
     const size_t items_bytes = std::max<size_t>(1, plan.items.size()) * sizeof(WorkItem);
     const size_t off_bytes = plan.cta_off.size() * sizeof(int32_t);
-    std::vector<uint8_t> staging(items_bytes + off_bytes);
-    if (!plan.items.empty()) std::memcpy(staging.data(), plan.items.data(), plan.items.size() * sizeof(WorkItem));
-    std::memcpy(staging.data() + items_bytes, plan.cta_off.data(), off_bytes);
-    GMX_CUDA(cudaMallocAsync(&plan.d_buf, staging.size(), stream));
-    GMX_CUDA(cudaMemcpyAsync(plan.d_buf, staging.data(), staging.size(), cudaMemcpyHostToDevice, stream));
-    plan.d_items = reinterpret_cast<WorkItem*>(plan.d_buf);
-    plan.d_off = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(plan.d_buf) + items_bytes);
-    if (plan.ws_floats > 0 || plan.n_counters > 0) {
-        const size_t ws_bytes = (size_t)plan.ws_floats * sizeof(float);
-        const size_t state = ws_bytes + (size_t)std::max(1, 2 * plan.n_counters) * sizeof(int32_t);
+    const size_t nstage = items_bytes + off_bytes, nal = (nstage + 255) & ~size_t(255);
+    const size_t ws_bytes = (size_t)plan.ws_floats * sizeof(float);
+    const size_t state = (plan.ws_floats > 0 || plan.n_counters > 0)
+                             ? ws_bytes + (size_t)std::max(1, 2 * plan.n_counters) * sizeof(int32_t) : 0;
+    auto fill = [&](uint8_t* dst) {
+        if (!plan.items.empty()) std::memcpy(dst, plan.items.data(), plan.items.size() * sizeof(WorkItem));
+        std::memcpy(dst + items_bytes, plan.cta_off.data(), off_bytes);
+    };
+    auto finish = [&]() {
+        plan.d_items = reinterpret_cast<WorkItem*>(plan.d_buf);
+        plan.d_off = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(plan.d_buf) + items_bytes);
+        if (state) {
+            plan.d_ws = reinterpret_cast<float*>(plan.d_state);
+            plan.d_counters = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(plan.d_state) + ws_bytes);
+        }
+        plan.stream = stream;
+        plan.uploaded = true;
+        return GMX_OK;
+    };
+    // during a residency: one block of the arena (plan + split-K state), the plan filled by ONE
+    // copy from pinned staging — no stream-ordered allocation, no pageable staging, no host wait.
+    // The arena is zeroed whenever it is (re)started and the kernel re-arms split-K state after
+    // use, so a new plan's state needs no clearing.
+    const size_t span = nal;
+    if (r.active && r.pin && r.pin_used + span <= r.pin_size) {
+        if (char* blk = static_cast<char*>(arena_alloc(ex, nal + state))) {
+            uint8_t* stg = reinterpret_cast<uint8_t*>(r.pin + r.pin_used);
+            r.pin_used += span;
+            fill(stg);
+            GMX_CUDA(cudaMemcpyAsync(blk, stg, nstage, cudaMemcpyHostToDevice, stream));
+            plan.d_buf = blk;
+            plan.d_state = state ? blk + nal : nullptr;
+            plan.in_arena = true;
+            return finish();
+        }
+    }
+    // general path: stream-ordered allocations
+    std::vector<uint8_t> staging(nstage);
+    fill(staging.data());
+    GMX_CUDA(cudaMallocAsync(&plan.d_buf, nstage, stream));
+    GMX_CUDA(cudaMemcpyAsync(plan.d_buf, staging.data(), nstage, cudaMemcpyHostToDevice, stream));
+    if (state) {
         GMX_CUDA(cudaMallocAsync(&plan.d_state, state, stream));
-        if (ex->res.active) {
+        if (r.active) {
             // a memset KERNEL could not get an SM while the persistent kernel holds them all:
             // zero through the copy engine instead
-            ex->res.zeros.resize(std::max(ex->res.zeros.size(), state));
-            GMX_CUDA(cudaMemcpyAsync(plan.d_state, ex->res.zeros.data(), state, cudaMemcpyHostToDevice, stream));
+            const void* zsrc = r.pin;
+            if (!r.pin || state > kPinZeros) {
+                r.zeros.resize(std::max(r.zeros.size(), state));
+                zsrc = r.zeros.data();
+            }
+            GMX_CUDA(cudaMemcpyAsync(plan.d_state, zsrc, state, cudaMemcpyHostToDevice, stream));
         } else {
             GMX_CUDA(cudaMemsetAsync(plan.d_state, 0, state, stream));
         }
-        plan.d_ws = reinterpret_cast<float*>(plan.d_state);
-        plan.d_counters = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(plan.d_state) + ws_bytes);
     }
-    plan.stream = stream;
-    plan.uploaded = true;
-    return GMX_OK;
+    return finish();
 }
 
 // Least-recently-used eighth of the cache goes when it is full (stream-ordered frees).
@@ -2215,6 +2301,26 @@ static void evict_plans(gmx_exec* ex) {
             }
         }
     }
+}
+
+// Drop every plan living in the residency arena and rewind the arena (only when no kernel can
+// still read it: called at resident_begin once the previous persistent launch has completed).
+static void recycle_arena(gmx_exec* ex) {
+    for (auto& kv : ex->plans) {
+        auto& bucket = kv.second;
+        for (size_t i = 0; i < bucket.size();) {
+            if (bucket[i]->in_arena) {
+                if (ex->last == bucket[i].get()) ex->last = nullptr;
+                for (auto& r : ex->recent)
+                    if (r == bucket[i].get()) r = nullptr;
+                bucket.erase(bucket.begin() + i);
+                --ex->n_plans;
+            } else {
+                ++i;
+            }
+        }
+    }
+    ex->res.arena_used = 0;
 }
 
 }  // namespace gmx
@@ -2286,25 +2392,59 @@ static int wait_slot_free(gmx_exec* ex, int64_t seq) {
     return GMX_OK;
 }
 
+static int64_t host_ns() {
+    timespec t;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    return (int64_t)t.tv_sec * 1000000000 + t.tv_nsec;
+}
+
 static int publish_step(gmx_exec* ex, const StepDesc& d) {
     auto& r = ex->res;
     int rc;
-    if ((rc = wait_slot_free(ex, r.seq))) return rc;
+    if (ex->dbg & 16) {
+        const int64_t t0 = host_ns();
+        const volatile int64_t* hd = r.hdone + (r.seq % kQueue);
+        const bool blocked = r.seq >= kQueue && *hd < r.seq - kQueue + 1;
+        if ((rc = wait_slot_free(ex, r.seq))) return rc;
+        if (blocked) { r.wait_ns += host_ns() - t0; ++r.waits; }
+    } else if ((rc = wait_slot_free(ex, r.seq))) {
+        return rc;
+    }
     StepDesc* slot = r.hring + (r.seq % kQueue);
+    const int64_t tp = (ex->dbg & 16) ? host_ns() : 0;
     std::memcpy(slot, &d, sizeof d);
     __atomic_store_n(r.hpub, r.seq + 1, __ATOMIC_RELEASE);   // x86: ordered after the entry
+    if (ex->dbg & 16) r.wr_ns += host_ns() - tp;
     ++r.seq;
     return GMX_OK;
 }
 
 // Resident mode: the step goes to the persistent kernel's queue instead of a launch.
+static int enqueue_resident_impl(gmx_exec* ex, Plan* plan, const std::vector<int32_t>& key, const int32_t* dep_slots,
+                                 int32_t ndep, int32_t flags, bool cached, int64_t* seq_out);
 static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>& key, const int32_t* dep_slots,
                             int32_t ndep, int32_t flags, bool cached, int64_t* seq_out) {
+    if (!(ex->dbg & 16)) return enqueue_resident_impl(ex, plan, key, dep_slots, ndep, flags, cached, seq_out);
+    const int64_t t0 = host_ns();
+    const int rc = enqueue_resident_impl(ex, plan, key, dep_slots, ndep, flags, cached, seq_out);
+    ex->res.pub_ns += host_ns() - t0;
+    ++ex->res.pubs;
+    return rc;
+}
+static int enqueue_resident_impl(gmx_exec* ex, Plan* plan, const std::vector<int32_t>& key, const int32_t* dep_slots,
+                                 int32_t ndep, int32_t flags, bool cached, int64_t* seq_out) {
     auto& r = ex->res;
     int rc;
+    bool pending = false;   // plan uploaded by this call: the step waits on the device for its flag
     if (plan && !plan->uploaded) {
+        const int64_t tu = (ex->dbg & 16) ? host_ns() : 0;
         if ((rc = upload_plan(ex, *plan, r.upload))) return rc;
-        GMX_CUDA(cudaStreamSynchronize(r.upload));
+        if (ex->dbg & 16) { r.up_ns += host_ns() - tu; ++r.ups; }
+        if (plan->in_arena && stream_write_fn()) {
+            pending = true;
+        } else {
+            GMX_CUDA(cudaStreamSynchronize(r.upload));
+        }
     }
     if (plan) {
         plan->stream = r.stream;   // later frees are ordered after the persistent kernel
@@ -2353,6 +2493,12 @@ static int enqueue_resident(gmx_exec* ex, Plan* plan, const std::vector<int32_t>
         for (size_t i = 0; i < key.size(); ++i) d.inline_slots[i] = key[i];
     }
     d.wait_all = wait_all ? 1 : 0;
+    if (pending) {   // copy-engine write of seq + 1 after the plan's copies, on the same stream
+        d.stop = 2;
+        const CUresult cr = stream_write_fn()(r.upload, reinterpret_cast<CUdeviceptr>(&r.dq->plan_ready[seq % kQueue]),
+                                              (cuuint32_t)(seq + 1), 0);
+        if (cr != CUDA_SUCCESS) return fail(GMX_ECUDA, "cuStreamWriteValue32 failed: " + std::to_string((int)cr));
+    }
     // nwait -1: no wait, only the proxy fence (inputs of already-observed producers)
     d.nwait = wait_all ? 0 : (nw == 0 && ((flags & GMX_LAUNCH_FENCE) || ndep > 0) ? -1 : nw);
     for (int q = 0; q < nw; ++q) d.wait_steps[q] = waits[q];
@@ -2429,6 +2575,12 @@ int gmx_exec_resident_begin_ex(gmx_exec* ex, void* stream_ptr, int32_t hold) {
         GMX_CUDA(cudaHostGetDevicePointer((void**)&r.hdone_d, r.hdone, 0));
         GMX_CUDA(cudaMalloc(&r.dq, sizeof(DevQueue)));
         GMX_CUDA(cudaStreamCreateWithFlags(&r.upload, cudaStreamNonBlocking));
+        r.arena_size = (size_t)256 << 20;
+        GMX_CUDA(cudaMalloc(&r.arena, r.arena_size));
+        GMX_CUDA(cudaMemset(r.arena, 0, r.arena_size));
+        r.pin_size = (size_t)32 << 20;
+        GMX_CUDA(cudaHostAlloc(&r.pin, r.pin_size, cudaHostAllocDefault));
+        std::memset(r.pin, 0, kPinZeros);
     }
     cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_ptr);
     int rc;
@@ -2442,7 +2594,14 @@ int gmx_exec_resident_begin_ex(gmx_exec* ex, void* stream_ptr, int32_t hold) {
                              sizeof(DevQueue) - offsetof(DevQueue, published), stream));
     if ((rc = set_kernel_attrs(ex))) return rc;
     r.grid = ex->num_sms * ex->ctas_per_sm;
+    // plans first built in earlier residencies live in the arena: once it is half full and the
+    // previous persistent launch has finished (nothing can read them), drop them and rewind
+    if (r.arena_used > r.arena_size / 2 && (!r.stream || cudaStreamQuery(r.stream) == cudaSuccess)) {
+        GMX_CUDA(cudaMemsetAsync(r.arena, 0, r.arena_used, stream));   // ordered before the launch below
+        recycle_arena(ex);
+    }
     r.seq = 0;
+    r.pin_used = kPinZeros;
     r.stream = stream;
     ++r.epoch;
     r.last_write.assign(ex->probs.size(), -1);
@@ -2544,6 +2703,13 @@ int gmx_exec_resident_end(gmx_exec* ex) {
     if (!ex) return fail(GMX_EINVAL, "null argument");
     auto& r = ex->res;
     if (!r.active) return fail(GMX_ESTATE, "not resident");
+    if (ex->dbg & 16) {
+        std::fprintf(stderr, "[gmx resident] steps %lld, host blocked on a full ring %lld times, %.3f ms; enqueue %.3f ms over %lld; plan uploads %lld, %.3f ms\n",
+                     (long long)r.seq, (long long)r.waits, r.wait_ns / 1e6, r.pub_ns / 1e6, (long long)r.pubs,
+                     (long long)r.ups, r.up_ns / 1e6);
+        std::fprintf(stderr, "[gmx resident] ring entry writes %.3f ms\n", r.wr_ns / 1e6);
+        r.wait_ns = r.waits = r.pub_ns = r.pubs = r.up_ns = r.ups = r.wr_ns = 0;
+    }
     __atomic_store_n(r.hpub + 1, (int64_t)1, __ATOMIC_RELEASE);   // a held start is released
     StepDesc d{};
     d.stop = 1;
@@ -2609,6 +2775,8 @@ void gmx_exec_destroy(gmx_exec* ex) {
     }
     ex->plans.clear();
     ex->uncached.reset();
+    if (ex->res.arena) cudaFree(ex->res.arena);   // after the plans that may live in it
+    if (ex->res.pin) cudaFreeHost(ex->res.pin);
     if (ex->d_probs) cudaFree(ex->d_probs);
     if (ex->ws) cudaFree(ex->ws);
     if (ex->counters) cudaFree(ex->counters);
@@ -2956,7 +3124,7 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
         ex->res.grab_ahead = (int)value;
         return GMX_OK;
     } else if (n == "resident_window") {
-        if (value < 1 || value > kMaxWindow) return fail(GMX_EINVAL, "resident_window must be in [1, 16]");
+        if (value < 1 || value > kMaxWindow) return fail(GMX_EINVAL, "resident_window must be in [1, 512]");
         ex->res.window = (int)value;
         return GMX_OK;
     } else if (n == "ctas_per_sm") {

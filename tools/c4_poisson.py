@@ -26,10 +26,13 @@ MODELS = ("resnet50", "bert_base", "mobilenet_v2")
 SLO_NS = 10_000_000
 
 
-def setup(tenants, models):
+def setup(tenants, models, opts=()):
     """Executor + operands per (stream, layer), shared by that stream's requests."""
     lib = gm.kernels.load_model_library()
     ex = Executor()
+    for kv in opts:
+        k, v = kv.split("=")
+        ex.set_option(k, int(v))
     slots = {}
     for i in range(tenants):
         protos = lib[models[i % len(models)]]
@@ -113,9 +116,13 @@ def main():
     ap.add_argument("--streams", default="8")
     ap.add_argument("--stagger-ns", default="10000")
     ap.add_argument("--resident", action="store_true", help="run the steps through the resident executor")
+    ap.add_argument("--opt", action="append", default=[], help="executor option k=v (repeatable)")
     args = ap.parse_args()
     models = args.models.split(",")
-    ex, slots = setup(args.tenants, models)
+    from bench import pin_serving_thread   # the serving loop on one idle core (as in bench.py)
+    _, core = pin_serving_thread(torch.cuda.current_device())
+    print(json.dumps({"serving_core": core}), flush=True)
+    ex, slots = setup(args.tenants, models, args.opt)
     # warm-up pass: CUDA/driver lazy init, TMA descriptors, plan cache for the recurring step shapes
     run(ex, slots, 20.0, args.tenants, 50_000_000, models, seed=99, resident=args.resident)
     for stagger in (int(x) for x in args.stagger_ns.split(",")):
