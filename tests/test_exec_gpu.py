@@ -498,3 +498,35 @@ def test_resident_long_lists_span_units(ex):
         _check(o)
     for sl in slots:
         ex.unregister(sl)
+
+
+def test_resident_plans_built_during_residency(ex):
+    """Compositions first seen WHILE the persistent kernel runs: their plans are built on the host,
+    copied into the residency arena on the upload stream and published at once, the steps waiting
+    on the device for the copy-engine flag (split-K workspaces included: the arena starts zeroed).
+    Many distinct compositions in a row, each launched twice, every output checked."""
+    from paper_1901_10008_b200.executor import OperandSet
+    ex.clear_plans()
+    ops = [OperandSet("gemm", dims, seed=1500 + i) for i, dims in
+           enumerate([(512, 49, 4608), (256, 196, 2304), (64, 3136, 147), (1024, 196, 256), (512, 49, 1024),
+                      (2048, 49, 512), (128, 784, 1152), (256, 3136, 64)])]
+    ops += [OperandSet("gemv", (1000, 2048), dtype="fp32", seed=1600),
+            OperandSet("elementwise", (50176,), seed=1601, activation="relu")]
+    slots = [o.register(ex) for o in ops]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for o in ops:
+            o.c.zero_()
+        n = 0
+        with ex.resident(s):
+            for r in range(1, len(slots)):          # every window of r consecutive members: a new plan
+                for j in range(0, len(slots) - r + 1, 3):
+                    ex.launch(slots[j:j + r], s, independent=True)
+                    ex.launch(slots[j:j + r], s, independent=True)
+                    n += 2
+        s.synchronize()
+    assert ex.resident_completed() == n
+    for o in ops:
+        _check(o)
+    for sl in slots:
+        ex.unregister(sl)
