@@ -367,8 +367,11 @@ def time_resident(bench, steps):
     torch = bench.torch
     s, side = torch.cuda.Stream(), torch.cuda.Stream()
     with torch.cuda.stream(s):
-        for j in range(bench.replicas):   # plans built and uploaded before the timed region
+        # resident plans (their own split: DESIGN.md §4) built and uploaded before the timed batch
+        bench.ex.resident_begin(s)
+        for j in range(bench.replicas):
             bench.ex.launch(bench.slots[j], s, independent=True)
+        bench.ex.resident_end()
         s.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         bench.ex.resident_begin(s, hold=True)

@@ -1904,6 +1904,7 @@ struct Plan {
     int32_t* d_counters = nullptr;
     bool uploaded = false;
     bool in_arena = false;          // device memory is the residency arena's (never freed per plan)
+    bool for_resident = false;      // built for resident steps (split_pct) or per-step launches (split_pct_step)
     int64_t ws_floats = 0;
     int32_t n_counters = 0;
     cudaStream_t stream = nullptr;  // stream of the last launch
@@ -1939,6 +1940,10 @@ struct gmx_exec {
     int32_t counters_cap = 0;
     int64_t max_split = 32;
     int64_t split_pct = 400;     // split a tile into pieces of about this % of the per-CTA share
+    // per-step launches run a step alone (no next step overlaps its tail), so their plans split
+    // finer: a lone C2 step 27.5 -> 23.5 us (CUDA events, queued), held resident steps keep the
+    // coarse split (5.96 vs 6.19 us at 200 %)
+    int64_t split_pct_step = 200;
     // GEMV rows through the TMA ring (bulk copies) when stageable. Off by default: faster for a
     // held batch of C1 steps (11.7 vs 13.3 us/step) but slower lone and live-fed (C1 through the
     // resident runtime 17.7 vs 11.6 us per round; tools/c1_kernel.py, tools/ab_c1.sh)
@@ -2086,7 +2091,7 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
     for (const TileRef& t : tiles) {
         const DevProblem& P = ex->probs[t.slot].dev;
         int nsplit = 1;
-        const double piece = target * (double)ex->split_pct / 100.0;
+        const double piece = target * (double)(ex->res.active ? ex->split_pct : ex->split_pct_step) / 100.0;
         if (t.cost > piece && P.kblocks >= 2 && P.tma_out) {
             nsplit = (int)std::min<int64_t>({(int64_t)std::ceil(t.cost / piece), (int64_t)P.kblocks, ex->max_split, 255});
             // splitting only pays when a piece plus the fixup beats the whole tile
@@ -3010,7 +3015,7 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
     if (ex->cache_plans) {
         auto& bucket = ex->plans[h];
         for (auto& p : bucket)
-            if (p->key == key) {
+            if (p->key == key && p->for_resident == ex->res.active) {   // per-mode split (split_pct*)
                 plan = p.get();
                 cached = true;
                 break;
@@ -3021,6 +3026,7 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
             auto p = std::make_unique<Plan>();
             if ((rc = build_plan(ex, key, *p))) return rc;
             p->key = key;
+            p->for_resident = ex->res.active;
             plan = p.get();
             ex->plans[h].push_back(std::move(p));
             ++ex->n_plans;
@@ -3132,9 +3138,10 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
         ex->ctas_per_sm = (int)value;
     } else if (n == "gemv_staged") {
         ex->gemv_staged = value != 0;   // applies to plans built afterwards (clear_plans)
-    } else if (n == "split_pct") {
+    } else if (n == "split_pct" || n == "split_pct_step") {   // split_pct sets both modes
         if (value < 10 || value > 2000) return fail(GMX_EINVAL, "split_pct must be in [10, 2000]");
-        ex->split_pct = value;
+        if (n == "split_pct") ex->split_pct = value;
+        ex->split_pct_step = value;
     } else if (n == "cache_plans") {
         ex->cache_plans = value != 0;
     } else if (n == "plan_capacity") {
