@@ -1004,10 +1004,10 @@ __device__ __forceinline__ StepView list_view(const KernelArgs& a, int64_t k, in
 // system-scope release store of seq + 1 into the host-mapped flag (cumulative over the other
 // lists' releases this acq_rel atomic observed). Reporting at the completing count instead of
 // from a polling lane took ~4.5 us off every step's completion latency as the host sees it.
-__device__ __forceinline__ void count_list_done(const KernelArgs& a, int64_t k) {
+__device__ __forceinline__ void count_list_done(const KernelArgs& a, int64_t k, uint32_t n = 1) {
     uint32_t old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&a.dq->done[k % kQueue]) : "memory");
-    if (old + 1u != gridDim.x * (uint32_t)(k / kQueue + 1)) return;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(&a.dq->done[k % kQueue]), "r"(n) : "memory");
+    if (old + n != gridDim.x * (uint32_t)(k / kQueue + 1)) return;
     asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(&a.hdone[k % kQueue]), "l"(k + 1) : "memory");
     const uint64_t t = global_timer_ns();
     atomicMax(reinterpret_cast<unsigned long long*>(&a.dq->t_last), (unsigned long long)t);
@@ -1274,9 +1274,11 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         if (lane == 0 && accountant) {
             for (int q = 0, ph = 0;; ) {
                 mbar_wait(&afull[q], (uint32_t)ph);
-                const int64_t kk = aq[q];
-                if (kk < 0) break;
-                count_list_done(args, kk);   // release: covers the epilogue's writes (synchronized via afull)
+                const int64_t kq = aq[q];
+                if (kq < 0) break;
+                // (lists << 48) | step: a CTA's lists of one step are counted together
+                count_list_done(args, kq & ((int64_t(1) << 48) - 1), (uint32_t)(kq >> 48));   // release: covers the
+                                                                                               // epilogue's writes (afull)
                 mbar_arrive(&aempty[q]);
                 if (++q == kAcctQ) { q = 0; ph ^= 1; }
             }
@@ -1653,17 +1655,18 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
         // is deferred until the CTA finished its next list (then only the older list's store
         // groups are waited for); at the end of a step (no more lists for this CTA) it is flushed,
         // since a later step may wait for this one.
-        int64_t acct_k = -1;
+        int64_t acct_k = -1;      // step of the finished lists not yet counted
+        uint32_t acct_n = 0;      // how many of them (a CTA's lists of one step are counted together)
         uint32_t acct_groups = 0;
         int aslot = 0;
         uint32_t aphase = 0;
-        auto hand_over = [&](int64_t kk) {   // etid 0: the accountant counts list kk (or stops, kk < 0)
+        auto hand_over = [&](int64_t kk, uint32_t n) {   // etid 0: the accountant counts n lists of step kk (or stops, kk < 0)
             mbar_wait(&aempty[aslot], aphase ^ 1);
-            aq[aslot] = kk;
+            aq[aslot] = kk < 0 ? kk : (kk | ((int64_t)n << 48));
             mbar_arrive(&afull[aslot]);   // release.cta: the epilogue's writes happen-before the count
             if (++aslot == kAcctQ) { aslot = 0; aphase ^= 1; }
         };
-        auto account_body = [&](int64_t kk, uint32_t newer_groups) {
+        auto account_body = [&](int64_t kk, uint32_t n, uint32_t newer_groups) {
             timed(ic, kIABar, true, [&] { named_bar_sync(1, 128); });   // all epilogue writes happen-before etid 0's release
             if (etid == 0) {
                 timed(ic, kIAWait, true, [&] {
@@ -1672,15 +1675,17 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 });
                 timed(ic, kIARed, true, [&] {
                     if (accountant)
-                        hand_over(kk);
+                        hand_over(kk, n);
                     else
-                        count_list_done(args, kk);
+                        count_list_done(args, kk, n);
                 });
                 if (args.rtrace && kk < args.rtrace_steps)
                     args.rtrace[(kk * gridDim.x + blockIdx.x) * 8 + 3] = global_timer_ns();
             }
         };
-        auto account = [&](int64_t kk, uint32_t newer_groups) { timed(ic, kIEAcct, true, [&] { account_body(kk, newer_groups); }); };
+        auto account = [&](int64_t kk, uint32_t n, uint32_t newer_groups) {
+            timed(ic, kIEAcct, true, [&] { account_body(kk, n, newer_groups); });
+        };
         for (bool first = true;; first = false) {
             const Unit* up;   // every epilogue thread waits on the unit barrier
             timed(ic, kIEUnit, !first, [&] { up = next_unit(first); });
@@ -1690,11 +1695,11 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 if (lane == 0) release_unit();
                 advance_unit();
                 if (acct_k >= 0) {
-                    account(acct_k, 0);
+                    account(acct_k, acct_n, 0);
                     acct_k = -1;
                 }
                 if (u.idx == kUnitStop) {
-                    if (etid == 0 && accountant) hand_over(-1);
+                    if (etid == 0 && accountant) hand_over(-1, 0);
                     if (etid == 0) {
                         instr_dump(args, ic, kIEUnit, kIETfull + 1);
                         instr_dump(args, ic, kIEStaged, kIXIssue + 1);
@@ -1783,8 +1788,13 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             advance_unit();
             if (rt && etid == 0) rt[7] = global_timer_ns();
             if (args.resident && u.last) {
-                if (acct_k >= 0) account(acct_k, groups - acct_groups);   // the previous list
-                acct_k = u.k;
+                if (acct_k == u.k) {   // another list of the pending step: counted with it
+                    ++acct_n;
+                } else {
+                    if (acct_k >= 0) account(acct_k, acct_n, groups - acct_groups);   // the previous step's lists
+                    acct_k = u.k;
+                    acct_n = 1;
+                }
                 acct_groups = groups;
             }
         }
