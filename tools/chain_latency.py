@@ -17,7 +17,11 @@ import paper_1901_10008_b200 as gm  # noqa: E402
 from paper_1901_10008_b200.executor import Executor, OperandSet  # noqa: E402
 from paper_1901_10008_b200.runtime import Runtime  # noqa: E402
 
-args = [a for a in sys.argv[1:] if "=" not in a]
+so = [a for a in sys.argv[1:] if a.endswith(".so")]
+if so:   # an A/B build of the executor (tools/ab_build.sh)
+    from paper_1901_10008_b200.executor import exec_lib
+    exec_lib(so[0])
+args = [a for a in sys.argv[1:] if "=" not in a and not a.endswith(".so")]
 kv = dict(a.split("=") for a in sys.argv[1:] if "=" in a)
 model = args[0] if args else "resnet50"
 resident = int(kv.pop("resident", 0)) != 0
