@@ -16,7 +16,11 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 
-kv = dict(a.split("=") for a in sys.argv[1:])
+so = [a for a in sys.argv[1:] if a.endswith(".so")]
+if so:   # an A/B build of the executor (tools/ab_build.sh)
+    from paper_1901_10008_b200.executor import exec_lib
+    exec_lib(so[0])
+kv = dict(a.split("=") for a in sys.argv[1:] if not a.endswith(".so"))
 STEPS = int(kv.pop("steps", 20))
 WARM = int(kv.pop("warmup", 5))
 DELAY_MS = float(kv.pop("delay_us", 0)) / 1e3
