@@ -19,9 +19,11 @@
  *   gemm (m,n,k):  C[m x n] = act(A[m x k] . B[k x n] + bias[m])
  *                  A given as A[m][lda] (K contiguous), B given TRANSPOSED as
  *                  Bt[n][ldb] (K contiguous: the NHWC im2col layout), C[m][ldc].
- *                  bf16 in, fp32 accumulate (tcgen05/TMEM), bf16 or fp32 out.
- *                  lda, ldb multiples of 8; pointers 16-byte aligned (TMA).
- *   gemv (m,n):    y[m] = act(W[m x n] . x[n] + bias[m]); W[m][lda]; fp32 or bf16.
+ *                  bf16 in (tcgen05 kind::f16) or fp32 in (kind::tf32: fp32-labelled
+ *                  GEMMs), fp32 accumulate in TMEM, bf16 or fp32 out. lda, ldb rows
+ *                  multiples of 16 bytes; pointers 16-byte aligned (TMA).
+ *   gemv (m,n):    y[m] = act(W[m x n] . x[n] + bias[m]); W[m][lda]; fp32 or bf16 (W
+ *                  streamed as 2D TMA tensor boxes when W rows and x are 16-byte aligned).
  *   elementwise n: y[i] = act(x[i] + bias?) ; x, y contiguous; fp32 or bf16.
  * All device pointers are caller-owned (torch tensors); the executor owns its
  * descriptor table, plans, and split-K workspace. Launches are asynchronous on
@@ -50,7 +52,7 @@ typedef struct gmx_exec gmx_exec;
 
 typedef struct gmx_problem_desc {
     int32_t op;            /* GMX_OP_GEMM / GMX_OP_GEMV / GMX_OP_ELEMENTWISE */
-    int32_t in_dtype;      /* GMX_ST_*: gemm must be BF16 */
+    int32_t in_dtype;      /* GMX_ST_*: gemm BF16 (bf16 tensor cores) or F32 (tf32 tensor cores) */
     int32_t out_dtype;     /* GMX_ST_* */
     int32_t activation;    /* GMX_ACT_* */
     int64_t m, n, k;       /* gemm (m,n,k); gemv (m,n,-); elementwise (n,-,-) in m */
