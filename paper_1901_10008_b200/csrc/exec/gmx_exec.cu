@@ -1025,6 +1025,28 @@ __device__ __forceinline__ bool step_published(const KernelArgs& a, int64_t k) {
     return (__ldcg(&a.dq->ring[k % kQueue].stop) & 1) != 0;
 }
 
+// Resident list scheduler: wait until step k is relayed (the descriptor is then read whole).
+__device__ __forceinline__ void step_relayed(const KernelArgs& a, int64_t k) {
+    const uint64_t t0 = global_timer_ns();
+    while (ld_acquire_gpu_s64(&a.dq->published) <= k) {
+        __nanosleep(64);
+        if (global_timer_ns() - t0 > 60000000000ull) __trap();   // host never published
+    }
+}
+
+// Ordering of step k from its descriptor head already in registers (one round trip for every
+// field instead of one per field).
+__device__ __forceinline__ void step_order_head(const KernelArgs& a, int64_t k, const StepDesc& d) {
+    if (d.wait_all) {
+        for (int64_t j = k - 1; j >= 0 && j >= k - a.window; --j) wait_step_done(a.dq, j, gridDim.x);
+        fence_proxy_async_global();   // later TMA loads read what those steps wrote
+    } else {
+        wait_step_done(a.dq, k - a.window, gridDim.x);
+        for (int q = 0; q < d.nwait; ++q) wait_step_done(a.dq, d.wait_steps[q], gridDim.x);
+        if (d.nwait != 0) fence_proxy_async_global();   // later TMA loads may read what they wrote
+    }
+}
+
 // Resident producer: bounded skew + explicit ordering before taking lists of step k.
 __device__ __forceinline__ void step_order(const KernelArgs& a, int64_t k) {
     const StepDesc* d = &a.dq->ring[k % kQueue];
@@ -1308,15 +1330,22 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
             uint32_t pre = 0;
             bool have_pre = false;
             for (int64_t k = 0;; ++k) {
-                bool stop = false;
-                timed(ic, kISPub, k > 0, [&] { stop = step_published(args, k); });
-                if (stop) {
+                timed(ic, kISPub, k > 0, [&] { step_relayed(args, k); });
+                // the descriptor head (6 x 16 B) in one round trip: flags, waits, plan pointers
+                StepDesc d;
+                {
+                    const uint4* hp = reinterpret_cast<const uint4*>(&args.dq->ring[k % kQueue]);
+                    uint4* hd = reinterpret_cast<uint4*>(&d);
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) hd[q] = __ldcg(hp + q);
+                }
+                if (d.stop & 1) {
                     push_ctl(k, kUnitStop);
                     instr_dump(args, ic, kISUempty, kISLists + 1);
                     break;
                 }
-                timed(ic, kISOrder, true, [&] { step_order(args, k); });
-                if (__ldcg(&args.dq->ring[k % kQueue].stop) & 2) {   // plan still uploading: wait for its flag
+                timed(ic, kISOrder, true, [&] { step_order_head(args, k, d); });
+                if (d.stop & 2) {   // plan still uploading: wait for its flag
                     const uint32_t want = (uint32_t)(k + 1);
                     const uint64_t t0 = global_timer_ns();
                     while (ld_acquire_sys_u32(&args.dq->plan_ready[k % kQueue]) != want) {
@@ -1330,15 +1359,14 @@ __global__ void __maxnreg__(kCtasPerSm == 2 ? 144 : 255) coalesced_step_kernel(c
                 uint32_t* grab = &args.dq->grab[k % kQueue];
                 uint32_t idx = have_pre ? pre : atomicAdd(grab, 1u) - base;
                 have_pre = false;
-                // the step's plan pointers (independent loads: one round trip)
-                const StepDesc* d = &args.dq->ring[k % kQueue];
-                const uint32_t L = (uint32_t)__ldcg(&d->grid);   // lists past L are empty
-                const int inl = __ldcg(&d->inline_n);
-                const DevProblem* probs = (const DevProblem*)__ldcg((const long long*)&d->probs);
-                const WorkItem* items = (const WorkItem*)__ldcg((const long long*)&d->items);
-                float* ws = (float*)__ldcg((const long long*)&d->ws);
-                int32_t* counters = (int32_t*)__ldcg((const long long*)&d->counters);
-                const int32_t* off = (const int32_t*)__ldcg((const long long*)&d->cta_off);
+                // the step's plan pointers (from the head read above)
+                const uint32_t L = (uint32_t)d.grid;   // lists past L are empty
+                const int inl = d.inline_n;
+                const DevProblem* probs = d.probs;
+                const WorkItem* items = d.items;
+                float* ws = d.ws;
+                int32_t* counters = d.counters;
+                const int32_t* off = d.cta_off;
                 auto begin_unit = [&](int32_t list, int32_t beg) -> Unit* {
                     Unit* u = unit_slot();
                     u->k = k;
