@@ -6,6 +6,7 @@
 //               scheduler.py:435-443): 64-bit hash + arena-stored members verified on hit.
 #pragma once
 
+#include <climits>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -20,12 +21,23 @@ inline uint64_t mix64(uint64_t x) {
     return x ^ (x >> 31);
 }
 
+// Hash of a short int64 sequence: one multiply-add per element, one finalizer (the element
+// chain of mix64 calls it replaces cost ~6 dependent operations per element).
+inline uint64_t hash_seq(uint64_t seed, const int64_t* v, size_t n) {
+    uint64_t h = seed;
+    for (size_t i = 0; i < n; ++i) h = (h ^ (uint64_t)v[i]) * 0x9E3779B97F4A7C15ull + (h >> 29);
+    return mix64(h ^ (uint64_t)n);
+}
+
+// IdMap keys are mostly consecutive ids (kernels, requests, dispatches): a Fibonacci
+// (multiplicative) hash spreads them over the table in one multiply, and the table is kept at
+// most half full so linear-probe chains stay short.
 class IdMap {
    public:
     IdMap() { rehash(64); }
 
     int32_t find(int64_t key) const {
-        size_t i = mix64((uint64_t)key) & mask_;
+        size_t i = home(key);
         while (slots_[i].used) {
             if (slots_[i].key == key) return slots_[i].val;
             i = (i + 1) & mask_;
@@ -35,8 +47,8 @@ class IdMap {
 
     // Insert or overwrite; returns the previous value or -1 (one probe sequence).
     int32_t put(int64_t key, int32_t val) {
-        if ((size_ + 1) * 4 > (mask_ + 1) * 3) rehash((mask_ + 1) * 2);
-        size_t i = mix64((uint64_t)key) & mask_;
+        if ((size_ + 1) * 2 > mask_ + 1) rehash((mask_ + 1) * 2);
+        size_t i = home(key);
         while (slots_[i].used) {
             if (slots_[i].key == key) {
                 const int32_t old = slots_[i].val;
@@ -50,17 +62,22 @@ class IdMap {
         return -1;
     }
 
-    bool erase(int64_t key) {
-        size_t i = mix64((uint64_t)key) & mask_;
+    bool erase(int64_t key) { return take(key) != kAbsent; }
+
+    // Remove `key` and return its value (kAbsent if it was not present): one probe sequence.
+    static constexpr int64_t kAbsent = INT64_MIN;
+    int64_t take(int64_t key) {
+        size_t i = home(key);
         while (slots_[i].used) {
             if (slots_[i].key == key) {
+                const int32_t val = slots_[i].val;
                 // backward-shift deletion keeps probe chains intact without tombstones
                 size_t j = i;
                 for (;;) {
                     j = (j + 1) & mask_;
                     if (!slots_[j].used) break;
-                    const size_t home = mix64((uint64_t)slots_[j].key) & mask_;
-                    const bool movable = (i <= j) ? (home <= i || home > j) : (home <= i && home > j);
+                    const size_t h = home(slots_[j].key);
+                    const bool movable = (i <= j) ? (h <= i || h > j) : (h <= i && h > j);
                     if (movable) {
                         slots_[i] = slots_[j];
                         i = j;
@@ -68,17 +85,18 @@ class IdMap {
                 }
                 slots_[i].used = 0;
                 --size_;
-                return true;
+                return val;
             }
             i = (i + 1) & mask_;
         }
-        return false;
+        return kAbsent;
     }
 
     size_t size() const { return size_; }
     void clear() {
         slots_.assign(64, Slot{0, 0, 0});
         mask_ = 63;
+        shift_ = 58;
         size_ = 0;
     }
 
@@ -89,10 +107,13 @@ class IdMap {
         int32_t used;
     };
 
+    size_t home(int64_t key) const { return (size_t)(((uint64_t)key * 0x9E3779B97F4A7C15ull) >> shift_); }
+
     void rehash(size_t cap) {
         std::vector<Slot> old = std::move(slots_);
         slots_.assign(cap, Slot{0, 0, 0});
         mask_ = cap - 1;
+        shift_ = 64 - __builtin_ctzll((unsigned long long)cap);
         size_ = 0;
         for (const Slot& e : old)
             if (e.used) put(e.key, e.val);
@@ -100,6 +121,7 @@ class IdMap {
 
     std::vector<Slot> slots_;
     size_t mask_ = 0, size_ = 0;
+    int shift_ = 58;
 };
 
 class SigSet {
@@ -157,8 +179,7 @@ class SigSet {
    private:
     static uint64_t hash(const int64_t* ids, int32_t n) {
         uint64_t h = 0x9E3779B97F4A7C15ull ^ (uint64_t)n;
-        for (int32_t i = 0; i < n; ++i) h = mix64(h ^ (uint64_t)ids[i]);
-        return h;
+        return hash_seq(h, ids, (size_t)n);
     }
     bool equal(int32_t e, const int64_t* ids, int32_t n) const {
         const int64_t* p = arena_.data() + offsets_[e];

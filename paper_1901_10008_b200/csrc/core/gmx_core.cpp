@@ -235,8 +235,7 @@ struct CostMemo {
     std::vector<Entry> tab = std::vector<Entry>(1024);
     template <typename F>
     int get(const int64_t (&key)[7], gmx_cost* out, F compute) {
-        uint64_t h = 0x9E3779B97F4A7C15ull;
-        for (int64_t k : key) h = mix64(h ^ (uint64_t)k);
+        const uint64_t h = hash_seq(0x9E3779B97F4A7C15ull, key, 7);
         Entry& e = tab[h & (tab.size() - 1)];
         if (e.used && std::memcmp(e.key, key, sizeof key) == 0) {
             *out = e.cost;
@@ -302,8 +301,8 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
     };
     for (int32_t i = 0; i < n; ++i) {
         const ShapeRec& r = recs[i];
-        uint64_t h = mix64(((uint64_t)r.op << 8 | (uint64_t)r.dtype) ^ mix64((uint64_t)r.dims[0]) ^
-                           mix64((uint64_t)r.dims[1] * 31) ^ mix64((uint64_t)r.dims[2] * 131));
+        const int64_t hk[4] = {(int64_t)((uint64_t)r.op << 8 | (uint64_t)r.dtype), r.dims[0], r.dims[1], r.dims[2]};
+        const uint64_t h = hash_seq(0x2545F4914F6CDD1Dull, hk, 4);
         size_t q = h & (cap - 1);
         while (htab[q] >= 0 && !same(recs[gfirst[htab[q]]], r)) q = (q + 1) & (cap - 1);
         if (htab[q] < 0) {
@@ -367,8 +366,7 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
             mkey.push_back(r.dims[2]);
             mkey.push_back(gcount[g]);
         }
-        mh = 0x243F6A8885A308D3ull;
-        for (int64_t x : mkey) mh = mix64(mh ^ (uint64_t)x);
+        mh = hash_seq(0x243F6A8885A308D3ull, mkey.data(), mkey.size());
         auto it = memo.find(mh);
         if (it != memo.end())
             for (const Memo& m : it->second)
@@ -665,7 +663,7 @@ static void make_dispatch(S* s, const std::vector<int32_t>& members, int64_t now
     s->v_disp.push_back(d.rec);
     s->free_sms -= alloc;
     s->has_last_ctx = true;
-    s->last_ctx = ctx_name;
+    if (s->last_ctx != ctx_name) s->last_ctx = ctx_name;
     s->inflight_slot.put(d.rec.dispatch_id, pi);
     ++s->n_inflight;
 }
@@ -1201,11 +1199,15 @@ int gmx_sched_add_request(gmx_sched* s, int64_t request_id, int32_t stream, int6
     r.first = (int32_t)s->kernels.size();
     r.count = 0;
     {   // distinct kernel ids (the reference's `remaining` is a set)
-        std::vector<int64_t>& ids = s->s_sig;
-        ids.clear();
-        for (int32_t i = 0; i < n; ++i) ids.push_back(ks[i].kernel_id);
-        std::sort(ids.begin(), ids.end());
-        r.remaining = (int64_t)(std::unique(ids.begin(), ids.end()) - ids.begin());
+        if (n <= 1) {
+            r.remaining = n;
+        } else {
+            std::vector<int64_t>& ids = s->s_sig;
+            ids.clear();
+            for (int32_t i = 0; i < n; ++i) ids.push_back(ks[i].kernel_id);
+            std::sort(ids.begin(), ids.end());
+            r.remaining = (int64_t)(std::unique(ids.begin(), ids.end()) - ids.begin());
+        }
     }
     const int32_t rslot = (int32_t)s->requests.size();
     if (s->evicted_stream[stream]) {

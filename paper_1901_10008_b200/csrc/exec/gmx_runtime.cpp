@@ -111,8 +111,8 @@ static void log_rec(gmx_runtime* rt, int32_t kind, int64_t t, int64_t a, int32_t
 
 // purge: an evicted request's undispatched kernels never reach a launch, so their slot and
 // producer-slot entries are dropped here (a finished request's were consumed at dispatch)
-static void release_request(gmx_runtime* rt, int64_t rid, bool purge = false) {
-    const int32_t pi = rt->req_index.find(rid);
+static void release_request(gmx_runtime* rt, int64_t rid, bool purge = false, int32_t known_pi = -1) {
+    const int32_t pi = known_pi >= 0 ? known_pi : rt->req_index.find(rid);
     if (pi < 0) return;
     if (purge) {
         const Pending& p = rt->pool[pi];
@@ -305,7 +305,7 @@ static int on_finished(gmx_runtime* rt, const gmx_complete_view& cv, int64_t now
         const int32_t pi = rt->req_index.find(r);
         if (pi >= 0) {
             if (now > rt->pool[pi].deadline) ++rt->st.slo_misses;
-            release_request(rt, r);
+            release_request(rt, r, false, pi);
         }
     }
     return GMX_OK;
@@ -365,18 +365,17 @@ static int step_and_launch(gmx_runtime* rt, int64_t now, void* stream, bool real
             const gmx_dispatch_rec& r = v.dispatches[d];
             for (int32_t j = 0; j < r.n_kernels; ++j) {
                 const int64_t kid = v.dispatch_kernel_ids[r.kernel_offset + j];
-                const int32_t slot = rt->slot_of.find(kid);
+                const int64_t taken = rt->slot_of.take(kid);
+                const int32_t slot = taken == gmx::IdMap::kAbsent ? -1 : (int32_t)taken;
                 if (slot < 0 && rt->ex) return fail(GMX_ESTATE, "dispatched kernel has no operands bound");
                 independent &= (slot & kHasDeps) == 0;
                 rt->launch_slots.push_back(slot & ~kHasDeps);
-                rt->slot_of.erase(kid);
                 if (slot & kHasDeps) {
-                    const int32_t off = rt->depslots_of.find(kid);
-                    if (off >= 0) {
+                    const int64_t off = rt->depslots_of.take(kid);
+                    if (off != gmx::IdMap::kAbsent) {
                         const int32_t cnt = rt->depslot_arena[off];
                         rt->launch_deps.insert(rt->launch_deps.end(), rt->depslot_arena.begin() + off + 1,
                                                rt->depslot_arena.begin() + off + 1 + cnt);
-                        rt->depslots_of.erase(kid);
                     }
                 }
             }
