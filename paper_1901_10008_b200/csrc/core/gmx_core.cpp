@@ -277,8 +277,10 @@ static double waste_ratio(u128 sum, int64_t count, int64_t padded_flops) {
 
 // coalesce.py:69-106. `order` receives member indices (into recs) grouped by
 // cluster in admission order.
+// `by_id`: recs are already in ascending id order (the scheduler's ready set usually is), so
+// the stable placement into shape groups leaves every group id-sorted.
 static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vector<int32_t>& order,
-                          std::vector<Cluster>& clusters) {
+                          std::vector<Cluster>& clusters, bool by_id = false) {
     if (!(budget >= 0.0 && budget < 1.0)) return fail(GMX_EINVAL, "pad_budget must be in [0, 1)");
     const int32_t n = (int32_t)recs.size();
     static thread_local std::vector<int32_t> idx;   // scratch: no allocation after warm-up
@@ -336,7 +338,7 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
         fill.assign(slot_of_group.begin(), slot_of_group.end());
         for (int32_t i = 0; i < n; ++i) idx[fill[gid[i]]++] = i;
     }
-    for (int32_t g = 0; g < ng; ++g) {
+    for (int32_t g = 0; g < ng && !by_id; ++g) {
         if (gcount[g] > 1)
             std::sort(idx.begin() + slot_of_group[g], idx.begin() + slot_of_group[g] + gcount[g],
                       [&](int32_t x, int32_t y) { return recs[x].id < recs[y].id; });
@@ -478,7 +480,14 @@ struct gmx_sched {
     gmx::IdMap kernel_slot;
     std::vector<gmx::RequestRec> requests;
     std::vector<int64_t> dep_arena;
-    std::vector<int32_t> ready;           // kernel slots
+    // Ready kernel slots, in arrival order with tombstones (-1) for removed ones: a removal is
+    // O(1) and keeps the order, the next live_ready() drops the tombstones. While every kernel
+    // entered in ascending id order (`ready_by_id`), live_ready() yields the set sorted by id
+    // and the coalescer skips its per-shape id sorts.
+    std::vector<int32_t> ready;
+    int32_t n_ready = 0;
+    int64_t ready_last_id = INT64_MIN;
+    bool ready_by_id = true;
     uint64_t ready_version = 1;           // bumped whenever the ready set / evictions change
     uint64_t clustered_version = 0;       // ready_version the cached clustering was built for
     std::vector<gmx::DispatchRec> pool;   // in-flight dispatches
@@ -532,6 +541,13 @@ struct gmx_sched {
         return stream_rank[st];
     }
     bool stream_less(int32_t a, int32_t b) { return rank(a) < rank(b); }
+    // sort stream indices by name (ranks refreshed once, then a branch-free comparator)
+    void sort_streams(std::vector<int32_t>& v) {
+        if (v.size() < 2) return;
+        rank(v[0]);
+        const int32_t* r = stream_rank.data();
+        std::sort(v.begin(), v.end(), [r](int32_t a, int32_t b) { return r[a] < r[b]; });
+    }
 };
 
 namespace gmx {
@@ -546,19 +562,37 @@ static void ready_add(S* s, int32_t slot) {
     KernelRec& k = s->kernels[slot];
     if (k.ready_pos >= 0) return;
     ++s->ready_version;
+    if (s->n_ready == 0) {   // empty: drop the tombstones, restart the id order
+        s->ready.clear();
+        s->ready_by_id = true;
+    } else if (k.id <= s->ready_last_id) {
+        s->ready_by_id = false;
+    }
+    s->ready_last_id = k.id;
     k.ready_pos = (int32_t)s->ready.size();
     s->ready.push_back(slot);
+    ++s->n_ready;
 }
 
 static void ready_remove(S* s, int32_t slot) {
     KernelRec& k = s->kernels[slot];
     if (k.ready_pos < 0) return;
     ++s->ready_version;
-    const int32_t last = s->ready.back();
-    s->ready[k.ready_pos] = last;
-    s->kernels[last].ready_pos = k.ready_pos;
-    s->ready.pop_back();
+    s->ready[k.ready_pos] = -1;
     k.ready_pos = -1;
+    --s->n_ready;
+}
+
+// drop the tombstones (order kept)
+static void ready_squeeze(S* s) {
+    if ((int32_t)s->ready.size() == s->n_ready) return;
+    int32_t w = 0;
+    for (int32_t slot : s->ready)
+        if (slot >= 0) {
+            s->kernels[slot].ready_pos = w;
+            s->ready[w++] = slot;
+        }
+    s->ready.resize(w);
 }
 
 // scheduler.py:195-203: this kernel plus every later, unfinished kernel of its request
@@ -579,7 +613,8 @@ static int64_t kernel_slack(const S* s, const KernelRec& k, int64_t now) {
 static int64_t slo_of(const S* s, const KernelRec& k) { return k.deadline - s->requests[k.req].arrival; }
 
 // scheduler.py:331-333
-static void live_ready(const S* s, std::vector<int32_t>& out) {
+static void live_ready(S* s, std::vector<int32_t>& out) {
+    ready_squeeze(s);
     out.clear();
     for (int32_t slot : s->ready)
         if (!s->evicted_stream[s->kernels[slot].stream]) out.push_back(slot);
@@ -589,14 +624,15 @@ static void live_ready(const S* s, std::vector<int32_t>& out) {
 static void active_streams(S* s, std::vector<int32_t>& out) {
     std::vector<char>& seen = s->s_seen;
     seen.assign(s->stream_names.size(), 0);
-    for (int32_t slot : s->ready) seen[s->kernels[slot].stream] = 1;
+    for (int32_t slot : s->ready)
+        if (slot >= 0) seen[s->kernels[slot].stream] = 1;
     for (const DispatchRec& d : s->pool)
         if (d.live)
             for (int32_t st : d.streams) seen[st] = 1;
     out.clear();
     for (size_t i = 0; i < seen.size(); ++i)
         if (seen[i] && !s->evicted_stream[i]) out.push_back((int32_t)i);
-    std::sort(out.begin(), out.end(), [s](int32_t a, int32_t b) { return s->stream_less(a, b); });
+    s->sort_streams(out);
 }
 
 // len(_active_streams()) without sorting (all the ooo step needs)
@@ -608,7 +644,8 @@ static int64_t count_active_streams(S* s) {
         if (!seen[st] && !s->evicted_stream[st]) ++n;
         seen[st] = 1;
     };
-    for (int32_t slot : s->ready) mark(s->kernels[slot].stream);
+    for (int32_t slot : s->ready)
+        if (slot >= 0) mark(s->kernels[slot].stream);
     for (const DispatchRec& d : s->pool)
         if (d.live)
             for (int32_t st : d.streams) mark(st);
@@ -658,7 +695,7 @@ static void make_dispatch(S* s, const std::vector<int32_t>& members, int64_t now
         d.streams.push_back(s->kernels[slot].stream);
         ready_remove(s, slot);
     }
-    std::sort(d.streams.begin(), d.streams.end(), [s](int32_t a, int32_t b) { return s->stream_less(a, b); });
+    s->sort_streams(d.streams);
     d.streams.erase(std::unique(d.streams.begin(), d.streams.end()), d.streams.end());
     s->v_disp.push_back(d.rec);
     s->free_sms -= alloc;
@@ -733,7 +770,7 @@ static int step_time_mux(S* s, int64_t now) {
     streams.clear();
     for (int32_t slot : live) streams.push_back(s->kernels[slot].stream);
     if (streams.empty()) return GMX_OK;
-    std::sort(streams.begin(), streams.end(), [s](int32_t a, int32_t b) { return s->stream_less(a, b); });
+    s->sort_streams(streams);
     streams.erase(std::unique(streams.begin(), streams.end()), streams.end());
     int32_t pick = streams[0];
     if (s->rr_last >= 0 && s->stream_less(s->rr_last, streams.back())) {
@@ -836,7 +873,7 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
             ShapeRec r{k.id, k.op, k.dtype, k.nd, {k.dims[0], k.dims[1], k.dims[2]}, k.flops, slot};
             recs.push_back(r);
         }
-        rc = cluster_shapes(recs, s->params.pad_budget, s->s_order, s->s_clusters);
+        rc = cluster_shapes(recs, s->params.pad_budget, s->s_order, s->s_clusters, s->ready_by_id);
         if (rc) return rc;
         s->clustered_version = s->ready_version;
         s->s_cost_tenancy.assign(s->s_clusters.size(), -1);   // superkernel costs of the new clusters
@@ -953,6 +990,7 @@ static void unlock_dependents(S* s, int64_t done_id, const RequestRec& r, std::v
 // blocked and in-flight kernels of unfinished requests), so they are unchanged; what changes is
 // that finished kernels can no longer be queried by id and kernel ids must not be reused.
 static void compact(S* s) {
+    ready_squeeze(s);   // before the kernel records (and their ready positions) are copied
     std::vector<int32_t> kmap(s->kernels.size(), -1);
     std::vector<KernelRec> nk;
     std::vector<RequestRec> nr;
@@ -1384,7 +1422,7 @@ int gmx_sched_find_stragglers(gmx_sched* s, int32_t* out_streams, int32_t cap, i
     order.clear();
     for (int32_t st = 0; st < (int32_t)s->has_win.size(); ++st)
         if (s->has_win[st] && s->win_above[st] > 0 && !s->evicted_stream[st]) order.push_back(st);
-    std::sort(order.begin(), order.end(), [s](int32_t a, int32_t b) { return s->stream_less(a, b); });
+    s->sort_streams(order);
     int32_t n = 0;
     for (int32_t st : order) {
         const int64_t len = (int64_t)s->ratio_win[st].size();
@@ -1399,7 +1437,7 @@ int gmx_sched_find_stragglers(gmx_sched* s, int32_t* out_streams, int32_t cap, i
     return GMX_OK;
 }
 
-int32_t gmx_sched_ready_count(const gmx_sched* s) { return s ? (int32_t)s->ready.size() : 0; }
+int32_t gmx_sched_ready_count(const gmx_sched* s) { return s ? s->n_ready : 0; }
 
 int gmx_sched_set_retire(gmx_sched* s, int32_t on) {
     if (!s) return fail(GMX_EINVAL, "null argument");
@@ -1483,7 +1521,7 @@ int gmx_sched_set_free_sms(gmx_sched* s, int64_t v) {
 
 int gmx_sched_num_ready(const gmx_sched* s, int64_t* out) {
     if (!s || !out) return fail(GMX_EINVAL, "null argument");
-    *out = (int64_t)s->ready.size();
+    *out = (int64_t)s->n_ready;
     return GMX_OK;
 }
 

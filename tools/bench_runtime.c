@@ -2,7 +2,7 @@
  * bench.py timed region without the GPU: 16 tenants x 1 request per round, then
  * gmx_runtime_run over the rounds (arrivals -> add_request -> step -> complete ...).
  *
- *   bench_runtime [rounds=700] [reps=1] [window=0]
+ *   bench_runtime [rounds=700] [reps=1] [window=0] [tenants=16]
  *
  * window 0: every round submitted up front, one run over all of them (large id tables);
  * window W: like bench.py's serving loop, W rounds are submitted, then run, and so on (only the
@@ -17,7 +17,7 @@ static const int64_t SH[13][3] = {{64,3136,147},{64,3136,64},{64,3136,576},{256,
   {128,784,1152},{512,784,128},{256,196,512},{256,196,2304},{1024,196,256},{512,49,1024},{512,49,4608},{2048,49,512}};
 static double now_us(void) { struct timespec t; clock_gettime(CLOCK_MONOTONIC, &t); return t.tv_sec * 1e6 + t.tv_nsec / 1e3; }
 
-static const int tenants = 16;
+static int tenants = 16;   /* C2; 512 = C5 */
 static const int64_t RNS = 1000000, SLO = 10000000;
 
 static int submit_rounds(gmx_runtime* rt, const int32_t* codes, int r0, int r1) {
@@ -38,6 +38,8 @@ int main(int argc, char** argv) {
     const int rounds = argc > 1 ? atoi(argv[1]) : 700;
     const int reps = argc > 2 ? atoi(argv[2]) : 1;   /* fresh runtime per repetition (profiling) */
     const int window = argc > 3 ? atoi(argv[3]) : 0;
+    if (argc > 4) tenants = atoi(argv[4]);
+    if (tenants < 1 || tenants > 4096) return 1;
     const int warm = 200;
     double best = 1e30;
     for (int rep = 0; rep < reps; ++rep) {
@@ -46,7 +48,7 @@ int main(int argc, char** argv) {
     gmx_sched* s;
     if (gmx_sched_create(&p, GMX_POLICY_OOO, &pp, NULL, 0.6, 0.4, 0, &s)) return 1;
     gmx_sched_set_retire(s, 1);
-    int32_t codes[64];
+    static int32_t codes[4096];
     char name[32];
     for (int i = 0; i < tenants; ++i) { snprintf(name, sizeof name, "t%03d", i); gmx_sched_intern_stream(s, name, &codes[i]); }
     gmx_runtime* rt;
