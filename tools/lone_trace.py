@@ -70,3 +70,17 @@ for c in pick:
               f" {r_(it['t_prod'])} {r_(it['t_mma_done'])} {r_(it['t_epi'])} {r_(it['t_end'])}"
               + (f" | reduced {r_(it['t_e_start'])} ticket {r_(it['t_e_staged'])} finalized {r_(it['t_e_bar'])}"
                  if it['nsplit'] > 1 else ""))
+
+# epilogue phases of the unsplit tiles (first pass of each): epi start -> staging free + barrier
+# -> chunks staged -> fence + barrier -> TMA stores issued -> item end (all warps done)
+ph = {k: [] for k in ("wait", "stage", "bar", "issue", "tail")}
+for it in items:
+    if it["nsplit"] > 1 or it["type"] & 0x3f != 0 or not (it["t_e_start"] and it["t_e_issued"] and it["t_epi"]):
+        continue
+    ph["wait"].append(it["t_e_start"] - it["t_epi"])
+    ph["stage"].append(it["t_e_staged"] - it["t_e_start"])
+    ph["bar"].append(it["t_e_bar"] - it["t_e_staged"])
+    ph["issue"].append(it["t_e_issued"] - it["t_e_bar"])
+    ph["tail"].append(it["t_end"] - it["t_e_issued"])
+print("\nunsplit tile epilogue phases (us, median / p90 over", len(ph["wait"]), "tiles):",
+      {k: (round(statistics.median(v) / 1e3, 3), round(sorted(v)[int(0.9 * len(v))] / 1e3, 3)) for k, v in ph.items() if v})
