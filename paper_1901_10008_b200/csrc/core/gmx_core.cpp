@@ -497,7 +497,7 @@ struct gmx_sched {
     int64_t free_sms;
     int64_t dispatch_seq = 0;
     bool has_last_ctx = false;
-    std::string last_ctx;
+    int32_t last_ctx = -2;   // context of the last dispatch: a stream index, or -2 for "jit"
     int32_t rr_last = -1;
     gmx::SigSet withheld_sigs;
     // retire mode (serving loops): finished requests are dropped from the tables once they
@@ -526,6 +526,12 @@ struct gmx_sched {
                                               // signature is known to be in withheld_sigs
     std::vector<int64_t> s_slack, s_sig, s_wakeups;
     std::vector<char> s_seen;
+    // compact() scratch (capacity kept across compactions: no regrowth of the tables)
+    std::vector<gmx::KernelRec> c_kernels;
+    std::vector<gmx::RequestRec> c_requests;
+    std::vector<int64_t> c_deps;
+    std::vector<int32_t> c_kmap;
+    std::vector<char> c_in_flight;
 
     const gmx_tuning_table* tbl() const { return has_table ? &table : nullptr; }
     int32_t rank(int32_t st) {
@@ -661,7 +667,7 @@ static double noise_factor(S* s) {
 
 // scheduler.py:294-316
 static void make_dispatch(S* s, const std::vector<int32_t>& members, int64_t now, int64_t duration,
-                          int64_t predicted, int64_t alloc, int32_t context, const char* ctx_name,
+                          int64_t predicted, int64_t alloc, int32_t context,
                           bool ctx_switch, bool is_super, int64_t useful, int64_t padded, bool infeasible) {
     int32_t pi;
     if (!s->pool_free.empty()) {
@@ -700,7 +706,7 @@ static void make_dispatch(S* s, const std::vector<int32_t>& members, int64_t now
     s->v_disp.push_back(d.rec);
     s->free_sms -= alloc;
     s->has_last_ctx = true;
-    if (s->last_ctx != ctx_name) s->last_ctx = ctx_name;
+    s->last_ctx = context;
     s->inflight_slot.put(d.rec.dispatch_id, pi);
     ++s->n_inflight;
 }
@@ -744,8 +750,7 @@ static int step_serial(S* s, int64_t now, bool by_deadline) {
     const int64_t dur = py_ceil((double)pred * noise_factor(s));
     const bool inf = kernel_slack(s, k, now) < 0;
     s->s_members.assign(1, best);
-    make_dispatch(s, s->s_members, now, dur, pred, s->prof.sm_count, k.stream,
-                  s->stream_names[k.stream].c_str(), false, false, k.flops, k.flops, inf);
+    make_dispatch(s, s->s_members, now, dur, pred, s->prof.sm_count, k.stream, false, false, k.flops, k.flops, inf);
     return GMX_OK;
 }
 
@@ -785,10 +790,12 @@ static int step_time_mux(S* s, int64_t now) {
     if (rc) return rc;
     const int64_t dur = py_ceil((double)pred * noise_factor(s));
     const std::string& name = s->stream_names[pick];
-    const bool sw = s->has_last_ctx && s->last_ctx != name;
+    // context switch iff the last context's name differs (names are unique per stream; the
+    // coalesced context is named "jit")
+    const bool sw = s->has_last_ctx && !(s->last_ctx == pick || (s->last_ctx == GMX_CONTEXT_JIT && name == "jit"));
     const bool inf = kernel_slack(s, k, now) < 0;
     s->s_members.assign(1, slot);
-    make_dispatch(s, s->s_members, now, dur, pred, s->prof.sm_count, pick, name.c_str(), sw, false,
+    make_dispatch(s, s->s_members, now, dur, pred, s->prof.sm_count, pick, sw, false,
                   k.flops, k.flops, inf);
     return GMX_OK;
 }
@@ -841,17 +848,17 @@ static int step_space_mux(S* s, int64_t now) {
         const int64_t dur = py_ceil((double)base * factor * noise_factor(s));
         const bool inf = kernel_slack(s, k, now) < 0;
         s->s_members.assign(1, slot);
-        make_dispatch(s, s->s_members, now, dur, base, alloc, st, s->stream_names[st].c_str(), false, false,
+        make_dispatch(s, s->s_members, now, dur, base, alloc, st, false, false,
                       k.flops, k.flops, inf);
     }
     return GMX_OK;
 }
 
-struct Scored {
-    int32_t infeasible_rank;   // 0 if any member late
+struct Scored {                // 24 bytes: cheap to move in the sort
     int64_t earliest_deadline;
     int64_t min_id;
     int32_t cluster;
+    int16_t infeasible_rank;   // 0 if any member late
     bool late;
 };
 
@@ -888,7 +895,7 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
     static thread_local std::vector<Scored> scored;
     scored.clear();
     for (int32_t c = 0; c < (int32_t)clusters.size(); ++c) {
-        Scored sc{1, INT64_MAX, INT64_MAX, c, false};
+        Scored sc{INT64_MAX, INT64_MAX, c, 1, false};
         for (int32_t i = clusters[c].begin; i < clusters[c].end; ++i) {
             const KernelRec& k = s->kernels[recs[order[i]].src];
             slack[order[i]] = kernel_slack(s, k, now);
@@ -956,7 +963,7 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
         const int64_t alloc = std::min<int64_t>(s->prof.sm_count, ceil_ratio(cost.block_count, s->prof.blocks_per_sm));
         if (s->free_sms < alloc) continue;
         const int64_t dur = py_ceil((double)cost.duration * noise_factor(s));
-        make_dispatch(s, members, now, dur, cost.duration, alloc, GMX_CONTEXT_JIT, "jit", false, true,
+        make_dispatch(s, members, now, dur, cost.duration, alloc, GMX_CONTEXT_JIT, false, true,
                       useful_of(s, members), cost.flops, sc.late);
     }
     return GMX_OK;
@@ -991,14 +998,18 @@ static void unlock_dependents(S* s, int64_t done_id, const RequestRec& r, std::v
 // that finished kernels can no longer be queried by id and kernel ids must not be reused.
 static void compact(S* s) {
     ready_squeeze(s);   // before the kernel records (and their ready positions) are copied
-    std::vector<int32_t> kmap(s->kernels.size(), -1);
-    std::vector<KernelRec> nk;
-    std::vector<RequestRec> nr;
-    std::vector<int64_t> nd;
-    nk.reserve(s->kernels.size() / 2 + 16);
+    std::vector<int32_t>& kmap = s->c_kmap;
+    kmap.assign(s->kernels.size(), -1);
+    std::vector<KernelRec>& nk = s->c_kernels;
+    std::vector<RequestRec>& nr = s->c_requests;
+    std::vector<int64_t>& nd = s->c_deps;
+    nk.clear();
+    nr.clear();
+    nd.clear();
     // evicted requests are dropped too, unless one of their kernels is still in a live
     // (multi-stream) dispatch: nothing else can reference them again
-    std::vector<char> in_flight(s->kernels.size(), 0);
+    std::vector<char>& in_flight = s->c_in_flight;
+    in_flight.assign(s->kernels.size(), 0);
     for (const DispatchRec& d : s->pool)
         if (d.live)
             for (int32_t slot : d.kernels) in_flight[slot] = 1;

@@ -59,7 +59,21 @@ struct gmx_runtime {
     // Arrivals submitted in (time, id) order — the common case, requests are queued ahead —
     // wait in a FIFO instead of the heap, which then only holds completions and wakeups; an
     // out-of-order arrival goes to the heap. The event order is unchanged (merge of the two).
-    std::deque<Event> arrivals;
+    // FIFO as a vector + head (no chunk allocation per push/pop; reset whenever it drains)
+    struct Fifo {
+        std::vector<Event> v;
+        size_t head = 0;
+        bool empty() const { return head == v.size(); }
+        const Event& front() const { return v[head]; }
+        const Event& back() const { return v.back(); }
+        void push_back(const Event& e) {
+            if (empty()) { v.clear(); head = 0; }
+            v.push_back(e);
+        }
+        void pop_front() {
+            if (++head == v.size()) { v.clear(); head = 0; }
+        }
+    } arrivals;
     std::vector<Pending> pool;
     std::vector<int32_t> pool_free;
     gmx::IdMap req_index;                 // request id -> pool index (until the request finishes)
