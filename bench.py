@@ -678,6 +678,9 @@ def run_ours(args, world, rank):
     total_tenants = args.tenants or N_TENANTS * world
     tenants = my_tenants(total_tenants, rank, world)
     bench = C2Bench(replicas_for(tenants, args.replicas), tuning=args.tuning, tenants=tenants)
+    for kv in args.exec_opt:
+        k, v = kv.split("=")
+        bench.ex.set_option(k, int(v))
     shapes = bench.shapes
     flops_round = useful_flops(shapes)
     args.replicas = bench.replicas
@@ -1008,6 +1011,8 @@ def main():
     ap.add_argument("--quick", action="store_true", help="skip comparators and CPU baseline")
     ap.add_argument("--tuning", default=None,
                     help="measured TuningTable JSON (tools/autotune.py) for decisions and tiles")
+    ap.add_argument("--exec-opt", action="append", default=[], metavar="K=V",
+                    help="executor option (gmx_exec_set_option), repeatable; experiments only")
     ap.add_argument("--launch-per-step", action="store_true",
                     help="one kernel launch per scheduler step instead of the resident executor")
     args = ap.parse_args()

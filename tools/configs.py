@@ -45,11 +45,21 @@ def build_streams(config):
     raise ValueError(config)
 
 
+def replicas_for(streams, requested=None):
+    """Operand replicas rotated over the rounds: like bench.py, enough that they exceed 4x the
+    126 MB L2 (every round reads cold operands from HBM), 2..16."""
+    if requested:
+        return requested
+    per_round = sum(gm.KernelSpec(0, sid, p["op_kind"], tuple(p["dims"]), p["dtype"]).bytes
+                    for sid, protos in streams for p in protos)
+    return max(2, min(16, -(-504_000_000 // per_round)))
+
+
 class ConfigRun:
-    def __init__(self, config, replicas=2):
+    def __init__(self, config, replicas=None):
         self.ex = Executor()
         self.streams = build_streams(config)
-        self.replicas = replicas
+        self.replicas = replicas = replicas_for(self.streams, replicas)
         # operands per (replica, stream, layer); layers of a chain use distinct buffers
         self.slots = []
         self.useful = 0
@@ -130,7 +140,7 @@ class ConfigRun:
                 "us_per_launch": sec / max(1, st["launches"] - before["launches"]) * 1e6,
                 "slo_misses_virtual": st["slo_misses"] - before["slo_misses"],
                 "algorithmic_gb_per_s": self.bytes * rounds / sec / 1e9,
-                "streams": len(self.streams),
+                "streams": len(self.streams), "replicas": self.replicas,
                 "kernels_per_round": sum(len(p) for _, p in self.streams)}
 
 
@@ -141,12 +151,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--resident", action="store_true", help="run the steps through the resident executor")
     ap.add_argument("--exec-lib", default=None, help="A/B runs: another build of libgmx_exec.so")
+    ap.add_argument("--replicas", type=int, default=0,
+                    help="operand replicas (0: enough to exceed 4x L2, like bench.py)")
     args = ap.parse_args()
     if args.exec_lib:
         from paper_1901_10008_b200 import executor
         executor.exec_lib(args.exec_lib)
     for cfg in args.configs.split(","):
-        run = ConfigRun(cfg)
+        run = ConfigRun(cfg, args.replicas or None)
         res = run.run(args.rounds, args.warmup, args.resident)
         res["config"] = cfg
         print(json.dumps(res), flush=True)
