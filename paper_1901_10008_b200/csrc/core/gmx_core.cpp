@@ -275,18 +275,39 @@ static double waste_ratio(u128 sum, int64_t count, int64_t padded_flops) {
     return 1.0 - true_div(sum, den);
 }
 
+// Scratch of the coalescer (no allocation after warm-up) and its memo of greedy results. The
+// scheduler owns one (no thread-local lookups on its hot path); the stateless ABI uses a
+// thread-local one. A memo entry may also carry the superkernel costs of its clusters at one
+// tenancy (set and used by the scheduler that owns the scratch: costs depend on its profile).
+struct ClusterMemo {
+    std::vector<int64_t> key;
+    std::vector<int32_t> pos;          // member positions (into idx) in output order
+    std::vector<Cluster> clusters;
+    std::vector<gmx_cost> costs;       // per cluster, valid when cost_tenancy >= 0
+    int64_t cost_tenancy = -1;
+};
+struct ClusterScratch {
+    std::vector<int32_t> idx, gid, gfirst, gcount, gorder, slot_of_group, htab, fill, posv;
+    std::vector<char> taken;
+    std::vector<int64_t> mkey;
+    std::unordered_map<uint64_t, std::vector<ClusterMemo>> memo;
+    ClusterMemo* last = nullptr;       // the entry the last call hit or created
+};
+
 // coalesce.py:69-106. `order` receives member indices (into recs) grouped by
 // cluster in admission order.
 // `by_id`: recs are already in ascending id order (the scheduler's ready set usually is), so
 // the stable placement into shape groups leaves every group id-sorted.
 static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vector<int32_t>& order,
-                          std::vector<Cluster>& clusters, bool by_id = false) {
+                          std::vector<Cluster>& clusters, ClusterScratch& sc, bool by_id = false) {
+    sc.last = nullptr;
     if (!(budget >= 0.0 && budget < 1.0)) return fail(GMX_EINVAL, "pad_budget must be in [0, 1)");
     const int32_t n = (int32_t)recs.size();
-    static thread_local std::vector<int32_t> idx;   // scratch: no allocation after warm-up
-    static thread_local std::vector<char> taken;
-    static thread_local std::vector<int32_t> gid, gfirst, gcount, gorder, slot_of_group;
-    static thread_local std::vector<int32_t> htab;
+    std::vector<int32_t>& idx = sc.idx;
+    std::vector<char>& taken = sc.taken;
+    std::vector<int32_t>&gid = sc.gid, &gfirst = sc.gfirst, &gcount = sc.gcount, &gorder = sc.gorder,
+                         &slot_of_group = sc.slot_of_group;
+    std::vector<int32_t>& htab = sc.htab;
     // Sort order (op, dtype, dims descending, id) built in two levels: kernels are grouped by
     // identical shape (exact-key hash table), only the distinct shapes are comparison-sorted,
     // and ids are sorted within each shape group — same order as one global sort, far fewer
@@ -334,7 +355,7 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
     }
     idx.resize(n);
     {
-        static thread_local std::vector<int32_t> fill;
+        std::vector<int32_t>& fill = sc.fill;
         fill.assign(slot_of_group.begin(), slot_of_group.end());
         for (int32_t i = 0; i < n; ++i) idx[fill[gid[i]]++] = i;
     }
@@ -346,13 +367,8 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
     // The greedy below depends only on the sorted sequence of (shape, multiplicity): members of
     // one shape group are interchangeable and taken in id order. Serving rounds repeat the same
     // shape mix, so the result is memoized as positions into idx (per thread, bounded).
-    struct Memo {
-        std::vector<int64_t> key;
-        std::vector<int32_t> pos;          // member positions (into idx) in output order
-        std::vector<Cluster> clusters;
-    };
-    static thread_local std::unordered_map<uint64_t, std::vector<Memo>> memo;
-    static thread_local std::vector<int64_t> mkey;
+    auto& memo = sc.memo;
+    std::vector<int64_t>& mkey = sc.mkey;
     mkey.clear();
     uint64_t mh;
     {
@@ -371,15 +387,16 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
         mh = hash_seq(0x243F6A8885A308D3ull, mkey.data(), mkey.size());
         auto it = memo.find(mh);
         if (it != memo.end())
-            for (const Memo& m : it->second)
+            for (ClusterMemo& m : it->second)
                 if (m.key == mkey) {
                     order.resize(m.pos.size());
                     for (size_t q = 0; q < m.pos.size(); ++q) order[q] = idx[m.pos[q]];
                     clusters = m.clusters;
+                    sc.last = &m;
                     return GMX_OK;
                 }
     }
-    static thread_local std::vector<int32_t> posv;   // positions of `order` entries
+    std::vector<int32_t>& posv = sc.posv;   // positions of `order` entries
     posv.clear();
     taken.assign(n, 0);
     order.clear();
@@ -421,7 +438,9 @@ static int cluster_shapes(std::vector<ShapeRec>& recs, double budget, std::vecto
         clusters.push_back(c);
     }
     if (memo.size() > 4096) memo.clear();
-    memo[mh].push_back(Memo{mkey, posv, clusters});
+    auto& bucket = memo[mh];
+    bucket.push_back(ClusterMemo{mkey, posv, clusters, {}, -1});
+    sc.last = &bucket.back();
     return GMX_OK;
 }
 
@@ -450,6 +469,14 @@ struct RequestRec {
     int32_t first, count;   // kernel slots [first, first + count) in request order
     int64_t remaining;      // distinct kernel ids not yet completed
     bool evicted, finished;
+};
+
+struct Scored {                // 24 bytes: cheap to move in the sort
+    int64_t earliest_deadline;
+    int64_t min_id;
+    int32_t cluster;
+    int16_t infeasible_rank;   // 0 if any member late
+    bool late;
 };
 
 struct DispatchRec {
@@ -517,6 +544,9 @@ struct gmx_sched {
     std::vector<int32_t> v_held_off;
     // scratch
     std::vector<gmx::ShapeRec> s_recs;
+    gmx::ClusterScratch cscratch;             // coalescer scratch + memo (costs cached per entry)
+    gmx::ClusterMemo* s_memo = nullptr;       // memo entry of the cached clustering
+    std::vector<gmx::Scored> s_scored;
     std::vector<int32_t> s_order, s_live, s_act, s_members, s_tmp;
     std::vector<gmx::Cluster> s_clusters;
     gmx::CostMemo solo_memo, super_memo;      // pure cost functions, memoized per shape
@@ -854,14 +884,6 @@ static int step_space_mux(S* s, int64_t now) {
     return GMX_OK;
 }
 
-struct Scored {                // 24 bytes: cheap to move in the sort
-    int64_t earliest_deadline;
-    int64_t min_id;
-    int32_t cluster;
-    int16_t infeasible_rank;   // 0 if any member late
-    bool late;
-};
-
 // scheduler.py:414-471
 static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
     std::vector<int32_t>& live = s->s_live;
@@ -880,19 +902,27 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
             ShapeRec r{k.id, k.op, k.dtype, k.nd, {k.dims[0], k.dims[1], k.dims[2]}, k.flops, slot};
             recs.push_back(r);
         }
-        rc = cluster_shapes(recs, s->params.pad_budget, s->s_order, s->s_clusters, s->ready_by_id);
+        rc = cluster_shapes(recs, s->params.pad_budget, s->s_order, s->s_clusters, s->cscratch, s->ready_by_id);
         if (rc) return rc;
         s->clustered_version = s->ready_version;
-        s->s_cost_tenancy.assign(s->s_clusters.size(), -1);   // superkernel costs of the new clusters
+        s->s_memo = s->cscratch.last;
         s->s_sig_seen.assign(s->s_clusters.size(), 0);
-        s->s_costs.resize(s->s_clusters.size());
+        // superkernel costs of the new clusters: from the memo entry when it holds them for this
+        // tenancy (a recurring composition), else computed below
+        if (s->s_memo && s->s_memo->cost_tenancy >= 0 && s->s_memo->costs.size() == s->s_clusters.size()) {
+            s->s_costs = s->s_memo->costs;
+            s->s_cost_tenancy.assign(s->s_clusters.size(), s->s_memo->cost_tenancy);
+        } else {
+            s->s_cost_tenancy.assign(s->s_clusters.size(), -1);
+            s->s_costs.resize(s->s_clusters.size());
+        }
     }
     const auto& order = s->s_order;
     const auto& clusters = s->s_clusters;
 
     std::vector<int64_t>& slack = s->s_slack;
     slack.assign(recs.size(), 0);
-    static thread_local std::vector<Scored> scored;
+    std::vector<Scored>& scored = s->s_scored;
     scored.clear();
     for (int32_t c = 0; c < (int32_t)clusters.size(); ++c) {
         Scored sc{INT64_MAX, INT64_MAX, c, 1, false};
@@ -965,6 +995,13 @@ static int step_ooo(S* s, int64_t now, std::vector<int64_t>& wakeups) {
         const int64_t dur = py_ceil((double)cost.duration * noise_factor(s));
         make_dispatch(s, members, now, dur, cost.duration, alloc, GMX_CONTEXT_JIT, false, true,
                       useful_of(s, members), cost.flops, sc.late);
+    }
+    // every cluster's cost is now known at this tenancy: keep them with the memo entry, so the
+    // next sighting of the same composition skips the cost lookups
+    if (s->s_memo && s->s_memo->cost_tenancy != tenancy &&
+        std::all_of(s->s_cost_tenancy.begin(), s->s_cost_tenancy.end(), [&](int64_t t) { return t == tenancy; })) {
+        s->s_memo->costs = s->s_costs;
+        s->s_memo->cost_tenancy = tenancy;
     }
     return GMX_OK;
 }
@@ -1163,7 +1200,8 @@ int gmx_cluster_shapes(const gmx_kernel_desc* pending, int32_t n, double budget,
     }
     std::vector<int32_t> order;
     std::vector<Cluster> clusters;
-    int rc = cluster_shapes(recs, budget, order, clusters);
+    static thread_local ClusterScratch scratch;
+    int rc = cluster_shapes(recs, budget, order, clusters, scratch);
     if (rc) return rc;
     for (size_t i = 0; i < order.size(); ++i) out_members[i] = recs[order[i]].src;
     for (size_t c = 0; c < clusters.size(); ++c) {
