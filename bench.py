@@ -754,10 +754,12 @@ def run_ours(args, world, rank):
     # set-up of the cooperative launch, a cold serving path), later ones do not.
     first = args.warmup
     prewarm = 0
-    rehearsals = []
+    rehearsals, rehearsal_host = [], []
     while prewarm < max(args.replicas, args.prewarm_rounds) or len(rehearsals) < 3:
         n = max(1, min(args.steps, 32))
-        rehearsals.append(round(window(first, n)[0] * 1e6 / n, 3))
+        w = window(first, n)
+        rehearsals.append(round(w[0] * 1e6 / n, 3))
+        rehearsal_host.append(w[3]["serving_loop_per_round"])
         first += n
         prewarm += n
     bench.next_round = first
@@ -852,6 +854,7 @@ def run_ours(args, world, rank):
         "host_core": host_core,
         "host_us": host_us,
         "rehearsal_us_per_round": rehearsals,
+        "rehearsal_host_loop_us_per_round": rehearsal_host,
         "executor": "launch per step" if args.launch_per_step else
                     "resident (one persistent launch; steps queued through pinned host ring)",
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],

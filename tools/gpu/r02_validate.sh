@@ -1,0 +1,6 @@
+# re-entry validation of HEAD: GPU tests, smoke, driver bench command x2, reference arm
+set -x
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/val_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/val_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/val_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/val_smoke.log
+for i in 1 2; do timeout 300 python bench.py --gpus 1 --steps 20 --warmup 5 >> gpurun_out/val_bench.jsonl 2>>gpurun_out/val_bench_err.txt; done
+timeout 300 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 >> gpurun_out/val_bench_ref.jsonl 2>>gpurun_out/val_bench_err.txt
