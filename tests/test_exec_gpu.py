@@ -7,6 +7,8 @@ Tolerances (stated in oracle/numerics.py):
   fp32 GEMM operands (tf32 UMMA) vs float64 on the UNROUNDED fp32 operands: <= 5e-3*max|ref| + 1e-6
 """
 
+import time
+
 import numpy as np
 import pytest
 import torch
@@ -315,6 +317,50 @@ def test_resident_queue_matches_launches(ex):
     for row in slots:
         for sl in row:
             ex.unregister(sl)
+
+
+@pytest.mark.parametrize("pct", [0, 100, 200])
+def test_resident_idle_device_latency_plan(ex, pct):
+    """A resident step published while nothing earlier is in flight takes its slot set's latency
+    plan (split_pct_idle; 0 = the resident throughput plan): lone steps, each waited for, then a
+    burst (throughput plans) over the same slots; every result correct, and the latency plan
+    splits finer than the throughput plan."""
+    from paper_1901_10008_b200.executor import OperandSet
+    sets = [[OperandSet("gemm", C2_SHAPES[(i + r) % 13], seed=900 + 16 * r + i) for i in range(16)] for r in range(2)]
+    slots = [[o.register(ex) for o in row] for row in sets]
+    s = torch.cuda.Stream()
+    ex.set_option("split_pct_idle", pct)
+    try:
+        ex.clear_plans()
+        with torch.cuda.stream(s):
+            with ex.resident(s):
+                for k in range(4):   # lone: the device is idle when each step is published
+                    seq = ex.launch(slots[k % 2], s, independent=True)
+                    lone = ex.last_plan()
+                    t0 = time.perf_counter()
+                    while not ex.resident_step_done(seq):
+                        assert time.perf_counter() - t0 < 5.0, "resident step did not complete"
+            s.synchronize()
+            ex.resident_begin(s, hold=True)   # burst: held, so every later step queues behind the first
+            for k in range(6):
+                ex.launch(slots[k % 2], s, independent=True)
+            burst = ex.last_plan()
+            ex.resident_release()
+            ex.resident_end()
+            s.synchronize()
+        for row in sets:
+            for o in row:
+                _check(o)
+        if pct == 0:
+            assert lone["n_split_items"] == burst["n_split_items"]
+        else:
+            assert lone["n_split_items"] > burst["n_split_items"]
+            assert lone["max_cta_cost"] < burst["max_cta_cost"]
+    finally:
+        ex.set_option("split_pct_idle", 200)
+        for row in slots:
+            for sl in row:
+                ex.unregister(sl)
 
 
 def test_resident_many_steps_ring_wrap(ex):
