@@ -154,9 +154,10 @@ class ClockSampler:
         "pynvml.nvmlInit(); h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1])); per = float(sys.argv[2])\n"
         "print('max', pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)\n"
         "while True:\n"
+        "    t = time.perf_counter()\n"
         "    c = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)\n"
         "    m = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)\n"
-        "    print(c, m, flush=True)\n"
+        "    print(c, m, round((time.perf_counter() - t) * 1e3, 3), flush=True)\n"
         "    time.sleep(per)\n")
 
     def __init__(self, device_index, period_s=0.2, avoid_core=None, allowed=None):
@@ -222,8 +223,9 @@ class ClockSampler:
             if f and f[0] == "max":
                 self.max_mhz = int(f[1])
         body = [f for f in self._lines[getattr(self, "_mark", 0) - 1 if getattr(self, "_mark", 0) else 0:]
-                if len(f) == 2 and f[0] != "max"]
-        for c, m in body:
+                if len(f) == 3 and f[0] != "max"]
+        self.query_ms = [float(f[2]) for f in self._lines if len(f) == 3 and f[0] != "max"]
+        for c, m, _ in body:
             self.samples.append(int(c))
             for name, bit in self.REASONS.items():
                 if int(m) & bit:
@@ -232,8 +234,10 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        q = getattr(self, "query_ms", [])
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "nvml_query_ms": {"median": round(statistics.median(q), 3), "max": round(max(q), 3)} if q else None}
 
 
 # ---------------------------------------------------------------- our arm
