@@ -636,6 +636,14 @@ def idlest_core(pool, window_s=0.2):
     return min(pool, key=lambda c: (b.get(c, 0) - a.get(c, 0), c))
 
 
+def rank_core_pool(pool, local_rank, local_world):
+    """The cores of `pool` this node-local rank may pin its serving loop to: every
+    local_world-th one, so the ranks of one node never share a serving core."""
+    if local_world <= 1:
+        return list(pool)
+    return [c for i, c in enumerate(pool) if i % local_world == local_rank % local_world] or list(pool)
+
+
 def pin_serving_thread(device_index):
     """Pin the calling (serving-loop) thread to one core: the native runtime is a single-threaded
     event loop, and migrations / a shared core add run-to-run noise. The core is taken from the
@@ -654,6 +662,9 @@ def pin_serving_thread(device_index):
     except Exception:  # noqa: BLE001 — fall back to the allowed set
         local = []
     pool = [c for c in (local or cpus) if c != 0] or cpus
+    # one serving loop per rank: ranks of one node take disjoint cores (every L-th core of the
+    # NUMA-local pool), or every rank's idlest-core pick lands on the same core
+    pool = rank_core_pool(pool, int(os.environ.get("LOCAL_RANK", "0")), int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
     core = idlest_core(pool)
     forced = os.environ.get("GMX_HOST_CORE")   # experiments: a fixed core, or -1 = no pinning
     if forced is not None:

@@ -43,3 +43,16 @@ def test_bench_partitions_a_fixed_tenant_set():
     got = sorted(t for r in line["ranks"] for t in r["tenants"])
     assert got == [f"t{i:02d}" for i in range(48)]
     assert all(len(r["tenants"]) == 24 for r in line["ranks"])
+
+
+def test_rank_core_pools_are_disjoint():
+    """Node-local ranks pin their serving loops to disjoint cores (bench.pin_serving_thread)."""
+    import bench
+    pool = list(range(1, 16))
+    for lw in (1, 2, 4, 8):
+        pools = [set(bench.rank_core_pool(pool, r, lw)) for r in range(lw)]
+        assert set().union(*pools) == set(pool)
+        for i in range(lw):
+            assert pools[i]
+            for j in range(i):
+                assert not pools[i] & pools[j]
